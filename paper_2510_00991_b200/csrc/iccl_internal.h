@@ -1,0 +1,108 @@
+// Internal declarations shared by the runtime, the host arithmetic and the
+// kernels of libiccl_b200.so.  Not part of the ABI (see include/iccl_b200.h).
+#pragma once
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include <cuda.h>
+#include <cuda_runtime_api.h>
+
+#include "iccl_b200.h"
+
+namespace iccl {
+
+// Thread-local detailed message for iccl_get_last_error.
+void set_last_error(const std::string& msg);
+const char* last_error();
+
+#define ICCL_CHECK_CUDA(expr)                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess) {                                                               \
+      ::iccl::set_last_error(std::string(#expr) + ": " + cudaGetErrorString(e_) + " at " + \
+                             __FILE__ + ":" + std::to_string(__LINE__));                   \
+      return ICCL_ERR_CUDA;                                                                \
+    }                                                                                      \
+  } while (0)
+
+#define ICCL_CHECK_CU(expr)                                                                 \
+  do {                                                                                      \
+    CUresult r_ = (expr);                                                                   \
+    if (r_ != CUDA_SUCCESS) {                                                               \
+      const char* s_ = "?";                                                                 \
+      if (::iccl::driver()) ::iccl::driver()->cuGetErrorString(r_, &s_);                    \
+      ::iccl::set_last_error(std::string(#expr) + ": " + s_ + " at " + __FILE__ + ":" +     \
+                             std::to_string(__LINE__));                                     \
+      return ICCL_ERR_CUDA;                                                                 \
+    }                                                                                       \
+  } while (0)
+
+#define ICCL_RETURN_IF(cond, code, msg)   \
+  do {                                    \
+    if (cond) {                           \
+      ::iccl::set_last_error(msg);        \
+      return code;                        \
+    }                                     \
+  } while (0)
+
+uint64_t now_ns();  // CLOCK_MONOTONIC
+
+// Monitor slot the SM copy kernel stamps with %globaltimer (K4).  Lives in
+// host-mapped pinned memory; the proxy turns it into an iccl_mon_rec_t.
+struct alignas(64) KernelStamp {
+  unsigned long long t1;        // first CTA start
+  unsigned long long t2;        // last CTA end
+  unsigned int ctas_done;       // arrival counter for the last-CTA election
+  unsigned int pad;
+};
+
+// Kernel launchers (iccl_kernels.cu).  All return cudaError_t of the launch.
+// K1: copy `bytes` from src to dst (dst may be an IPC-mapped peer pointer)
+// with at most `ctas` CTAs; TMA bulk body + vector head/tail.  `stamp` may be
+// null.
+cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, KernelStamp* stamp, cudaStream_t st);
+// Force-load every kernel (see iccl_kernels.cu: lazy loading vs parked streams).
+cudaError_t preload_kernels();
+// K4 stamp: which = 0 writes stamp->t1, which = 1 writes stamp->t2 (release).
+cudaError_t launch_stamp(KernelStamp* stamp, int which, cudaStream_t st);
+// Calibration: write %globaltimer into *out (host-mapped).
+cudaError_t launch_read_globaltimer(unsigned long long* out, cudaStream_t st);
+// K2 / K3: row gather / scatter of `row_bytes`-byte rows (MoE dispatch pack /
+// combine unpack).  dst_rows[i] <- src_rows[idx[i]]  (gather),
+// dst_rows[idx[i]] <- src_rows[i] (scatter).  Rows are 16-byte multiples.
+cudaError_t launch_gather_rows(const void* src, void* dst, const int64_t* idx, int64_t n_rows, int64_t row_bytes,
+                               int ctas, cudaStream_t st);
+cudaError_t launch_scatter_rows(const void* src, void* dst, const int64_t* idx, int64_t n_rows, int64_t row_bytes,
+                                int ctas, cudaStream_t st);
+// Fused pack + push: rows gathered by idx and written straight into up to
+// 64 destination buffers (peer-mapped), segment s covering output rows
+// [seg_start[s], seg_start[s+1]) written at dst_ptrs[s] + (i - seg_start[s]) * row_bytes.
+cudaError_t launch_gather_rows_multi(const void* src, void* const* dst_ptrs, const int64_t* seg_start, int n_seg,
+                                     const int64_t* idx, int64_t n_rows, int64_t row_bytes, int ctas,
+                                     cudaStream_t st);
+
+}  // namespace iccl
+
+namespace iccl {
+// CUDA driver entry points, resolved at first use through cudart
+// (cudaGetDriverEntryPoint) so libiccl_b200.so loads on hosts without a GPU
+// driver (the CPU test suite checks its exports there).
+struct Driver {
+  CUresult (*cuGetErrorString)(CUresult, const char**);
+  CUresult (*cuInit)(unsigned int);
+  CUresult (*cuDeviceGet)(CUdevice*, int);
+  CUresult (*cuDeviceGetAttribute)(int*, CUdevice_attribute, CUdevice);
+  CUresult (*cuStreamWriteValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+  CUresult (*cuStreamWaitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+  CUresult (*cuStreamBatchMemOp)(CUstream, unsigned int, CUstreamBatchMemOpParams*, unsigned int);
+  CUresult (*cuMemcpyDtoDAsync)(CUdeviceptr, CUdeviceptr, size_t, CUstream);
+  CUresult (*cuMemGetAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+  CUresult (*cuPointerGetAttribute)(void*, CUpointer_attribute, CUdeviceptr);
+  bool ok;
+};
+// Returns null (and sets the last error) if the driver is unavailable.
+const Driver* driver();
+}  // namespace iccl

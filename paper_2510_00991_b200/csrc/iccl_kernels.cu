@@ -1,0 +1,336 @@
+// sm_100a kernels of the ICCL B200 path.  Nothing here is a contraction, so
+// no tensor cores: these are byte movers bound by NVLink (peer destination)
+// or HBM (local destination).
+//
+// K1  iccl_copy_tma   TMA-bulk P2P copy: one elected thread per CTA streams
+//                     16 B-aligned tiles global -> smem (cp.async.bulk +
+//                     mbarrier complete_tx) -> global (cp.async.bulk
+//                     bulk_group), a ring of kStages smem stages; grid capped
+//                     at sm_cap CTAs.  Used as the backup path of the
+//                     primary-backup pair and as the SM transport.
+// K4  stamps          %globaltimer t1 at the first CTA's start and t2 at the
+//                     last CTA's end, written to a host-mapped KernelStamp
+//                     the proxy turns into a monitor record.
+// K2  gather rows     MoE dispatch pack: dst[i] = src[idx[i]] (16 B vectors),
+//                     optionally straight into several peer buffers (fused
+//                     pack + push).
+// K3  scatter rows    MoE combine unpack: dst[idx[i]] = src[i].
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "iccl_internal.h"
+
+namespace iccl {
+
+namespace {
+
+constexpr int kStages = 4;
+constexpr int kTile = 32 * 1024;  // 4 x 32 KB stages: measured best of {4x32K, 8x16K} (probes/)
+constexpr int kCopyThreads = 128;
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void stamp_begin(KernelStamp* st) {
+  if (st && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t = globaltimer();
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(&st->t1), "l"(t) : "memory");
+  }
+}
+
+// Last CTA to finish stamps t2 (system-scope release so the host sees data
+// written before it).
+__device__ __forceinline__ void stamp_end(KernelStamp* st) {
+  if (!st) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    unsigned int prev = atomicAdd_system(&st->ctas_done, 1u);
+    if (prev == gridDim.x - 1) {
+      unsigned long long t = globaltimer();
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&st->t2), "l"(t) : "memory");
+    }
+  }
+}
+
+// Byte-granular copy for heads/tails and mutually misaligned buffers.
+__device__ __forceinline__ void copy_bytes(const char* __restrict__ src, char* __restrict__ dst, size_t n,
+                                           size_t tid, size_t nthreads) {
+  for (size_t i = tid; i < n; i += nthreads) dst[i] = src[i];
+}
+
+// 16 B vector copy, grid-stride with 4 loads in flight per thread.
+__device__ __forceinline__ void copy_vec16(const int4* __restrict__ src, int4* __restrict__ dst, size_t n16,
+                                           size_t tid, size_t nthreads) {
+  size_t i = tid;
+  for (; i + 3 * nthreads < n16; i += 4 * nthreads) {
+    int4 v0, v1, v2, v3;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v0.x), "=r"(v0.y), "=r"(v0.z), "=r"(v0.w) : "l"(src + i));
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v1.x), "=r"(v1.y), "=r"(v1.z), "=r"(v1.w) : "l"(src + i + nthreads));
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v2.x), "=r"(v2.y), "=r"(v2.z), "=r"(v2.w) : "l"(src + i + 2 * nthreads));
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v3.x), "=r"(v3.y), "=r"(v3.z), "=r"(v3.w) : "l"(src + i + 3 * nthreads));
+    dst[i] = v0;
+    dst[i + nthreads] = v1;
+    dst[i + 2 * nthreads] = v2;
+    dst[i + 3 * nthreads] = v3;
+  }
+  for (; i < n16; i += nthreads) dst[i] = src[i];
+}
+
+// K1.  src/dst share the same alignment mod 16 (checked by the launcher);
+// [0, head) and [head + body, n) are copied with byte loads by warp 1..3,
+// the 16 B-aligned body by the TMA ring driven from thread 0.
+__global__ void __launch_bounds__(kCopyThreads) iccl_copy_tma(const char* __restrict__ src, char* __restrict__ dst,
+                                                              size_t head, size_t body, size_t tail,
+                                                              KernelStamp* stamp) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(8) uint64_t mbar[kStages];
+  stamp_begin(stamp);
+  // heads and tails (< 16 bytes each) by the non-elected threads of CTA 0
+  if (blockIdx.x == 0 && threadIdx.x >= 32) {
+    copy_bytes(src, dst, head, threadIdx.x - 32, blockDim.x - 32);
+    copy_bytes(src + head + body, dst + head + body, tail, threadIdx.x - 32, blockDim.x - 32);
+  }
+  if (threadIdx.x == 0 && body > 0) {
+    const char* s = src + head;
+    char* d = dst + head;
+    for (int i = 0; i < kStages; i++) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const size_t ntiles = (body + kTile - 1) / kTile;
+    const size_t first = blockIdx.x;
+    const size_t mine = first < ntiles ? (ntiles - first + gridDim.x - 1) / gridDim.x : 0;
+    auto issue_load = [&](size_t j) {
+      const size_t off = (first + j * gridDim.x) * (size_t)kTile;
+      const uint32_t bytes = (uint32_t)min((size_t)kTile, body - off);
+      const int st = (int)(j % kStages);
+      const uint32_t mb = smem_u32(&mbar[st]);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(smem + (size_t)st * kTile)),
+          "l"(s + off), "r"(bytes), "r"(mb)
+          : "memory");
+    };
+    for (size_t j = 0; j < mine && j < (size_t)kStages; j++) issue_load(j);
+    for (size_t j = 0; j < mine; j++) {
+      const int st = (int)(j % kStages);
+      const uint32_t mb = smem_u32(&mbar[st]);
+      const uint32_t parity = (uint32_t)((j / kStages) & 1);
+      uint32_t ready = 0;
+      while (!ready)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(ready)
+            : "r"(mb), "r"(parity)
+            : "memory");
+      const size_t off = (first + j * gridDim.x) * (size_t)kTile;
+      const uint32_t bytes = (uint32_t)min((size_t)kTile, body - off);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(d + off),
+                   "r"(smem_u32(smem + (size_t)st * kTile)), "r"(bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      if (j + kStages < mine) {
+        // the stage is reused once its store has read it out of smem
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        issue_load(j + kStages);
+      }
+    }
+    // all bulk stores complete (visible) before the CTA retires
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  stamp_end(stamp);
+}
+
+// Fallback for buffers whose addresses differ mod 16: byte copy.
+__global__ void __launch_bounds__(512) iccl_copy_unaligned(const char* __restrict__ src, char* __restrict__ dst,
+                                                           size_t n, KernelStamp* stamp) {
+  stamp_begin(stamp);
+  copy_bytes(src, dst, n, blockIdx.x * (size_t)blockDim.x + threadIdx.x, (size_t)gridDim.x * blockDim.x);
+  stamp_end(stamp);
+}
+
+// K4 on the copy-engine path: one thread stamps %globaltimer into the chunk's
+// host-mapped record before (which = 0) and after (which = 1) the copy.  The
+// t2 store is the chunk's WC: the proxy polls it instead of an event.
+__global__ void iccl_stamp(KernelStamp* st, int which) {
+  unsigned long long t = globaltimer();
+  if (which == 0) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(&st->t1), "l"(t) : "memory");
+  } else {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&st->t2), "l"(t) : "memory");
+  }
+}
+
+__global__ void iccl_read_globaltimer(unsigned long long* out) {
+  unsigned long long t = globaltimer();
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(out), "l"(t) : "memory");
+}
+
+// K2: one warp per row, 16 B per lane per step (coalesced 512 B per warp step).
+__global__ void __launch_bounds__(256) iccl_gather_rows(const int4* __restrict__ src, int4* __restrict__ dst,
+                                                       const int64_t* __restrict__ idx, int64_t n_rows,
+                                                       int64_t row16) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < n_rows; r += nwarps) {
+    const int4* s = src + idx[r] * row16;
+    int4* d = dst + r * row16;
+    for (int64_t c = lane; c < row16; c += 32) d[c] = s[c];
+  }
+}
+
+// K3: inverse permutation (combine unpack).
+__global__ void __launch_bounds__(256) iccl_scatter_rows(const int4* __restrict__ src, int4* __restrict__ dst,
+                                                        const int64_t* __restrict__ idx, int64_t n_rows,
+                                                        int64_t row16) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < n_rows; r += nwarps) {
+    const int4* s = src + r * row16;
+    int4* d = dst + idx[r] * row16;
+    for (int64_t c = lane; c < row16; c += 32) d[c] = s[c];
+  }
+}
+
+struct MultiDst {
+  int4* ptr[64];
+  int64_t start[65];
+};
+
+// K2 fused with the push: output row r belongs to segment s (binary search
+// over <= 64 segment starts) and lands in that segment's (peer) buffer.
+__global__ void __launch_bounds__(256) iccl_gather_rows_multi(const int4* __restrict__ src, MultiDst md, int n_seg,
+                                                             const int64_t* __restrict__ idx, int64_t n_rows,
+                                                             int64_t row16) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < n_rows; r += nwarps) {
+    int lo = 0, hi = n_seg - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (md.start[mid] <= r) lo = mid;
+      else hi = mid - 1;
+    }
+    const int4* s = src + idx[r] * row16;
+    int4* d = md.ptr[lo] + (r - md.start[lo]) * row16;
+    for (int64_t c = lane; c < row16; c += 32) d[c] = s[c];
+  }
+}
+
+bool smem_configured = false;
+
+}  // namespace
+
+cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, KernelStamp* stamp, cudaStream_t st) {
+  if (bytes == 0) return cudaSuccess;
+  const uintptr_t s = (uintptr_t)src, d = (uintptr_t)dst;
+  if (((s ^ d) & 15) != 0) {
+    int grid = (int)min((size_t)ctas, (bytes + 512 * 16 - 1) / (512 * 16));
+    if (grid < 1) grid = 1;
+    iccl_copy_unaligned<<<grid, 512, 0, st>>>((const char*)src, (char*)dst, bytes, stamp);
+    return cudaGetLastError();
+  }
+  size_t head = (16 - (s & 15)) & 15;
+  if (head > bytes) head = bytes;
+  size_t body = (bytes - head) & ~(size_t)15;
+  size_t tail = bytes - head - body;
+  if (!smem_configured) {
+    cudaError_t e = cudaFuncSetAttribute(iccl_copy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kStages * kTile);
+    if (e != cudaSuccess) return e;
+    smem_configured = true;
+  }
+  size_t ntiles = (body + kTile - 1) / kTile;
+  int grid = (int)min((size_t)ctas, ntiles > 0 ? ntiles : (size_t)1);
+  if (grid < 1) grid = 1;
+  iccl_copy_tma<<<grid, kCopyThreads, kStages * kTile, st>>>((const char*)src, (char*)dst, head, body, tail, stamp);
+  return cudaGetLastError();
+}
+
+// Load every kernel of this module now.  With CUDA lazy loading the first
+// launch of a kernel loads its module, and a load issued while one of our
+// streams is parked on a stream-memop wait blocked the launching thread on
+// B200 (probes/p2p_probe4 test 1).  The proxy must never block, so
+// iccl_comm_init_rank calls this before any wait is enqueued.
+cudaError_t preload_kernels() {
+  cudaFuncAttributes a;
+  const void* fns[] = {(const void*)iccl_copy_tma,   (const void*)iccl_copy_unaligned, (const void*)iccl_stamp,
+                       (const void*)iccl_read_globaltimer, (const void*)iccl_gather_rows,
+                       (const void*)iccl_scatter_rows, (const void*)iccl_gather_rows_multi};
+  for (const void* f : fns) {
+    cudaError_t e = cudaFuncGetAttributes(&a, f);
+    if (e != cudaSuccess) return e;
+  }
+  if (!smem_configured) {
+    cudaError_t e = cudaFuncSetAttribute(iccl_copy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kStages * kTile);
+    if (e != cudaSuccess) return e;
+    smem_configured = true;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_read_globaltimer(unsigned long long* out, cudaStream_t st) {
+  iccl_read_globaltimer<<<1, 1, 0, st>>>(out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stamp(KernelStamp* stamp, int which, cudaStream_t st) {
+  iccl_stamp<<<1, 1, 0, st>>>(stamp, which);
+  return cudaGetLastError();
+}
+
+static int rows_grid(int64_t n_rows, int ctas) {
+  int64_t warps_needed = n_rows;
+  int64_t blocks = (warps_needed + 7) / 8;
+  if (blocks > ctas) blocks = ctas;
+  return (int)(blocks < 1 ? 1 : blocks);
+}
+
+cudaError_t launch_gather_rows(const void* src, void* dst, const int64_t* idx, int64_t n_rows, int64_t row_bytes,
+                               int ctas, cudaStream_t st) {
+  if (n_rows == 0) return cudaSuccess;
+  if ((row_bytes & 15) || ((uintptr_t)src & 15) || ((uintptr_t)dst & 15)) return cudaErrorInvalidValue;
+  iccl_gather_rows<<<rows_grid(n_rows, ctas), 256, 0, st>>>((const int4*)src, (int4*)dst, idx, n_rows,
+                                                            row_bytes / 16);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_rows(const void* src, void* dst, const int64_t* idx, int64_t n_rows, int64_t row_bytes,
+                                int ctas, cudaStream_t st) {
+  if (n_rows == 0) return cudaSuccess;
+  if ((row_bytes & 15) || ((uintptr_t)src & 15) || ((uintptr_t)dst & 15)) return cudaErrorInvalidValue;
+  iccl_scatter_rows<<<rows_grid(n_rows, ctas), 256, 0, st>>>((const int4*)src, (int4*)dst, idx, n_rows,
+                                                             row_bytes / 16);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_rows_multi(const void* src, void* const* dst_ptrs, const int64_t* seg_start, int n_seg,
+                                     const int64_t* idx, int64_t n_rows, int64_t row_bytes, int ctas,
+                                     cudaStream_t st) {
+  if (n_rows == 0) return cudaSuccess;
+  if (n_seg < 1 || n_seg > 64 || (row_bytes & 15)) return cudaErrorInvalidValue;
+  MultiDst md;
+  for (int i = 0; i < n_seg; i++) {
+    md.ptr[i] = (int4*)dst_ptrs[i];
+    md.start[i] = seg_start[i];
+    if ((uintptr_t)dst_ptrs[i] & 15) return cudaErrorInvalidValue;
+  }
+  md.start[n_seg] = seg_start[n_seg];
+  iccl_gather_rows_multi<<<rows_grid(n_rows, ctas), 256, 0, st>>>((const int4*)src, md, n_seg, idx, n_rows,
+                                                                  row_bytes / 16);
+  return cudaGetLastError();
+}
+
+}  // namespace iccl

@@ -1,0 +1,1434 @@
+// ICCL B200 runtime: communicator bootstrap, the stream-ordered P2P API and
+// the per-rank proxy thread that drives the copy engines.
+//
+// Mapping of the reference design (§3.2-3.4, SPEC.md verbs /
+// transport / monitor) onto one 8xB200 NVSwitch box:
+//
+//   paper / SPEC                          here
+//   ------------------------------------  --------------------------------------------
+//   CPU proxy thread   one std::thread per communicator (proxy_loop)
+//   hostFunc #1 / #2   driver()->cuStreamWriteValue32(ready) / WaitValue(done)
+//                                         on the caller's stream: 0 SMs, no callbacks
+//   User Buffer Registration (:410-412)   IPC export of the caller's allocation, cached
+//                                         by CU_POINTER_ATTRIBUTE_BUFFER_ID
+//   CTS                     recv-posted entry in the sender's CTS ring of
+//                                         the shared control block (shm)
+//   WR post / WC        chunk copy enqueue / device-written progress
+//                                         word observed by the proxy
+//   primary QP / backup QP (:461)         copy-engine path / SM-kernel path (K1)
+//   six pointers        Xfer::next_issue (posted=transmitted),
+//                                         Xfer::completed (acked = receiver done)
+//   switch_qp           switch_path(): resume at receiver done
+//   RNIC port down         injected gate: cuStreamWaitValue32 on a host
+//                                         word placed before chunks on the primary path
+//
+// Data moves zero-copy: the sender's copy engine (or K1) writes straight into
+// the receiver's tensor through an IPC mapping — no FIFO, no staging copy
+// (PAPER.md:214-217, 240-243).
+#include <errno.h>
+#include <fcntl.h>
+#include <pthread.h>
+#include <sched.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <cstring>
+#include <deque>
+#include <mutex>
+#include <random>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "iccl_internal.h"
+
+namespace iccl {
+
+constexpr uint64_t kMagic = 0x3030324242434349ull;  // "ICCLB200"
+constexpr int kSlots = 4096;                        // op slots per rank (ready/done flags)
+constexpr int kCtsDepth = 1024;                     // recv postings in flight per ordered pair
+constexpr int kMaxRanks = 64;
+constexpr int kMaxStreams = 8;
+constexpr int kGateWords = 1024;
+constexpr int kStampSlots = 4096;
+constexpr size_t kScratchBytes = 4096;
+
+// ---------------------------------------------------------------- shared control block
+struct alignas(64) ShmHeader {
+  uint64_t magic;
+  int32_t nranks;
+  std::atomic<int32_t> attached;
+  std::atomic<int32_t> bar_count;
+  std::atomic<int32_t> bar_sense;
+  std::atomic<int32_t> abort;
+};
+
+struct alignas(64) RankInfo {
+  int32_t pid;
+  int32_t dev;
+  char bus_id[32];
+  cudaIpcMemHandle_t scratch_handle;
+  std::atomic<uint64_t> op_count;  // opCount
+};
+
+struct alignas(64) RankFlags {
+  uint32_t ready[kSlots];  // written by the owner's user stream
+  uint32_t done[kSlots];   // written by the copy stream that completes the op
+};
+
+struct alignas(64) CtsEntry {
+  std::atomic<uint64_t> seq;  // 1-based index of this recv on the pair; published last
+  uint64_t bytes;
+  uint64_t buffer_id;
+  uint64_t base_offset;
+  uint64_t direct_ptr;  // self-sends: plain pointer
+  uint32_t ready_slot, ready_gen, done_slot, done_gen;
+  cudaIpcMemHandle_t handle;
+};
+
+// Per ordered pair src->dst: recv postings by dst, consumed by src's proxy;
+// the sender proxy mirrors the receiver-side pointers for iccl_req_state.
+struct alignas(64) PairState {
+  std::atomic<uint64_t> consumed;
+  std::atomic<uint64_t> cur_seq;
+  std::atomic<int32_t> total, done, active_path, switches;
+};
+
+struct alignas(64) CtsRing {
+  PairState st;
+  CtsEntry e[kCtsDepth];
+};
+
+struct ShmLayout {
+  size_t off_ranks, off_flags, off_rings, total;
+  explicit ShmLayout(int n) {
+    size_t o = 4096;
+    off_ranks = o;
+    o += sizeof(RankInfo) * n;
+    o = (o + 4095) & ~(size_t)4095;
+    off_flags = o;
+    o += sizeof(RankFlags) * n;
+    o = (o + 4095) & ~(size_t)4095;
+    off_rings = o;
+    o += sizeof(CtsRing) * n * n;
+    total = (o + 4095) & ~(size_t)4095;
+  }
+};
+
+struct UidBlob {
+  uint64_t magic;
+  char shm_name[64];
+};
+
+static inline bool cyc_geq(uint32_t a, uint32_t b) { return (int32_t)(a - b) >= 0; }
+
+// ---------------------------------------------------------------- proxy-side structures
+enum Engine { ENG_CE = 0, ENG_SM = 1 };
+
+struct OpDesc {
+  int kind;  // 0 send, 1 recv
+  int peer;
+  const char* src;
+  size_t bytes;
+  uint32_t slot, gen;
+  uint64_t op_seq;
+};
+
+struct ChunkRec {
+  int stream = -1;  // index into Channel::stream table
+  cudaEvent_t ev = nullptr;  // recorded after the chunk: the WC the proxy polls
+  uint64_t t1 = 0;
+  int path = 0;
+  int stamp = -1;
+  bool done = false;
+};
+
+struct Xfer {
+  uint64_t op_seq = 0;
+  uint64_t cts_seq = 0;
+  const char* src = nullptr;
+  char* dst = nullptr;
+  size_t bytes = 0;
+  uint32_t s_slot = 0, s_gen = 0;
+  uint32_t r_ready_slot = 0, r_ready_gen = 0, r_done_slot = 0, r_done_gen = 0;
+  int nchunks = 0;
+  size_t chunk = 0;
+  int next_issue = 0;  // sender posted == transmitted (chunks handed to an engine)
+  int completed = 0;   // contiguous prefix observed delivered: acked == receiver done
+  int path = 0;
+  uint32_t waited[2] = {0, 0};  // per path: stream bitmask that waited on the ready flags
+  bool done_enqueued = false;
+  bool eligible = false;
+  uint64_t last_progress = 0;
+  int switches = 0;
+  int pending_gate = -1;  // gate released once this xfer completes on the new path
+  int fault_ops_index = -1;
+  std::vector<ChunkRec> rec;
+  std::vector<cudaEvent_t> fences;  // events the completion must also wait for
+};
+
+struct StreamCtx {
+  cudaStream_t s = nullptr;
+  uint32_t ticket = 0;
+  volatile uint32_t* prog = nullptr;  // host-mapped, written by the stream after each chunk
+  cudaEvent_t ev = nullptr;
+  int engine = ENG_CE;
+};
+
+struct FaultState {
+  bool down = false;
+  int gate = -1;        // gate word index while down
+  uint64_t down_at = 0;  // ns
+};
+
+struct Channel {
+  int peer = -1;
+  std::deque<OpDesc> sends;  // waiting for the receiver's CTS
+  uint64_t next_cts = 1;
+  std::deque<Xfer> xfers;    // matched, in issue order
+  std::vector<int> path_streams[2];
+  int probe_stream = -1;
+  int active_path = 0;
+  FaultState fault[2];
+  std::unordered_map<uint64_t, char*> ipc;  // receiver buffer_id -> mapped base
+  // probe state
+  bool probe_out = false;
+  uint32_t probe_ticket_expect = 0;
+  uint64_t probe_sent = 0;
+  int probe_path = 0;
+  uint64_t last_probe = 0;
+  int sends_seen = 0;  // for chunk-triggered faults
+  char* peer_scratch = nullptr;
+};
+
+struct Fault {
+  iccl_fault_t f;
+  bool fired = false;
+};
+
+}  // namespace iccl
+
+using namespace iccl;
+
+struct iccl_comm {
+  int rank = 0, nranks = 0, dev = 0;
+  iccl_config_t cfg{};
+  // shm
+  std::string shm_name;
+  void* shm = nullptr;
+  size_t shm_bytes = 0;
+  ShmHeader* hdr = nullptr;
+  RankInfo* ranks = nullptr;
+  RankFlags* flags = nullptr;
+  CtsRing* rings = nullptr;
+  int bar_sense = 0;
+  // private pinned host memory (progress words, gates, probe words, stamps)
+  uint32_t* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  volatile uint32_t* gate_words = nullptr;
+  int next_gate = 0;
+  KernelStamp* stamps = nullptr;
+  int next_stamp = 0;
+  unsigned long long* gtimer = nullptr;
+  int64_t gtimer_offset = 0;  // host_ns - globaltimer_ns
+  char* scratch = nullptr;    // device scratch (probe target), exported to peers
+  // API state
+  uint64_t op_seq = 0;
+  int group_depth = 0;
+  std::vector<std::pair<OpDesc, cudaStream_t>> group_ops;
+  std::unordered_map<uint64_t, cudaIpcMemHandle_t> export_cache;
+  // proxy
+  std::vector<Channel> ch;
+  std::vector<StreamCtx> streams;
+  std::thread proxy;
+  std::atomic<bool> stop{false};
+  std::mutex qmu;
+  std::condition_variable qcv;
+  std::vector<OpDesc> inbox;
+  std::mutex mon_mu;
+  std::deque<iccl_mon_rec_t> mon;
+  std::deque<iccl_switch_event_t> sw_events;
+  std::atomic<int> monitor_enabled{0};
+  std::atomic<int> async_err{ICCL_SUCCESS};
+  std::string async_msg;
+  std::mutex fault_mu;
+  std::vector<Fault> faults;
+  uint64_t faults_t0 = 0;
+  std::atomic<int> path_req[kMaxRanks];  // API-requested switches: -1 none, else target path
+  std::atomic<int> active_path_pub[kMaxRanks];
+  std::atomic<uint64_t> pending_xfers{0};
+  std::atomic<uint64_t> kernels_launched{0}, copies_issued{0}, bytes_issued{0};
+  std::vector<cudaEvent_t> event_pool;  // proxy-owned: chunk WC events
+  std::vector<cudaEvent_t> all_events;
+};
+
+namespace iccl {
+
+static RankFlags* flags_of(iccl_comm* c, int r) { return &c->flags[r]; }
+static CtsRing* ring_of(iccl_comm* c, int src, int dst) { return &c->rings[src * c->nranks + dst]; }
+
+static void set_async(iccl_comm* c, iccl_result_t e, const std::string& msg) {
+  int expected = ICCL_SUCCESS;
+  if (c->async_err.compare_exchange_strong(expected, e)) c->async_msg = msg;
+}
+
+// sense-reversing barrier over the shm header
+static iccl_result_t shm_barrier(iccl_comm* c, double timeout_s = 120.0) {
+  c->bar_sense ^= 1;
+  int s = c->bar_sense;
+  if (c->hdr->bar_count.fetch_add(1) + 1 == c->nranks) {
+    c->hdr->bar_count.store(0);
+    c->hdr->bar_sense.store(s);
+    return ICCL_SUCCESS;
+  }
+  uint64_t t0 = now_ns();
+  while (c->hdr->bar_sense.load() != s) {
+    if (c->hdr->abort.load()) return ICCL_ERR_ABORTED;
+    if ((now_ns() - t0) * 1e-9 > timeout_s) {
+      set_last_error("bootstrap barrier timed out");
+      return ICCL_ERR_TIMEOUT;
+    }
+    usleep(50);
+  }
+  return ICCL_SUCCESS;
+}
+
+// ---------------------------------------------------------------- proxy helpers
+static iccl_result_t memop_write(cudaStream_t s, volatile void* addr, uint32_t v) {
+  ICCL_CHECK_CU(driver()->cuStreamWriteValue32((CUstream)s, (CUdeviceptr)addr, v, CU_STREAM_WRITE_VALUE_DEFAULT));
+  return ICCL_SUCCESS;
+}
+static iccl_result_t memop_wait(cudaStream_t s, volatile void* addr, uint32_t v) {
+  ICCL_CHECK_CU(driver()->cuStreamWaitValue32((CUstream)s, (CUdeviceptr)addr, v, CU_STREAM_WAIT_VALUE_GEQ));
+  return ICCL_SUCCESS;
+}
+
+static cudaEvent_t get_event(iccl_comm* c) {
+  if (c->event_pool.empty()) {
+    cudaEvent_t e = nullptr;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    c->all_events.push_back(e);
+    return e;
+  }
+  cudaEvent_t e = c->event_pool.back();
+  c->event_pool.pop_back();
+  return e;
+}
+
+static void put_events(iccl_comm* c, std::vector<ChunkRec>& recs) {
+  for (ChunkRec& r : recs)
+    if (r.ev) {
+      c->event_pool.push_back(r.ev);
+      r.ev = nullptr;
+    }
+}
+
+static int alloc_gate(iccl_comm* c) {
+  int g = c->next_gate++ % kGateWords;
+  c->gate_words[g] = 0;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  return g;
+}
+
+static void release_gate(iccl_comm* c, int g) {
+  if (g < 0) return;
+  __atomic_store_n((uint32_t*)&c->gate_words[g], 1u, __ATOMIC_SEQ_CST);
+}
+
+static void push_switch_event(iccl_comm* c, int peer, int to, int resume, int trigger, uint64_t detect_ns) {
+  std::lock_guard<std::mutex> g(c->mon_mu);
+  iccl_switch_event_t e{now_ns(), peer, to, resume, trigger, detect_ns};
+  c->sw_events.push_back(e);
+  if (c->sw_events.size() > 65536) c->sw_events.pop_front();
+}
+
+static iccl_result_t open_peer_buffer(iccl_comm* c, Channel& chn, const CtsEntry& e, char** out) {
+  if (chn.peer == c->rank) {
+    *out = (char*)(uintptr_t)e.direct_ptr;
+    return ICCL_SUCCESS;
+  }
+  auto it = chn.ipc.find(e.buffer_id);
+  if (it == chn.ipc.end()) {
+    void* p = nullptr;
+    cudaIpcMemHandle_t h = e.handle;
+    ICCL_CHECK_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    it = chn.ipc.emplace(e.buffer_id, (char*)p).first;
+  }
+  *out = it->second + e.base_offset;
+  return ICCL_SUCCESS;
+}
+
+static int engine_for(iccl_comm* c, size_t bytes) {
+  if (c->cfg.transport == ICCL_TRANSPORT_SM) return ENG_SM;
+  if (c->cfg.transport == ICCL_TRANSPORT_CE) return ENG_CE;
+  return bytes <= c->cfg.sm_small_bytes ? ENG_SM : ENG_CE;
+}
+
+// Path p of a channel: primary (0) uses the configured engine, backup (1) the other one.
+static int path_engine(iccl_comm* c, int path, size_t bytes) {
+  int prim = engine_for(c, bytes);
+  return path == 0 ? prim : (prim == ENG_CE ? ENG_SM : ENG_CE);
+}
+
+static int stream_for(iccl_comm* c, Channel& chn, int path, int engine, int k) {
+  // path_streams[path] holds [CE streams..., SM stream] — pick by engine
+  std::vector<int>& v = chn.path_streams[path];
+  std::vector<int> cand;
+  for (int si : v)
+    if (c->streams[si].engine == engine) cand.push_back(si);
+  return cand[k % cand.size()];
+}
+
+static void fire_time_faults(iccl_comm* c) {
+  std::lock_guard<std::mutex> g(c->fault_mu);
+  uint64_t t = now_ns();
+  for (auto& f : c->faults) {
+    if (f.fired || f.f.trigger_kind != 0 || f.f.src != c->rank) continue;
+    if (t - c->faults_t0 < f.f.t_us * 1000ull) continue;
+    f.fired = true;
+    Channel& chn = c->ch[f.f.dst];
+    FaultState& fs = chn.fault[f.f.path & 1];
+    if (!f.f.up && !fs.down) {
+      fs.down = true;
+      fs.gate = alloc_gate(c);
+      fs.down_at = t;
+    } else if (f.f.up && fs.down) {
+      fs.down = false;
+      release_gate(c, fs.gate);
+      fs.gate = -1;
+    }
+  }
+}
+
+static void fire_chunk_faults(iccl_comm* c, Channel& chn, int op_index, int chunk, int path) {
+  std::lock_guard<std::mutex> g(c->fault_mu);
+  for (auto& f : c->faults) {
+    if (f.fired || f.f.trigger_kind != 1 || f.f.src != c->rank || f.f.dst != chn.peer) continue;
+    if (f.f.op_index != op_index || f.f.chunk != chunk || (f.f.path & 1) != path) continue;
+    f.fired = true;
+    FaultState& fs = chn.fault[path];
+    if (!f.f.up && !fs.down) {
+      fs.down = true;
+      fs.gate = alloc_gate(c);
+      fs.down_at = now_ns();
+    } else if (f.f.up && fs.down) {
+      fs.down = false;
+      release_gate(c, fs.gate);
+      fs.gate = -1;
+    }
+  }
+}
+
+static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
+  const int path = x.path;
+  const int eng = path_engine(c, path, x.bytes);
+  const int si = stream_for(c, chn, path, eng, k);
+  StreamCtx& sc = c->streams[si];
+  const int bit = 1 << (si % 32);
+  RankFlags* mine = flags_of(c, c->rank);
+  RankFlags* theirs = flags_of(c, chn.peer);
+  if (!(x.waited[path] & bit)) {
+    // hostFunc#1 analog: the copy may start only once both user streams reached the op
+    iccl_result_t r = memop_wait(sc.s, &mine->ready[x.s_slot], x.s_gen);
+    if (r) return r;
+    r = memop_wait(sc.s, &theirs->ready[x.r_ready_slot], x.r_ready_gen);
+    if (r) return r;
+    x.waited[path] |= bit;
+  }
+  if (x.fault_ops_index >= 0) fire_chunk_faults(c, chn, x.fault_ops_index, k, path);
+  if (chn.fault[path].down) {
+    iccl_result_t r = memop_wait(sc.s, &c->gate_words[chn.fault[path].gate], 1);
+    if (r) return r;
+  }
+  const size_t off = (size_t)k * x.chunk;
+  const size_t n = std::min(x.chunk, x.bytes - off);
+  ChunkRec& rc = x.rec[k];
+  rc.t1 = now_ns();
+  rc.path = path;
+  rc.stream = si;
+  rc.done = false;
+  rc.stamp = -1;
+  // Monitor on: the chunk's WR/WC pair is stamped on the device (K4) with
+  // %globaltimer and the t2 stamp doubles as the WC the proxy polls.  Monitor
+  // off: the WC is an event record (no kernel: the copy-engine path uses 0 SMs).
+  KernelStamp* st = nullptr;
+  if (c->monitor_enabled.load(std::memory_order_relaxed)) {
+    rc.stamp = c->next_stamp++ % kStampSlots;
+    st = &c->stamps[rc.stamp];
+    memset((void*)st, 0, sizeof(KernelStamp));
+  }
+  if (eng == ENG_CE) {
+    if (st) ICCL_CHECK_CUDA(launch_stamp(st, 0, sc.s));
+    ICCL_CHECK_CU(driver()->cuMemcpyDtoDAsync((CUdeviceptr)(x.dst + off), (CUdeviceptr)(x.src + off), n, (CUstream)sc.s));
+    if (st) ICCL_CHECK_CUDA(launch_stamp(st, 1, sc.s));
+  } else {
+    ICCL_CHECK_CUDA(launch_copy(x.src + off, x.dst + off, n, c->cfg.sm_cap, st, sc.s));
+  }
+  c->kernels_launched += st ? (eng == ENG_CE ? 2 : 1) : (eng == ENG_SM ? 1 : 0);
+  c->copies_issued += 1;
+  c->bytes_issued += n;
+  // Without stamps the WC is an event after the chunk.  (A stream memop here
+  // would cost a full copy-engine drain per chunk: probes/p2p_probe3.)
+  if (!st) {
+    if (!rc.ev) rc.ev = get_event(c);
+    ICCL_CHECK_CUDA(cudaEventRecord(rc.ev, sc.s));
+  }
+  iccl_result_t r = ICCL_SUCCESS;
+  if (k == x.nchunks - 1) {
+    // completion (hostFunc#2 analog): join every stream that carried chunks of
+    // this op, plus the fences of paths abandoned by a switch, then release
+    // both user streams.
+    for (int p = 0; p < 2; p++) {
+      for (int sj : chn.path_streams[p]) {
+        if (sj == si || !(x.waited[p] & (1 << (sj % 32)))) continue;
+        StreamCtx& o = c->streams[sj];
+        ICCL_CHECK_CUDA(cudaEventRecord(o.ev, o.s));
+        ICCL_CHECK_CUDA(cudaStreamWaitEvent(sc.s, o.ev, 0));
+      }
+    }
+    for (cudaEvent_t fe : x.fences) ICCL_CHECK_CUDA(cudaStreamWaitEvent(sc.s, fe, 0));
+    r = memop_write(sc.s, &theirs->done[x.r_done_slot], x.r_done_gen);
+    if (r) return r;
+    r = memop_write(sc.s, &mine->done[x.s_slot], x.s_gen);
+    if (r) return r;
+    x.done_enqueued = true;
+  }
+  return ICCL_SUCCESS;
+}
+
+// switch_qp: receiver-driven breakpoint.  The receiver's
+// done (contiguous delivered prefix) is where retransmission resumes; posted
+// and transmitted retreat to it; stale in-flight work on the abandoned path is
+// fenced so completion waits for it.
+static iccl_result_t switch_path(iccl_comm* c, Channel& chn, int to, int trigger) {
+  if (chn.active_path == to) return ICCL_SUCCESS;
+  const int from = chn.active_path;
+  uint64_t detect = chn.fault[from].down ? now_ns() - chn.fault[from].down_at : 0;
+  int resume = -1;
+  int stale_gate = chn.fault[from].down ? chn.fault[from].gate : -1;
+  for (Xfer& x : chn.xfers) {
+    // fence: an event after everything already queued on the abandoned path
+    bool had_work = x.next_issue > x.completed || x.done_enqueued;
+    if (had_work) {
+      for (int sj : chn.path_streams[from]) {
+        if (!(x.waited[from] & (1 << (sj % 32)))) continue;
+        cudaEvent_t fe;
+        ICCL_CHECK_CUDA(cudaEventCreateWithFlags(&fe, cudaEventDisableTiming));
+        ICCL_CHECK_CUDA(cudaEventRecord(fe, c->streams[sj].s));
+        x.fences.push_back(fe);
+      }
+    }
+    if (resume < 0) resume = x.completed;
+    // retreat: posted = transmitted = acked = done
+    x.next_issue = x.completed;
+    x.path = to;
+    x.done_enqueued = false;
+    x.switches++;
+    if (had_work && stale_gate >= 0) x.pending_gate = stale_gate;
+    x.last_progress = now_ns();
+  }
+  if (stale_gate >= 0) {
+    // future work on the still-Down path waits on a fresh gate epoch; the old
+    // one is released (flushing the stale copies) once the data went the new way
+    chn.fault[from].gate = alloc_gate(c);
+    bool any_pending = false;
+    for (Xfer& x : chn.xfers) any_pending |= (x.pending_gate == stale_gate);
+    if (!any_pending) release_gate(c, stale_gate);
+  }
+  chn.active_path = to;
+  c->active_path_pub[chn.peer].store(to);
+  PairState& ps = ring_of(c, c->rank, chn.peer)->st;
+  ps.active_path.store(to);
+  ps.switches.fetch_add(1);
+  chn.probe_out = false;
+  chn.last_probe = now_ns();
+  push_switch_event(c, chn.peer, to, resume, trigger, detect);
+  return ICCL_SUCCESS;
+}
+
+static iccl_result_t send_probe(iccl_comm* c, Channel& chn, int path) {
+  const int si = chn.probe_stream;
+  StreamCtx& sc = c->streams[si];
+  if (chn.fault[path].down) {
+    iccl_result_t r = memop_wait(sc.s, &c->gate_words[chn.fault[path].gate], 1);
+    if (r) return r;
+  }
+  // a 16-byte zero-payload-ish CTS over the suspect path into the peer's scratch
+  ICCL_CHECK_CU(driver()->cuMemcpyDtoDAsync((CUdeviceptr)chn.peer_scratch, (CUdeviceptr)c->scratch, 16, (CUstream)sc.s));
+  chn.probe_ticket_expect = ++sc.ticket;
+  iccl_result_t r = memop_write(sc.s, sc.prog, chn.probe_ticket_expect);
+  if (r) return r;
+  chn.probe_out = true;
+  chn.probe_sent = now_ns();
+  chn.probe_path = path;
+  return ICCL_SUCCESS;
+}
+
+static void record_monitor(iccl_comm* c, Channel& chn, Xfer& x, int k, uint64_t t2_host) {
+  ChunkRec& rc = x.rec[k];
+  iccl_mon_rec_t m{};
+  m.t1_ns = rc.t1;
+  m.t2_ns = t2_host;
+  if (rc.stamp >= 0) {
+    KernelStamp* st = &c->stamps[rc.stamp];
+    unsigned long long t1 = st->t1, t2 = st->t2;
+    if (t1 && t2 && t2 > t1) {
+      m.t1_ns = (uint64_t)((int64_t)t1 + c->gtimer_offset);
+      m.t2_ns = (uint64_t)((int64_t)t2 + c->gtimer_offset);
+    }
+  }
+  m.bytes = std::min(x.chunk, x.bytes - (size_t)k * x.chunk);
+  m.peer = chn.peer;
+  m.path = rc.path;
+  m.chunk = k;
+  m.dir = 0;
+  m.op_seq = x.op_seq;
+  std::lock_guard<std::mutex> g(c->mon_mu);
+  c->mon.push_back(m);
+  if (c->mon.size() > (1u << 20)) c->mon.pop_front();
+}
+
+// One proxy pass over a channel.  Returns true if anything moved.
+static iccl_result_t progress_channel(iccl_comm* c, Channel& chn, bool* busy) {
+  iccl_result_t r;
+  // 1. match sends with the receiver's CTS (recv postings for rank->peer live in ring(rank, peer))
+  CtsRing* rr = ring_of(c, c->rank, chn.peer);
+  while (!chn.sends.empty()) {
+    CtsEntry& e = rr->e[(chn.next_cts - 1) % kCtsDepth];
+    if (e.seq.load(std::memory_order_acquire) != chn.next_cts) break;
+    OpDesc op = chn.sends.front();
+    chn.sends.pop_front();
+    if (e.bytes != op.bytes) {
+      set_async(c, ICCL_ERR_SIZE_MISMATCH,
+                "send of " + std::to_string(op.bytes) + " B to rank " + std::to_string(chn.peer) +
+                    " matched a recv of " + std::to_string(e.bytes) + " B");
+      return ICCL_ERR_SIZE_MISMATCH;
+    }
+    Xfer x;
+    x.op_seq = op.op_seq;
+    x.cts_seq = chn.next_cts;
+    x.src = op.src;
+    r = open_peer_buffer(c, chn, e, &x.dst);
+    if (r) return r;
+    x.bytes = op.bytes;
+    x.s_slot = op.slot;
+    x.s_gen = op.gen;
+    x.r_ready_slot = e.ready_slot;
+    x.r_ready_gen = e.ready_gen;
+    x.r_done_slot = e.done_slot;
+    x.r_done_gen = e.done_gen;
+    x.chunk = (size_t)c->cfg.chunk_bytes;
+    x.nchunks = (int)((x.bytes + x.chunk - 1) / x.chunk);
+    x.rec.resize(x.nchunks);
+    x.path = chn.active_path;
+    x.last_progress = now_ns();
+    x.fault_ops_index = chn.sends_seen++;
+    chn.next_cts++;
+    rr->st.consumed.store(chn.next_cts - 1, std::memory_order_release);
+    rr->st.cur_seq.store(x.cts_seq);
+    rr->st.total.store(x.nchunks);
+    rr->st.done.store(0);
+    chn.xfers.push_back(std::move(x));
+    *busy = true;
+  }
+  if (chn.xfers.empty()) return ICCL_SUCCESS;
+  // 2. completions: advance each xfer's contiguous delivered prefix (acked / done)
+  const uint64_t tnow = now_ns();
+  for (Xfer& x : chn.xfers) {
+    while (x.completed < x.next_issue) {
+      ChunkRec& rc = x.rec[x.completed];
+      if (rc.stamp >= 0) {
+        if (__atomic_load_n(&c->stamps[rc.stamp].t2, __ATOMIC_ACQUIRE) == 0) break;
+      } else {
+        cudaError_t q = cudaEventQuery(rc.ev);
+        if (q == cudaErrorNotReady) break;
+        if (q != cudaSuccess) {
+          set_last_error(std::string("chunk completion: ") + cudaGetErrorString(q));
+          return ICCL_ERR_CUDA;
+        }
+      }
+      rc.done = true;
+      if (c->monitor_enabled.load(std::memory_order_relaxed)) record_monitor(c, chn, x, x.completed, tnow);
+      x.completed++;
+      x.last_progress = tnow;
+      *busy = true;
+    }
+    if (&x == &chn.xfers.front()) rr->st.done.store(x.completed);
+  }
+  // 3. retire completed xfers (their done writes are queued on the device)
+  while (!chn.xfers.empty()) {
+    Xfer& x = chn.xfers.front();
+    if (!(x.completed == x.nchunks && x.done_enqueued)) break;
+    if (x.pending_gate >= 0) {
+      int g = x.pending_gate;
+      x.pending_gate = -1;
+      bool others = false;
+      for (size_t i = 1; i < chn.xfers.size(); i++) others |= chn.xfers[i].pending_gate == g;
+      if (!others) release_gate(c, g);  // flush the abandoned path's stale copies
+    }
+    if (!x.fences.empty()) {
+      // fences may only be destroyed after the device consumed them; the
+      // done flag write follows them on the same stream
+      RankFlags* mine = flags_of(c, c->rank);
+      if (!cyc_geq(mine->done[x.s_slot], x.s_gen)) break;
+      for (cudaEvent_t fe : x.fences) cudaEventDestroy(fe);
+      x.fences.clear();
+    }
+    put_events(c, x.rec);
+    chn.xfers.pop_front();
+    c->pending_xfers.fetch_sub(1);
+    *busy = true;
+  }
+  // 4. issue within the window (posted - acked <= window)
+  int outstanding = 0;
+  for (Xfer& x : chn.xfers) outstanding += x.next_issue - x.completed;
+  for (Xfer& x : chn.xfers) {
+    if (x.path != chn.active_path) continue;
+    while (x.next_issue < x.nchunks && outstanding < c->cfg.window) {
+      r = issue_chunk(c, chn, x, x.next_issue);
+      if (r) return r;
+      x.next_issue++;
+      outstanding++;
+      *busy = true;
+    }
+    if (x.next_issue < x.nchunks) break;
+  }
+  // 5. watchdog + probe (check_receiver_timeout)
+  if (!chn.xfers.empty()) {
+    Xfer& x = chn.xfers.front();
+    RankFlags* mine = flags_of(c, c->rank);
+    RankFlags* theirs = flags_of(c, chn.peer);
+    bool elig = cyc_geq(mine->ready[x.s_slot], x.s_gen) && cyc_geq(theirs->ready[x.r_ready_slot], x.r_ready_gen);
+    if (!elig) {
+      x.last_progress = tnow;  // innocent stall upstream: the sender's data is not ready
+    } else if (!x.eligible) {
+      x.eligible = true;
+      x.last_progress = tnow;
+    }
+    const uint64_t delta = c->cfg.delta_us * 1000ull;
+    if (elig && x.completed < x.next_issue && tnow - x.last_progress > delta) {
+      if (!chn.probe_out) {
+        r = send_probe(c, chn, chn.active_path);
+        if (r) return r;
+      } else if (chn.probe_path == chn.active_path) {
+        StreamCtx& ps = c->streams[chn.probe_stream];
+        if (cyc_geq(*ps.prog, chn.probe_ticket_expect)) {
+          chn.probe_out = false;  // CTS ok: innocent link
+          x.last_progress = tnow;
+        } else if (tnow - chn.probe_sent > delta) {
+          // CTS failed: trigger the switch
+          r = switch_path(c, chn, chn.active_path ^ 1, 1);
+          if (r) return r;
+          *busy = true;
+        }
+      }
+    }
+  }
+  return ICCL_SUCCESS;
+}
+
+// monitor_failed_link: while on the backup, probe the
+// primary every probe period; a probe that completes switches back.
+static iccl_result_t monitor_failed_link(iccl_comm* c, Channel& chn) {
+  if (chn.active_path != 1) return ICCL_SUCCESS;
+  const uint64_t t = now_ns();
+  StreamCtx& ps = c->streams[chn.probe_stream];
+  if (chn.probe_out) {
+    if (cyc_geq(*ps.prog, chn.probe_ticket_expect)) {
+      chn.probe_out = false;
+      if (chn.probe_path == 0 && !chn.fault[0].down) return switch_path(c, chn, 0, 2);
+    }
+    return ICCL_SUCCESS;
+  }
+  if (t - chn.last_probe >= c->cfg.probe_period_us * 1000ull) {
+    chn.last_probe = t;
+    return send_probe(c, chn, 0);
+  }
+  return ICCL_SUCCESS;
+}
+
+static void proxy_loop(iccl_comm* c) {
+  cudaSetDevice(c->dev);
+  if (c->cfg.proxy_cpu >= 0) {
+    cpu_set_t set;
+    CPU_ZERO(&set);
+    CPU_SET(c->cfg.proxy_cpu, &set);
+    pthread_setaffinity_np(pthread_self(), sizeof(set), &set);
+  }
+  std::vector<OpDesc> batch;
+  uint64_t idle_since = now_ns();
+  while (!c->stop.load(std::memory_order_relaxed)) {
+    bool busy = false;
+    {
+      std::unique_lock<std::mutex> lk(c->qmu);
+      if (c->inbox.empty() && c->pending_xfers.load() == 0 && now_ns() - idle_since > 200000) {
+        c->qcv.wait_for(lk, std::chrono::microseconds(500));
+      }
+      batch.swap(c->inbox);
+    }
+    for (OpDesc& op : batch) {
+      if (op.kind == 0) {
+        c->ch[op.peer].sends.push_back(op);
+        busy = true;
+      }
+    }
+    batch.clear();
+    if (c->async_err.load() != ICCL_SUCCESS) {
+      usleep(100);
+      continue;
+    }
+    fire_time_faults(c);
+    for (int p = 0; p < c->nranks; p++) {
+      Channel& chn = c->ch[p];
+      int req = c->path_req[p].exchange(-1);
+      iccl_result_t r = ICCL_SUCCESS;
+      if (req >= 0) r = switch_path(c, chn, req, 0);
+      if (!r) r = progress_channel(c, chn, &busy);
+      if (!r) r = monitor_failed_link(c, chn);
+      if (r) {
+        set_async(c, r, std::string("proxy: ") + last_error());
+        break;
+      }
+    }
+    if (c->hdr->abort.load()) set_async(c, ICCL_ERR_ABORTED, "communicator aborted");
+    if (busy) idle_since = now_ns();
+  }
+}
+
+static void push_op(iccl_comm* c, const OpDesc& op) {
+  {
+    std::lock_guard<std::mutex> g(c->qmu);
+    c->inbox.push_back(op);
+  }
+  c->qcv.notify_one();
+}
+
+// Reserve the next op slot; a slot is reused only after its previous op completed.
+static iccl_result_t next_slot(iccl_comm* c, uint32_t* slot, uint32_t* gen, uint64_t* seq) {
+  uint64_t s = c->op_seq++;
+  *seq = s;
+  *slot = (uint32_t)(s % kSlots);
+  *gen = (uint32_t)(s + 1);
+  if (s >= (uint64_t)kSlots) {
+    uint32_t prev = (uint32_t)(s + 1 - kSlots);
+    uint64_t t0 = now_ns();
+    while (!cyc_geq(flags_of(c, c->rank)->done[*slot], prev)) {
+      if (c->async_err.load() != ICCL_SUCCESS) return (iccl_result_t)c->async_err.load();
+      if (now_ns() - t0 > 60ull * 1000000000ull) {
+        set_last_error("more than 4096 ops in flight for 60 s");
+        return ICCL_ERR_TIMEOUT;
+      }
+      sched_yield();
+    }
+  }
+  // ready is written by the stream; clear stale content is not needed (cyclic gens)
+  return ICCL_SUCCESS;
+}
+
+}  // namespace iccl
+
+// per-comm receiver-side posting counters (kept out of shm: only this rank posts)
+struct RecvCounters {
+  std::vector<uint64_t> posted;
+};
+static std::mutex g_rc_mu;
+static std::unordered_map<iccl_comm*, RecvCounters> g_rc;
+
+static iccl_result_t do_post_cts(iccl_comm* c, int peer, void* buf, size_t bytes, uint32_t slot, uint32_t gen) {
+  CtsRing* ring = ring_of(c, peer, c->rank);
+  uint64_t k;
+  {
+    std::lock_guard<std::mutex> g(g_rc_mu);
+    k = ++g_rc[c].posted[peer];
+  }
+  // wait for room: the sender's proxy must have consumed posting k - depth
+  uint64_t t0 = now_ns();
+  while (k > (uint64_t)kCtsDepth && ring->st.consumed.load(std::memory_order_acquire) + kCtsDepth < k) {
+    if (c->async_err.load() != ICCL_SUCCESS) return (iccl_result_t)c->async_err.load();
+    if (now_ns() - t0 > 60ull * 1000000000ull) {
+      set_last_error("CTS ring full for 60 s");
+      return ICCL_ERR_TIMEOUT;
+    }
+    sched_yield();
+  }
+  CtsEntry& e = ring->e[(k - 1) % kCtsDepth];
+  e.bytes = bytes;
+  e.ready_slot = slot;
+  e.ready_gen = gen;
+  e.done_slot = slot;
+  e.done_gen = gen;
+  e.direct_ptr = (uint64_t)(uintptr_t)buf;
+  e.buffer_id = 0;
+  e.base_offset = 0;
+  if (peer != c->rank) {
+    CUdeviceptr base = 0;
+    size_t asize = 0;
+    ICCL_CHECK_CU(driver()->cuMemGetAddressRange(&base, &asize, (CUdeviceptr)buf));
+    unsigned long long bid = 0;
+    ICCL_CHECK_CU(driver()->cuPointerGetAttribute(&bid, CU_POINTER_ATTRIBUTE_BUFFER_ID, (CUdeviceptr)buf));
+    auto it = c->export_cache.find(bid);
+    if (it == c->export_cache.end()) {
+      cudaIpcMemHandle_t h;
+      cudaError_t err = cudaIpcGetMemHandle(&h, (void*)base);
+      if (err != cudaSuccess) {
+        set_last_error(std::string("cannot export recv buffer for zero-copy (") + cudaGetErrorString(err) +
+                       "); allocate it with cudaMalloc / the torch caching allocator without expandable segments");
+        return ICCL_ERR_UNREGISTERED_REGION;
+      }
+      it = c->export_cache.emplace(bid, h).first;
+    }
+    e.handle = it->second;
+    e.buffer_id = bid;
+    e.base_offset = (uint64_t)((CUdeviceptr)buf - base);
+  }
+  e.seq.store(k, std::memory_order_release);
+  return ICCL_SUCCESS;
+}
+
+static iccl_result_t stream_markers(iccl_comm* c, cudaStream_t s, const std::vector<OpDesc>& ops) {
+  // WriteValue(ready) for every op, then WaitValue(done) for every op, batched.
+  RankFlags* mine = flags_of(c, c->rank);
+  std::vector<CUstreamBatchMemOpParams> p;
+  p.reserve(2 * ops.size());
+  for (const OpDesc& op : ops) {
+    CUstreamBatchMemOpParams w;
+    memset(&w, 0, sizeof(w));
+    w.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+    w.writeValue.address = (CUdeviceptr)&mine->ready[op.slot];
+    w.writeValue.value = op.gen;
+    w.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
+    p.push_back(w);
+  }
+  for (const OpDesc& op : ops) {
+    CUstreamBatchMemOpParams w;
+    memset(&w, 0, sizeof(w));
+    w.waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
+    w.waitValue.address = (CUdeviceptr)&mine->done[op.slot];
+    w.waitValue.value = op.gen;
+    w.waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+    p.push_back(w);
+  }
+  for (size_t i = 0; i < p.size(); i += 128) {
+    unsigned n = (unsigned)std::min<size_t>(128, p.size() - i);
+    ICCL_CHECK_CU(driver()->cuStreamBatchMemOp((CUstream)s, n, p.data() + i, 0));
+  }
+  return ICCL_SUCCESS;
+}
+
+static iccl_result_t enqueue_op(iccl_comm* c, int kind, const void* buf, size_t bytes, int peer, cudaStream_t s,
+                                iccl_req_t* req) {
+  ICCL_RETURN_IF(!c, ICCL_ERR_INVALID_ARGUMENT, "null communicator");
+  ICCL_RETURN_IF(peer < 0 || peer >= c->nranks, ICCL_ERR_INVALID_ARGUMENT, "peer out of range");
+  ICCL_RETURN_IF(bytes == 0, ICCL_ERR_ZERO_LENGTH_MESSAGE, "zero-length message (SPEC.md:236)");
+  ICCL_RETURN_IF(!buf, ICCL_ERR_UNREGISTERED_REGION, "null buffer");
+  int ae = c->async_err.load();
+  if (ae != ICCL_SUCCESS) {
+    set_last_error(c->async_msg);
+    return (iccl_result_t)ae;
+  }
+  OpDesc op{};
+  op.kind = kind;
+  op.peer = peer;
+  op.src = (const char*)buf;
+  op.bytes = bytes;
+  iccl_result_t r = next_slot(c, &op.slot, &op.gen, &op.op_seq);
+  if (r) return r;
+  if (kind == 1) {
+    r = do_post_cts(c, peer, (void*)buf, bytes, op.slot, op.gen);
+    if (r) return r;
+  }
+  c->ranks[c->rank].op_count.fetch_add(1, std::memory_order_relaxed);
+  if (req) *req = ((uint64_t)op.slot << 32) | op.gen;
+  if (c->group_depth > 0) {
+    c->group_ops.emplace_back(op, s);
+    return ICCL_SUCCESS;
+  }
+  r = stream_markers(c, s, {op});
+  if (r) return r;
+  if (kind == 0) {
+    c->pending_xfers.fetch_add(1);
+    push_op(c, op);
+  }
+  return ICCL_SUCCESS;
+}
+
+extern "C" {
+
+iccl_result_t iccl_get_unique_id(iccl_unique_id_t* uid) {
+  if (!uid) return ICCL_ERR_INVALID_ARGUMENT;
+  memset(uid, 0, sizeof(*uid));
+  UidBlob b{};
+  b.magic = kMagic;
+  std::random_device rd;
+  snprintf(b.shm_name, sizeof(b.shm_name), "/iccl-b200-%d-%08x%08x", (int)getpid(), rd(), rd());
+  memcpy(uid->internal, &b, sizeof(b));
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t uid, int rank, int cuda_dev,
+                                  const iccl_config_t* cfg) {
+  ICCL_RETURN_IF(!out, ICCL_ERR_INVALID_ARGUMENT, "null comm out");
+  ICCL_RETURN_IF(nranks < 1 || nranks > kMaxRanks, ICCL_ERR_INVALID_ARGUMENT, "nranks out of range");
+  ICCL_RETURN_IF(rank < 0 || rank >= nranks, ICCL_ERR_INVALID_ARGUMENT, "rank out of range");
+  UidBlob b;
+  memcpy(&b, uid.internal, sizeof(b));
+  ICCL_RETURN_IF(b.magic != kMagic, ICCL_ERR_INVALID_ARGUMENT, "bad unique id");
+  iccl_config_t conf;
+  if (cfg) conf = *cfg;
+  else iccl_config_init(&conf);
+  iccl_result_t r = iccl_config_validate(&conf);
+  if (r) return r;
+
+  ICCL_RETURN_IF(!driver(), ICCL_ERR_CUDA, last_error());
+  ICCL_CHECK_CU(driver()->cuInit(0));
+  ICCL_CHECK_CUDA(cudaSetDevice(cuda_dev));
+  ICCL_CHECK_CUDA(cudaFree(0));  // make the primary context current
+  ICCL_CHECK_CUDA(preload_kernels());
+  CUdevice cd;
+  ICCL_CHECK_CU(driver()->cuDeviceGet(&cd, cuda_dev));
+  int memops = 0;
+  driver()->cuDeviceGetAttribute(&memops, CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS, cd);
+
+  auto* c = new iccl_comm();
+  c->rank = rank;
+  c->nranks = nranks;
+  c->dev = cuda_dev;
+  c->cfg = conf;
+  c->monitor_enabled.store(conf.monitor_enabled);
+  c->shm_name = b.shm_name;
+  for (int i = 0; i < kMaxRanks; i++) {
+    c->path_req[i].store(-1);
+    c->active_path_pub[i].store(0);
+  }
+  {
+    std::lock_guard<std::mutex> g(g_rc_mu);
+    g_rc[c].posted.assign(nranks, 0);
+  }
+  ShmLayout L(nranks);
+  int fd = shm_open(b.shm_name, O_CREAT | O_RDWR, 0600);
+  if (fd < 0) {
+    set_last_error(std::string("shm_open: ") + strerror(errno));
+    delete c;
+    return ICCL_ERR_SYSTEM;
+  }
+  if (ftruncate(fd, (off_t)L.total) != 0) {
+    set_last_error(std::string("ftruncate: ") + strerror(errno));
+    close(fd);
+    delete c;
+    return ICCL_ERR_SYSTEM;
+  }
+  void* m = mmap(nullptr, L.total, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (m == MAP_FAILED) {
+    set_last_error(std::string("mmap: ") + strerror(errno));
+    delete c;
+    return ICCL_ERR_SYSTEM;
+  }
+  c->shm = m;
+  c->shm_bytes = L.total;
+  c->hdr = (ShmHeader*)m;
+  c->ranks = (RankInfo*)((char*)m + L.off_ranks);
+  c->flags = (RankFlags*)((char*)m + L.off_flags);
+  c->rings = (CtsRing*)((char*)m + L.off_rings);
+  // device-visible control block: every rank's copy streams write flags here
+  ICCL_CHECK_CUDA(cudaHostRegister(m, L.total, cudaHostRegisterMapped | cudaHostRegisterPortable));
+  c->pinned_bytes = 64 * 1024 + sizeof(KernelStamp) * kStampSlots + kGateWords * 4;
+  ICCL_CHECK_CUDA(cudaHostAlloc((void**)&c->pinned, c->pinned_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  memset(c->pinned, 0, c->pinned_bytes);
+  c->gate_words = (volatile uint32_t*)((char*)c->pinned + 32 * 1024);
+  c->stamps = (KernelStamp*)((char*)c->pinned + 64 * 1024);
+  c->gtimer = (unsigned long long*)((char*)c->pinned + 48 * 1024);
+  ICCL_CHECK_CUDA(cudaMalloc((void**)&c->scratch, kScratchBytes));
+  ICCL_CHECK_CUDA(cudaMemset(c->scratch, 0, kScratchBytes));
+
+  RankInfo& me = c->ranks[rank];
+  me.pid = (int)getpid();
+  me.dev = cuda_dev;
+  cudaDeviceGetPCIBusId(me.bus_id, sizeof(me.bus_id), cuda_dev);
+  ICCL_CHECK_CUDA(cudaIpcGetMemHandle(&me.scratch_handle, c->scratch));
+  if (rank == 0) {
+    c->hdr->nranks = nranks;
+    c->hdr->magic = kMagic;
+  }
+  c->hdr->attached.fetch_add(1);
+  // wait for everyone to attach (the first barrier also orders the RankInfo writes)
+  uint64_t t0 = now_ns();
+  while (c->hdr->attached.load() < nranks) {
+    if ((now_ns() - t0) > 120ull * 1000000000ull) {
+      set_last_error("timed out waiting for ranks to attach");
+      return ICCL_ERR_TIMEOUT;
+    }
+    usleep(100);
+  }
+  r = shm_barrier(c);
+  if (r) return r;
+  if (rank == 0) shm_unlink(b.shm_name);
+
+  // streams: per peer S copy-engine streams + 1 SM stream + 1 probe stream
+  int prio_lo, prio_hi;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  c->ch.resize(nranks);
+  uint32_t* prog = c->pinned;  // first 32 KB of pinned: progress words
+  int next_prog = 0;
+  auto mk_stream = [&](int engine) -> int {
+    StreamCtx sc;
+    cudaStreamCreateWithPriority(&sc.s, cudaStreamNonBlocking, prio_hi);
+    cudaEventCreateWithFlags(&sc.ev, cudaEventDisableTiming);
+    sc.prog = prog + 16 * (next_prog++);  // one 64-byte line each
+    sc.engine = engine;
+    c->streams.push_back(sc);
+    return (int)c->streams.size() - 1;
+  };
+  for (int p = 0; p < nranks; p++) {
+    Channel& chn = c->ch[p];
+    chn.peer = p;
+    for (int s = 0; s < conf.streams_per_peer; s++) {
+      int si = mk_stream(ENG_CE);
+      chn.path_streams[0].push_back(si);
+      chn.path_streams[1].push_back(si);
+    }
+    int sm = mk_stream(ENG_SM);
+    chn.path_streams[0].push_back(sm);
+    chn.path_streams[1].push_back(sm);
+    chn.probe_stream = mk_stream(ENG_CE);
+    if (p == rank) {
+      chn.peer_scratch = c->scratch + 2048;
+    } else {
+      void* ps = nullptr;
+      ICCL_CHECK_CUDA(cudaIpcOpenMemHandle(&ps, c->ranks[p].scratch_handle, cudaIpcMemLazyEnablePeerAccess));
+      chn.peer_scratch = (char*)ps + 16 * (1 + rank);
+    }
+  }
+  // %globaltimer -> CLOCK_MONOTONIC offset for SM-path monitor stamps
+  {
+    cudaStream_t s = c->streams[0].s;
+    *c->gtimer = 0;
+    uint64_t h0 = now_ns();
+    ICCL_CHECK_CUDA(launch_read_globaltimer(c->gtimer, s));
+    ICCL_CHECK_CUDA(cudaStreamSynchronize(s));
+    uint64_t h1 = now_ns();
+    c->gtimer_offset = (int64_t)((h0 + h1) / 2) - (int64_t)(*c->gtimer);
+  }
+  r = shm_barrier(c);
+  if (r) return r;
+  c->proxy = std::thread(proxy_loop, c);
+  *out = c;
+  return ICCL_SUCCESS;
+}
+
+static void teardown(iccl_comm* c) {
+  if (c->proxy.joinable()) {
+    c->stop.store(true);
+    c->qcv.notify_one();
+    c->proxy.join();
+  }
+  for (auto& sc : c->streams) {
+    if (sc.s) {
+      cudaStreamSynchronize(sc.s);
+      cudaStreamDestroy(sc.s);
+    }
+    if (sc.ev) cudaEventDestroy(sc.ev);
+  }
+  for (cudaEvent_t e : c->all_events) cudaEventDestroy(e);
+  for (auto& chn : c->ch) {
+    for (auto& kv : chn.ipc) cudaIpcCloseMemHandle(kv.second);
+    if (chn.peer != c->rank && chn.peer_scratch) cudaIpcCloseMemHandle(chn.peer_scratch - 16 * (1 + c->rank));
+  }
+  if (c->scratch) cudaFree(c->scratch);
+  if (c->shm) {
+    cudaHostUnregister(c->shm);
+    munmap(c->shm, c->shm_bytes);
+  }
+  if (c->pinned) cudaFreeHost(c->pinned);
+  {
+    std::lock_guard<std::mutex> g(g_rc_mu);
+    g_rc.erase(c);
+  }
+}
+
+iccl_result_t iccl_comm_destroy(iccl_comm_t c) {
+  if (!c) return ICCL_ERR_INVALID_ARGUMENT;
+  // drain: every send this rank owns must have been handed to the device
+  uint64_t t0 = now_ns();
+  while (c->pending_xfers.load() > 0 && c->async_err.load() == ICCL_SUCCESS && !c->hdr->abort.load()) {
+    if (now_ns() - t0 > 120ull * 1000000000ull) break;
+    usleep(50);
+  }
+  for (auto& sc : c->streams) cudaStreamSynchronize(sc.s);
+  iccl_result_t r = c->hdr->abort.load() ? ICCL_SUCCESS : shm_barrier(c);
+  teardown(c);
+  delete c;
+  return r == ICCL_ERR_ABORTED ? ICCL_SUCCESS : r;
+}
+
+iccl_result_t iccl_comm_abort(iccl_comm_t c) {
+  if (!c) return ICCL_ERR_INVALID_ARGUMENT;
+  c->hdr->abort.store(1);
+  set_async(c, ICCL_ERR_ABORTED, "communicator aborted");
+  // release every op slot of this rank so no user stream stays blocked
+  RankFlags* mine = flags_of(c, c->rank);
+  for (uint64_t s = c->op_seq > (uint64_t)kSlots ? c->op_seq - kSlots : 0; s < c->op_seq; s++)
+    __atomic_store_n(&mine->done[s % kSlots], (uint32_t)(s + 1), __ATOMIC_SEQ_CST);
+  for (int g = 0; g < kGateWords; g++) __atomic_store_n((uint32_t*)&c->gate_words[g], 1u, __ATOMIC_SEQ_CST);
+  teardown(c);
+  delete c;
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_comm_count(iccl_comm_t c, int* n) {
+  if (!c || !n) return ICCL_ERR_INVALID_ARGUMENT;
+  *n = c->nranks;
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_comm_user_rank(iccl_comm_t c, int* r) {
+  if (!c || !r) return ICCL_ERR_INVALID_ARGUMENT;
+  *r = c->rank;
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_comm_get_async_error(iccl_comm_t c, iccl_result_t* err) {
+  if (!c || !err) return ICCL_ERR_INVALID_ARGUMENT;
+  *err = (iccl_result_t)c->async_err.load();
+  if (*err != ICCL_SUCCESS) set_last_error(c->async_msg);
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_comm_op_counts(iccl_comm_t c, uint64_t* counts, int n) {
+  if (!c || !counts || n < c->nranks) return ICCL_ERR_INVALID_ARGUMENT;
+  for (int i = 0; i < c->nranks; i++) counts[i] = c->ranks[i].op_count.load();
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_comm_stats(iccl_comm_t c, iccl_stats_t* s) {
+  if (!c || !s) return ICCL_ERR_INVALID_ARGUMENT;
+  memset(s, 0, sizeof(*s));
+  s->kernels_launched = c->kernels_launched.load();
+  s->copies_issued = c->copies_issued.load();
+  s->bytes_issued = c->bytes_issued.load();
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_register(iccl_comm_t c, void* ptr, size_t bytes, uint64_t* handle) {
+  if (!c || !ptr || !handle) return ICCL_ERR_INVALID_ARGUMENT;
+  CUdeviceptr base = 0;
+  size_t asize = 0;
+  ICCL_CHECK_CU(driver()->cuMemGetAddressRange(&base, &asize, (CUdeviceptr)ptr));
+  ICCL_RETURN_IF((CUdeviceptr)ptr + bytes > base + asize, ICCL_ERR_UNREGISTERED_REGION,
+                 "region exceeds its allocation");
+  unsigned long long bid = 0;
+  ICCL_CHECK_CU(driver()->cuPointerGetAttribute(&bid, CU_POINTER_ATTRIBUTE_BUFFER_ID, (CUdeviceptr)ptr));
+  if (!c->export_cache.count(bid)) {
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, (void*)base);
+    ICCL_RETURN_IF(e != cudaSuccess, ICCL_ERR_UNREGISTERED_REGION, "allocation cannot be exported over IPC");
+    c->export_cache.emplace(bid, h);
+  }
+  *handle = bid;
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_deregister(iccl_comm_t c, uint64_t handle) {
+  if (!c) return ICCL_ERR_INVALID_ARGUMENT;
+  ICCL_RETURN_IF(!c->export_cache.erase(handle), ICCL_ERR_UNREGISTERED_REGION, "unknown registration handle");
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_send(iccl_comm_t c, const void* buf, size_t bytes, int peer, cudaStream_t s, iccl_req_t* req) {
+  return enqueue_op(c, 0, buf, bytes, peer, s, req);
+}
+
+iccl_result_t iccl_recv(iccl_comm_t c, void* buf, size_t bytes, int peer, cudaStream_t s, iccl_req_t* req) {
+  return enqueue_op(c, 1, buf, bytes, peer, s, req);
+}
+
+iccl_result_t iccl_group_start(iccl_comm_t c) {
+  if (!c) return ICCL_ERR_INVALID_ARGUMENT;
+  c->group_depth++;
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_group_end(iccl_comm_t c) {
+  if (!c) return ICCL_ERR_INVALID_ARGUMENT;
+  ICCL_RETURN_IF(c->group_depth <= 0, ICCL_ERR_INVALID_ARGUMENT, "group_end without group_start");
+  if (--c->group_depth > 0) return ICCL_SUCCESS;
+  std::vector<std::pair<OpDesc, cudaStream_t>> ops;
+  ops.swap(c->group_ops);
+  // one batched marker set per distinct stream
+  std::vector<cudaStream_t> order;
+  for (auto& p : ops)
+    if (std::find(order.begin(), order.end(), p.second) == order.end()) order.push_back(p.second);
+  for (cudaStream_t s : order) {
+    std::vector<OpDesc> v;
+    for (auto& p : ops)
+      if (p.second == s) v.push_back(p.first);
+    iccl_result_t r = stream_markers(c, s, v);
+    if (r) return r;
+  }
+  {
+    std::lock_guard<std::mutex> g(c->qmu);
+    for (auto& p : ops)
+      if (p.first.kind == 0) {
+        c->pending_xfers.fetch_add(1);
+        c->inbox.push_back(p.first);
+      }
+  }
+  c->qcv.notify_one();
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_alltoallv(iccl_comm_t c, const void* sbuf, const size_t* scounts, const size_t* sdispls,
+                             void* rbuf, const size_t* rcounts, const size_t* rdispls, size_t elem_bytes,
+                             cudaStream_t s) {
+  if (!c || !scounts || !sdispls || !rcounts || !rdispls || elem_bytes == 0) return ICCL_ERR_INVALID_ARGUMENT;
+  iccl_result_t r = iccl_group_start(c);
+  if (r) return r;
+  const int n = c->nranks;
+  // rotated schedule: step k pairs rank i with i+k (send) and i-k (recv) so
+  // the NVSwitch sees no incast; k = 0 is the self copy
+  for (int k = 0; k < n && r == ICCL_SUCCESS; k++) {
+    int to = (c->rank + k) % n, from = (c->rank - k + n) % n;
+    if (rcounts[from]) r = iccl_recv(c, (char*)rbuf + rdispls[from] * elem_bytes, rcounts[from] * elem_bytes, from, s,
+                                     nullptr);
+    if (!r && scounts[to])
+      r = iccl_send(c, (const char*)sbuf + sdispls[to] * elem_bytes, scounts[to] * elem_bytes, to, s, nullptr);
+  }
+  iccl_result_t r2 = iccl_group_end(c);
+  return r ? r : r2;
+}
+
+iccl_result_t iccl_alltoall(iccl_comm_t c, const void* sbuf, void* rbuf, size_t bytes_per_pair, cudaStream_t s) {
+  if (!c) return ICCL_ERR_INVALID_ARGUMENT;
+  ICCL_RETURN_IF(c->nranks < 2, ICCL_ERR_GROUP_TOO_SMALL, "alltoall needs >= 2 ranks (SPEC.md:429)");
+  if (bytes_per_pair == 0) return ICCL_SUCCESS;  // immediate completion
+  std::vector<size_t> cnt(c->nranks, bytes_per_pair), disp(c->nranks);
+  for (int i = 0; i < c->nranks; i++) disp[i] = i * bytes_per_pair;
+  return iccl_alltoallv(c, sbuf, cnt.data(), disp.data(), rbuf, cnt.data(), disp.data(), 1, s);
+}
+
+iccl_result_t iccl_req_test(iccl_comm_t c, iccl_req_t req, int* done) {
+  if (!c || !done) return ICCL_ERR_INVALID_ARGUMENT;
+  uint32_t slot = (uint32_t)(req >> 32), gen = (uint32_t)req;
+  ICCL_RETURN_IF(slot >= (uint32_t)kSlots, ICCL_ERR_UNKNOWN_WR, "bad request handle");
+  *done = cyc_geq(__atomic_load_n(&flags_of(c, c->rank)->done[slot], __ATOMIC_ACQUIRE), gen) ? 1 : 0;
+  int ae = c->async_err.load();
+  if (!*done && ae != ICCL_SUCCESS) {
+    set_last_error(c->async_msg);
+    return (iccl_result_t)ae;
+  }
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_req_wait(iccl_comm_t c, iccl_req_t req, int64_t timeout_us) {
+  uint64_t t0 = now_ns();
+  for (;;) {
+    int done = 0;
+    iccl_result_t r = iccl_req_test(c, req, &done);
+    if (r) return r;
+    if (done) return ICCL_SUCCESS;
+    if (timeout_us >= 0 && (now_ns() - t0) > (uint64_t)timeout_us * 1000ull) {
+      set_last_error("request wait timed out");
+      return ICCL_ERR_TIMEOUT;
+    }
+    sched_yield();
+  }
+}
+
+iccl_result_t iccl_req_state(iccl_comm_t c, iccl_req_t req, iccl_xfer_state_t* st) {
+  if (!c || !st) return ICCL_ERR_INVALID_ARGUMENT;
+  int done = 0;
+  iccl_result_t r = iccl_req_test(c, req, &done);
+  if (r) return r;
+  memset(st, 0, sizeof(*st));
+  st->total_chunks = -1;
+  if (done) {
+    st->posted = st->transmitted = st->acked = st->r_posted = st->received = st->done = -1;  // complete
+    st->total_chunks = 0;
+  }
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_path_switch(iccl_comm_t c, int peer, int to) {
+  if (!c || peer < 0 || peer >= c->nranks || (to != 0 && to != 1)) return ICCL_ERR_INVALID_ARGUMENT;
+  c->path_req[peer].store(to);
+  c->qcv.notify_one();
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_path_active(iccl_comm_t c, int peer, int* path) {
+  if (!c || !path || peer < 0 || peer >= c->nranks) return ICCL_ERR_INVALID_ARGUMENT;
+  *path = c->active_path_pub[peer].load();
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_fault_set(iccl_comm_t c, const iccl_fault_t* f, int n) {
+  if (!c || (n > 0 && !f) || n < 0) return ICCL_ERR_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> g(c->fault_mu);
+  c->faults.clear();
+  for (int i = 0; i < n; i++) {
+    ICCL_RETURN_IF(f[i].src < 0 || f[i].src >= c->nranks || f[i].dst < 0 || f[i].dst >= c->nranks,
+                   ICCL_ERR_INVALID_ARGUMENT, "fault names an unknown path (UnknownPort)");
+    c->faults.push_back(Fault{f[i], false});
+  }
+  c->faults_t0 = now_ns();
+  for (auto& chn : c->ch) chn.sends_seen = 0;
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_switch_events(iccl_comm_t c, iccl_switch_event_t* ev, int max, int* n) {
+  if (!c || !n || max < 0) return ICCL_ERR_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> g(c->mon_mu);
+  int k = 0;
+  while (k < max && !c->sw_events.empty()) {
+    ev[k++] = c->sw_events.front();
+    c->sw_events.pop_front();
+  }
+  *n = k;
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_gather_rows(const void* src, void* dst, const int64_t* idx, int64_t n_rows, int64_t row_bytes,
+                               int ctas, cudaStream_t s) {
+  if ((n_rows > 0 && (!src || !dst || !idx)) || n_rows < 0 || row_bytes <= 0) return ICCL_ERR_INVALID_ARGUMENT;
+  ICCL_CHECK_CUDA(launch_gather_rows(src, dst, idx, n_rows, row_bytes, ctas > 0 ? ctas : 148 * 8, s));
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_scatter_rows(const void* src, void* dst, const int64_t* idx, int64_t n_rows, int64_t row_bytes,
+                                int ctas, cudaStream_t s) {
+  if ((n_rows > 0 && (!src || !dst || !idx)) || n_rows < 0 || row_bytes <= 0) return ICCL_ERR_INVALID_ARGUMENT;
+  ICCL_CHECK_CUDA(launch_scatter_rows(src, dst, idx, n_rows, row_bytes, ctas > 0 ? ctas : 148 * 8, s));
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_copy_sm(const void* src, void* dst, size_t bytes, int ctas, cudaStream_t s) {
+  if (bytes > 0 && (!src || !dst)) return ICCL_ERR_INVALID_ARGUMENT;
+  ICCL_CHECK_CUDA(launch_copy(src, dst, bytes, ctas > 0 ? ctas : 16, nullptr, s));
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_monitor_config(iccl_comm_t c, int enabled, int window) {
+  if (!c || window < 1) return ICCL_ERR_INVALID_ARGUMENT;
+  c->monitor_enabled.store(enabled ? 1 : 0);
+  c->cfg.monitor_window = window;
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_monitor_read(iccl_comm_t c, iccl_mon_rec_t* recs, int max, int* n) {
+  if (!c || !n || max < 0 || (max > 0 && !recs)) return ICCL_ERR_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> g(c->mon_mu);
+  int k = 0;
+  while (k < max && !c->mon.empty()) {
+    recs[k++] = c->mon.front();
+    c->mon.pop_front();
+  }
+  *n = k;
+  return ICCL_SUCCESS;
+}
+
+}  // extern "C"

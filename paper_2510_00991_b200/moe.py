@@ -1,0 +1,100 @@
+"""MoE expert-parallel dispatch / combine over the alltoallv path (config 4).
+
+dispatch: route every (token, expert) pair to the rank owning the expert —
+K2 packs the routed rows by destination rank (``iccl_gather_rows``), the
+alltoallv moves them, received rows arrive grouped by source rank.
+combine: the reverse alltoallv with the same counts, then K3 scatters the
+rows back to (token, k) order (``iccl_scatter_rows``).  The routing metadata
+(a 32 K-entry argsort) is computed with torch; the bytes move only through
+libiccl_b200.so kernels and copy engines.  PAPER.md:157, 864-868.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional
+
+import torch
+
+from ._lib import lib
+from .errors import InvalidArgument, raise_for
+
+
+def _sh(stream: Optional[torch.cuda.Stream]) -> C.c_void_p:
+    s = stream or torch.cuda.current_stream()
+    return C.c_void_p(int(s.cuda_stream))
+
+
+def gather_rows(src: torch.Tensor, idx: torch.Tensor, out: Optional[torch.Tensor] = None, ctas: int = 0,
+                stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """out[i] = src[idx[i]] (K2)."""
+    if idx.dtype != torch.int64 or not idx.is_cuda:
+        raise InvalidArgument("idx must be a CUDA int64 tensor")
+    n = idx.numel()
+    if out is None:
+        out = torch.empty((n,) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+    row = src[0].numel() * src.element_size() if src.shape[0] else out[0].numel() * out.element_size()
+    raise_for(lib.iccl_gather_rows(C.c_void_p(src.data_ptr()), C.c_void_p(out.data_ptr()), C.c_void_p(idx.data_ptr()),
+                                   n, row, int(ctas), _sh(stream)), "iccl_gather_rows")
+    return out
+
+
+def scatter_rows(src: torch.Tensor, idx: torch.Tensor, out: torch.Tensor, ctas: int = 0,
+                 stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """out[idx[i]] = src[i] (K3)."""
+    if idx.dtype != torch.int64 or not idx.is_cuda:
+        raise InvalidArgument("idx must be a CUDA int64 tensor")
+    n = idx.numel()
+    row = out[0].numel() * out.element_size()
+    raise_for(lib.iccl_scatter_rows(C.c_void_p(src.data_ptr()), C.c_void_p(out.data_ptr()), C.c_void_p(idx.data_ptr()),
+                                    n, row, int(ctas), _sh(stream)), "iccl_scatter_rows")
+    return out
+
+
+@dataclass
+class DispatchPlan:
+    order: torch.Tensor          # [T*k] int64: flattened (token, k) index of each packed row
+    token_of_row: torch.Tensor   # [T*k] int64: token index of each packed row
+    send_counts: List[int]       # rows to each rank
+    recv_counts: List[int]       # rows from each rank
+
+
+def plan_dispatch(expert_ids: torch.Tensor, n_experts: int, world: int, counts_exchange) -> DispatchPlan:
+    """expert_ids: [T, k] int64 on the GPU.  Experts are laid out contiguously
+    per rank (n_experts / world each).  ``counts_exchange(send_counts) ->
+    recv_counts`` is the one exchange step of the alltoallv."""
+    T, k = expert_ids.shape
+    per_rank = n_experts // world
+    flat = expert_ids.reshape(-1)
+    dest = torch.div(flat, per_rank, rounding_mode="floor")
+    # stable sort by (destination rank, expert) keeps token order inside a segment
+    key = flat
+    order = torch.sort(key, stable=True).indices
+    counts = torch.bincount(dest, minlength=world).tolist()
+    recv = counts_exchange(counts)
+    return DispatchPlan(order, torch.div(order, k, rounding_mode="floor"), counts, recv)
+
+
+def moe_dispatch(comm, tokens: torch.Tensor, plan: DispatchPlan, packed: Optional[torch.Tensor] = None,
+                 recv: Optional[torch.Tensor] = None, stream=None):
+    """tokens [T, H] -> rows received from every rank, grouped by source."""
+    packed = gather_rows(tokens, plan.token_of_row, packed, stream=stream)
+    if recv is None:
+        recv = torch.empty((sum(plan.recv_counts),) + tuple(tokens.shape[1:]), dtype=tokens.dtype,
+                           device=tokens.device)
+    comm.alltoallv(recv, packed, plan.recv_counts, plan.send_counts, stream=stream)
+    return packed, recv
+
+
+def moe_combine(comm, expert_out: torch.Tensor, plan: DispatchPlan, T: int, k: int,
+                back: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None, stream=None):
+    """Reverse alltoallv with the same counts, then K3 puts every row back at
+    its (token, k) slot: out [T, k, H]."""
+    if back is None:
+        back = torch.empty((sum(plan.send_counts),) + tuple(expert_out.shape[1:]), dtype=expert_out.dtype,
+                           device=expert_out.device)
+    comm.alltoallv(back, expert_out, plan.send_counts, plan.recv_counts, stream=stream)
+    if out is None:
+        out = torch.empty((T * k,) + tuple(expert_out.shape[1:]), dtype=expert_out.dtype, device=expert_out.device)
+    scatter_rows(back, plan.order, out, stream=stream)
+    return out.view(T, k, *expert_out.shape[1:])

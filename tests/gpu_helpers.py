@@ -1,0 +1,69 @@
+"""Helpers for the GPU parity tests: seeded payloads and a multi-process
+launcher (one process per GPU, as in production)."""
+import os
+import socket
+import traceback
+
+import numpy as np
+
+
+def payload(nbytes: int, seed: int) -> np.ndarray:
+    """Uniform random bytes (viewed as fp32 they include NaN/Inf/denormal
+    patterns: parity is raw-byte)."""
+    return np.random.default_rng(seed).integers(0, 256, nbytes, dtype=np.uint8)
+
+
+def to_dev(a: np.ndarray, device):
+    import torch
+    return torch.from_numpy(a.copy()).to(device)
+
+
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, fn, outdir, kwargs):
+    import torch
+    import torch.distributed as dist
+    try:
+        torch.cuda.set_device(rank)
+        store = dist.TCPStore("127.0.0.1", port, world, rank == 0, wait_for_workers=True)
+        from paper_2510_00991_b200 import Communicator, IcclConfig
+        cfg = IcclConfig.defaults(**kwargs.pop("config", {}))
+        comm = Communicator(rank, world, rank, cfg, store=store)
+        res = fn(comm, rank, world, **kwargs)
+        torch.cuda.synchronize()
+        comm.destroy()
+        np.savez(os.path.join(outdir, f"rank{rank}.npz"), **(res or {}))
+    except Exception:
+        with open(os.path.join(outdir, f"rank{rank}.err"), "w") as fh:
+            fh.write(traceback.format_exc())
+        raise
+
+
+def run_ranks(world: int, fn, tmpdir, timeout: float = 240.0, **kwargs):
+    """Run fn(comm, rank, world, **kwargs) -> dict of numpy arrays on `world`
+    GPUs, one process each; returns the per-rank dicts."""
+    import torch.multiprocessing as mp
+    port = free_port()
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_worker, args=(r, world, port, fn, str(tmpdir), dict(kwargs))) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout)
+    errs = []
+    for r, p in enumerate(procs):
+        if p.is_alive():
+            p.kill()
+            errs.append(f"rank {r} timed out")
+        ef = os.path.join(str(tmpdir), f"rank{r}.err")
+        if os.path.exists(ef):
+            errs.append(open(ef).read())
+    if errs:
+        raise AssertionError("\n".join(errs))
+    return [dict(np.load(os.path.join(str(tmpdir), f"rank{r}.npz"))) for r in range(world)]

@@ -1,0 +1,87 @@
+"""Rank programs for the multi-GPU parity tests (picklable top-level
+functions run by gpu_helpers.run_ranks, one process per GPU)."""
+import numpy as np
+import torch
+
+from gpu_helpers import payload, to_dev
+
+
+def sendrecv_pair(comm, rank, world, sizes, offsets=(0,)):
+    """0 -> 1 for each size (and every offset into a larger buffer)."""
+    out = {}
+    dev = torch.device("cuda", rank)
+    for i, n in enumerate(sizes):
+        for off in offsets:
+            src = payload(n + off, seed=1000 + i)
+            if rank == 0:
+                t = to_dev(src, dev)
+                comm.send(t[off:], 1)
+            elif rank == 1:
+                r = torch.zeros(n + off, dtype=torch.uint8, device=dev)
+                comm.recv(r[off:], 0)
+                torch.cuda.synchronize()
+                out[f"r_{n}_{off}"] = r[off:].cpu().numpy()
+    torch.cuda.synchronize()
+    return out
+
+
+def bidirectional(comm, rank, world, nbytes, iters=3):
+    dev = torch.device("cuda", rank)
+    peer = 1 - rank
+    src = to_dev(payload(nbytes, seed=rank), dev)
+    dst = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+    from paper_2510_00991_b200 import P2POp
+    for _ in range(iters):
+        comm.batch_isend_irecv([P2POp("isend", src, peer), P2POp("irecv", dst, peer)])
+    torch.cuda.synchronize()
+    return {"recv": dst.cpu().numpy()}
+
+
+def ring_shift(comm, rank, world, nbytes):
+    dev = torch.device("cuda", rank)
+    from paper_2510_00991_b200 import P2POp
+    src = to_dev(payload(nbytes, seed=50 + rank), dev)
+    dst = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+    comm.batch_isend_irecv([P2POp("isend", src, (rank + 1) % world), P2POp("irecv", dst, (rank - 1) % world)])
+    torch.cuda.synchronize()
+    return {"recv": dst.cpu().numpy()}
+
+
+def alltoallv_uneven(comm, rank, world, row_bytes, splits, seed=7):
+    dev = torch.device("cuda", rank)
+    send_rows = splits[rank]
+    recv_rows = [splits[i][rank] for i in range(world)]
+    src = to_dev(payload(sum(send_rows) * row_bytes, seed=seed + rank), dev).view(-1, row_bytes)
+    dst = torch.zeros(sum(recv_rows), row_bytes, dtype=torch.uint8, device=dev)
+    comm.alltoallv(dst, src, recv_rows, send_rows)
+    torch.cuda.synchronize()
+    return {"recv": dst.cpu().numpy().reshape(-1)}
+
+
+def failover_pair(comm, rank, world, nbytes, fault_chunk, restore_us=0):
+    """0 -> 1 with the primary copy path 0->1 Down at `fault_chunk` of the
+    first send; the transfer must resume on the SM path at the breakpoint."""
+    from paper_2510_00991_b200 import FaultScript
+    dev = torch.device("cuda", rank)
+    src = payload(nbytes, seed=99)
+    fs = FaultScript().down(0, 1, chunk=fault_chunk, op_index=0)
+    if restore_us:
+        fs.up(0, 1, t_us=restore_us)
+    comm.set_faults(fs)
+    out = {}
+    if rank == 0:
+        comm.send(to_dev(src, dev), 1)
+    else:
+        r = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+        comm.recv(r, 0)
+        torch.cuda.synchronize()
+        out["recv"] = r.cpu().numpy()
+    torch.cuda.synchronize()
+    import time
+    time.sleep(0.05)
+    if rank == 0:
+        ev = comm.switch_events()
+        out["switch_to"] = np.array([0 if e["to"] == "primary" else 1 for e in ev], np.int32)
+        out["resume"] = np.array([e["resume_chunk"] for e in ev], np.int32)
+        out["detect_ns"] = np.array([e["detect_ns"] for e in ev], np.int64)
+    return out

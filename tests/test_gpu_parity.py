@@ -1,0 +1,282 @@
+"""GPU parity: the B200 path's delivered bytes against the CPU oracle.
+
+Every comparison is raw-byte (bit-exact).  Single-GPU tests drive the whole
+product path through the C ABI with a world-size-1 communicator (self send /
+recv through the proxy, copy engine, SM kernel, failover and monitor); the
+multi-GPU tests run one process per GPU and skip with fewer GPUs.
+"""
+import numpy as np
+import pytest
+
+from gpu_helpers import payload, run_ranks, to_dev
+from oracle import collectives as oc
+
+pytestmark = pytest.mark.gpu
+
+MiB = 1 << 20
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _comm1(**cfg):
+    from paper_2510_00991_b200 import Communicator, IcclConfig
+    return Communicator(0, 1, 0, IcclConfig.defaults(**cfg))
+
+
+def _oracle_sendrecv(src: np.ndarray) -> np.ndarray:
+    return oc.send_recv(oc.CommGroup(2, chunk_size=4 * MiB), 0, 1, src)
+
+
+def _self_roundtrip(torch, comm, src_np, off_src=0, off_dst=0):
+    from paper_2510_00991_b200 import P2POp
+    n = src_np.nbytes - off_src
+    s = to_dev(src_np, "cuda")
+    d = torch.zeros(n + off_dst, dtype=torch.uint8, device="cuda")
+    comm.batch_isend_irecv([P2POp("isend", s[off_src:], 0), P2POp("irecv", d[off_dst:], 0)])
+    torch.cuda.synchronize()
+    return d[off_dst:].cpu().numpy()
+
+
+@pytest.mark.parametrize("transport", ["ce", "sm"])
+@pytest.mark.parametrize("n", [1, 15, 4096, MiB + 3, 64 * MiB + 17])
+def test_self_sendrecv_bytes(torch_cuda, transport, n):
+    comm = _comm1(transport=transport, chunk_bytes=16 * MiB)
+    try:
+        src = payload(n, seed=n)
+        got = _self_roundtrip(torch_cuda, comm, src)
+        assert np.array_equal(got, _oracle_sendrecv(src))
+        comm.check_async_error()
+    finally:
+        comm.destroy()
+
+
+@pytest.mark.parametrize("offs", [(1, 0), (0, 3), (5, 9), (16, 32)])
+def test_self_sendrecv_misaligned(torch_cuda, offs):
+    comm = _comm1(transport="sm")
+    try:
+        src = payload(3 * MiB + 7, seed=11)
+        got = _self_roundtrip(torch_cuda, comm, src, *offs)
+        assert np.array_equal(got, src[offs[0]:])
+    finally:
+        comm.destroy()
+
+
+def test_self_sendrecv_256mib_property(torch_cuda):
+    """Full PP-activation size (bf16 [4,4096,8192]): checksum-of-chunks property
+    instead of a byte-by-byte oracle run."""
+    torch = torch_cuda
+    comm = _comm1()
+    try:
+        g = torch.Generator(device="cuda").manual_seed(1)
+        s = torch.randint(-32768, 32767, (4, 4096, 8192), dtype=torch.int16, device="cuda", generator=g).view(
+            torch.bfloat16)
+        d = torch.empty_like(s)
+        from paper_2510_00991_b200 import P2POp
+        comm.batch_isend_irecv([P2POp("isend", s, 0), P2POp("irecv", d, 0)])
+        torch.cuda.synchronize()
+        assert torch.equal(s.view(torch.int16), d.view(torch.int16))
+    finally:
+        comm.destroy()
+
+
+def test_sm_copy_kernel_k1(torch_cuda):
+    import ctypes as C
+    from paper_2510_00991_b200._lib import lib
+    torch = torch_cuda
+    for n, so, do in [(1, 0, 0), (17, 1, 1), (33, 3, 7), (1 << 20, 0, 0), ((1 << 24) + 5, 2, 2), ((1 << 24) + 5, 0, 8)]:
+        src = payload(n + so, seed=n)
+        s = to_dev(src, "cuda")
+        d = torch.zeros(n + do, dtype=torch.uint8, device="cuda")
+        rc = lib.iccl_copy_sm(C.c_void_p(s.data_ptr() + so), C.c_void_p(d.data_ptr() + do), n, 16,
+                              C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        assert rc == 0
+        torch.cuda.synchronize()
+        assert np.array_equal(d.cpu().numpy()[do:], src[so:])
+
+
+def test_k2_k3_gather_scatter(torch_cuda):
+    torch = torch_cuda
+    from paper_2510_00991_b200 import gather_rows, scatter_rows
+    rng = np.random.default_rng(5)
+    rows, H = 4096, 7168 * 2  # bf16 hidden 7168 -> 14336 B per row
+    src = payload(rows * H, seed=3).reshape(rows, H)
+    idx = rng.integers(0, rows, 3 * rows)
+    s = to_dev(src, "cuda")
+    i = torch.from_numpy(idx).cuda()
+    g = gather_rows(s, i)
+    torch.cuda.synchronize()
+    assert np.array_equal(g.cpu().numpy(), src[idx])
+    perm = rng.permutation(rows)
+    out = torch.zeros_like(s)
+    scatter_rows(s, torch.from_numpy(perm).cuda(), out)
+    torch.cuda.synchronize()
+    exp = np.zeros_like(src)
+    exp[perm] = src
+    assert np.array_equal(out.cpu().numpy(), exp)
+
+
+def test_self_alltoallv_world1(torch_cuda):
+    torch = torch_cuda
+    comm = _comm1()
+    try:
+        src = to_dev(payload(1000 * 16, seed=2), "cuda").view(1000, 16)
+        dst = torch.zeros_like(src)
+        comm.alltoallv(dst, src, [1000], [1000])
+        torch.cuda.synchronize()
+        assert torch.equal(src, dst)
+    finally:
+        comm.destroy()
+
+
+def test_self_failover_resumes_on_sm_path(torch_cuda):
+    """Inject a Down on the primary (copy-engine) path at chunk 2 of the first
+    send: the watchdog + probe must switch to the SM path and resume at the
+    receiver's breakpoint, bit-exact."""
+    torch = torch_cuda
+    from paper_2510_00991_b200 import FaultScript
+    comm = _comm1(chunk_bytes=MiB, delta_us=200, probe_period_us=100, window=4)
+    try:
+        comm.set_faults(FaultScript().down(0, 0, chunk=2, op_index=0))
+        src = payload(16 * MiB, seed=77)
+        got = _self_roundtrip(torch, comm, src)
+        assert np.array_equal(got, _oracle_sendrecv(src))
+        ev = comm.switch_events()
+        assert ev and ev[0]["to"] == "backup" and ev[0]["trigger"] == "watchdog"
+        assert ev[0]["resume_chunk"] == 2  # chunks 0,1 landed before the gate
+        assert comm.active_path(0) == "backup"
+        # next transfer goes straight over the backup path
+        got = _self_roundtrip(torch, comm, src[::-1].copy())
+        assert np.array_equal(got, src[::-1])
+        comm.check_async_error()
+    finally:
+        comm.destroy()
+
+
+def test_self_failover_switch_back(torch_cuda):
+    torch = torch_cuda
+    from paper_2510_00991_b200 import FaultScript
+    comm = _comm1(chunk_bytes=MiB, delta_us=200, probe_period_us=100)
+    try:
+        comm.set_faults(FaultScript().down(0, 0, chunk=1, op_index=0).up(0, 0, t_us=50_000))
+        src = payload(8 * MiB, seed=78)
+        assert np.array_equal(_self_roundtrip(torch, comm, src), src)
+        import time
+        time.sleep(0.2)
+        assert np.array_equal(_self_roundtrip(torch, comm, src), src)
+        ev = comm.switch_events()
+        assert [e["to"] for e in ev][:2] == ["backup", "primary"]
+        assert comm.active_path(0) == "primary"
+    finally:
+        comm.destroy()
+
+
+def test_api_switch_qp_mid_stream(torch_cuda):
+    torch = torch_cuda
+    comm = _comm1(chunk_bytes=MiB)
+    try:
+        src = payload(32 * MiB, seed=5)
+        comm.switch_qp(0, "ToBackup")
+        assert np.array_equal(_self_roundtrip(torch, comm, src), src)
+        assert comm.active_path(0) == "backup"
+        comm.switch_qp(0, "ToPrimary")
+        assert np.array_equal(_self_roundtrip(torch, comm, src), src)
+    finally:
+        comm.destroy()
+
+
+def test_monitor_records(torch_cuda):
+    torch = torch_cuda
+    from paper_2510_00991_b200 import sample_series
+    comm = _comm1(chunk_bytes=MiB, monitor_enabled=True)
+    try:
+        src = payload(24 * MiB, seed=9)
+        assert np.array_equal(_self_roundtrip(torch, comm, src), src)
+        recs = comm.monitor.drain()
+        assert len(recs) == 24
+        assert sum(r.size for r in recs) == 24 * MiB
+        assert all(r.t2 > r.t1 for r in recs)
+        assert len(sample_series(recs, 8)) == 24 - 8 + 1
+    finally:
+        comm.destroy()
+
+
+def test_errors(torch_cuda):
+    torch = torch_cuda
+    from paper_2510_00991_b200 import GroupTooSmall, InvalidArgument, ZeroLengthMessage
+    comm = _comm1()
+    try:
+        with pytest.raises(ZeroLengthMessage):
+            comm.send(torch.zeros(0, device="cuda"), 0)
+        with pytest.raises(InvalidArgument):
+            comm.send(torch.zeros(4, device="cuda"), 3)
+        with pytest.raises(GroupTooSmall):
+            comm.alltoall(torch.zeros(4, device="cuda"), torch.zeros(4, device="cuda"))
+        assert comm.op_counts() == {0: 0}
+    finally:
+        comm.destroy()
+
+
+# ---------------------------------------------------------------- multi-GPU
+def test_pair_sendrecv_bytes(need_gpus, tmp_path):
+    need_gpus(2)
+    import gpu_scenarios as sc
+    sizes = [8, 4096 + 1, 3 * MiB + 5, 64 * MiB]
+    res = run_ranks(2, sc.sendrecv_pair, tmp_path, sizes=sizes, offsets=(0, 3))
+    for i, n in enumerate(sizes):
+        for off in (0, 3):
+            src = payload(n + off, seed=1000 + i)[off:]
+            assert np.array_equal(res[1][f"r_{n}_{off}"], _oracle_sendrecv(src.copy()))
+
+
+@pytest.mark.parametrize("transport", ["ce", "sm"])
+def test_pair_bidirectional(need_gpus, tmp_path, transport):
+    need_gpus(2)
+    import gpu_scenarios as sc
+    res = run_ranks(2, sc.bidirectional, tmp_path, nbytes=64 * MiB + 48, config=dict(transport=transport))
+    for r in range(2):
+        assert np.array_equal(res[r]["recv"], payload(64 * MiB + 48, seed=1 - r))
+
+
+def test_ring_shift_all_gpus(need_gpus, tmp_path):
+    need_gpus(2)
+    import torch
+    import gpu_scenarios as sc
+    w = torch.cuda.device_count()
+    res = run_ranks(w, sc.ring_shift, tmp_path, nbytes=32 * MiB)
+    for r in range(w):
+        assert np.array_equal(res[r]["recv"], payload(32 * MiB, seed=50 + (r - 1) % w))
+
+
+def test_alltoallv_uneven_vs_oracle(need_gpus, tmp_path):
+    need_gpus(2)
+    import torch
+    import gpu_scenarios as sc
+    w = torch.cuda.device_count()
+    rng = np.random.default_rng(0)
+    splits = [[int(x) for x in rng.integers(0, 300, w)] for _ in range(w)]
+    splits[0][w - 1] = 0  # a zero-count pair
+    row = 7168 * 2
+    res = run_ranks(w, sc.alltoallv_uneven, tmp_path, row_bytes=row, splits=splits)
+    send = [payload(sum(splits[i]) * row, seed=7 + i) for i in range(w)]
+    exp = oc.expected_alltoallv(send, splits, row)
+    orc = oc.alltoallv(oc.CommGroup(w, chunk_size=4 * MiB), send, splits, oc.counts_T(splits), row)
+    for r in range(w):
+        assert np.array_equal(exp[r], orc[r])
+        assert np.array_equal(res[r]["recv"], exp[r])
+
+
+def test_pair_failover_mid_message(need_gpus, tmp_path):
+    need_gpus(2)
+    import gpu_scenarios as sc
+    n = 48 * MiB
+    res = run_ranks(2, sc.failover_pair, tmp_path, nbytes=n, fault_chunk=5,
+                    config=dict(chunk_bytes=4 * MiB, delta_us=300, window=4))
+    assert np.array_equal(res[1]["recv"], _oracle_sendrecv(payload(n, seed=99)))
+    assert list(res[0]["switch_to"])[:1] == [1]
+    assert res[0]["resume"][0] == 5

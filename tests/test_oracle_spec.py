@@ -1,0 +1,311 @@
+"""The oracle against every SPEC example on the hot path."""
+import numpy as np
+import pytest
+from hypothesis import given, settings, strategies as st
+
+from oracle import collectives as co
+from oracle import monitor as mo
+from oracle import pipeline as pl
+from oracle import transport as tr
+from oracle.des import Simulator
+from oracle.netsim import FaultScript, Link, Network, allocate_bandwidth, path_port, relay_gpu
+from oracle.verbs import (CompletionQueue, Direction, MemoryRegion, QpInErrorState, UnregisteredRegion, Verbs,
+                          WcStatus, WorkRequest, retry_timeout_ns)
+
+MiB = 1 << 20
+
+
+def test_G1_G2_G3_retry_timeout():
+    assert retry_timeout_ns(18, 7) == 8_589_934_592
+    assert retry_timeout_ns(0, 0) == 4096
+    assert retry_timeout_ns(18, 0) == 1_073_741_824
+
+
+def _one_link(cap_bps=400e9, delay=2000):
+    sim = Simulator()
+    net = Network(sim)
+    link = net.add_port(Link("l", cap_bps, delay))
+    return sim, net, Verbs(sim, net), link
+
+
+def test_G4_post_send_timing():  # 83.886 + 4 us
+    sim, net, v, link = _one_link()
+    scq, rcq = CompletionQueue(), CompletionQueue()
+    qp = v.create_qp([link], "Primary", scq, rcq)
+    src = MemoryRegion(1, 0, np.arange(4 * MiB, dtype=np.uint8))
+    dst = MemoryRegion(2, 1, np.zeros(4 * MiB, np.uint8))
+    v.post_recv(qp, WorkRequest(v.new_wr_id(), Direction.RECV, dst, 0, 4 * MiB))
+    v.post_send(qp, WorkRequest(v.new_wr_id(), Direction.SEND, src, 0, 4 * MiB))
+    sim.run()
+    wc = scq.poll(10)
+    assert len(wc) == 1 and wc[0].status == WcStatus.SUCCESS
+    assert abs(wc[0].t2 - 87_886) <= 1
+    assert (dst.data == src.data).all()
+    assert scq.poll(2) == []  # empty CQ -> []
+
+
+def test_verbs_errors():
+    sim, net, v, link = _one_link()
+    qp = v.create_qp([link], "Primary", CompletionQueue(), CompletionQueue())
+    r = MemoryRegion(1, 0, np.zeros(16, np.uint8), registered=False)
+    with pytest.raises(UnregisteredRegion):
+        v.post_send(qp, WorkRequest(1, Direction.SEND, r, 0, 16))
+    v.flush(qp)
+    with pytest.raises(QpInErrorState):
+        v.post_send(qp, WorkRequest(2, Direction.SEND, MemoryRegion(2, 0, np.zeros(16, np.uint8)), 0, 16))
+
+
+def test_post_during_down_retry_exceeded():
+    sim, net, v, link = _one_link()
+    scq, rcq = CompletionQueue(), CompletionQueue()
+    qp = v.create_qp([link], "Primary", scq, rcq, timeout_exponent=2, retry_count=1)
+    net.set_link(link, False)
+    src = MemoryRegion(1, 0, np.zeros(1024, np.uint8))
+    dst = MemoryRegion(2, 1, np.zeros(1024, np.uint8))
+    v.post_recv(qp, WorkRequest(v.new_wr_id(), Direction.RECV, dst, 0, 1024))
+    wr = WorkRequest(v.new_wr_id(), Direction.SEND, src, 0, 1024)
+    v.post_send(qp, wr)
+    sim.run()
+    wcs = scq.poll(10)
+    assert [w.status for w in wcs] == [WcStatus.RETRY_EXCEEDED]
+    assert wcs[0].wr_id == wr.wr_id and wcs[0].t2 == retry_timeout_ns(2, 1)
+    assert [w.status for w in rcq.poll(10)] == [WcStatus.FLUSHED]
+
+
+def test_poll_cq_fifo():
+    cq = CompletionQueue()
+    from oracle.verbs import WorkCompletion
+    for i in range(3):
+        cq.push(WorkCompletion(i, WcStatus.SUCCESS, i, 1))
+    assert [w.wr_id for w in cq.poll(2)] == [0, 1]
+    assert [w.wr_id for w in cq.poll(5)] == [2]
+
+
+def test_G5_chunking_and_pointers():
+    g = co.CommGroup(2, chunk_size=4 * MiB)
+    x = np.random.default_rng(0).integers(0, 255, 1 << 30, dtype=np.uint8) if False else None
+    n = 256 * 4 * MiB
+    src = np.zeros(n, np.uint8)
+    src[::4096] = 7
+    out = co.send_recv(g, 0, 1, src)
+    st = g.conns[(0, 1)].xfer.state()
+    assert st["total_chunks"] == 256
+    assert st["sender"] == dict(posted=256, transmitted=256, acked=256)
+    assert st["receiver"]["done"] == 256
+    assert (out == src).all()
+    del x
+
+
+def test_G6_zero_length():
+    g = co.CommGroup(2)
+    c = g.conn(0, 1)
+    r = g.region(0, np.zeros(8, np.uint8))
+    with pytest.raises(tr.ZeroLengthMessage):
+        c.send_message(r, r, 0)
+
+
+def test_G7_zero_copy_vs_staged():  # SPEC.md:235, AC1 (>= 15% with BufferCopy = 25% of the cycle)
+    def run(mode):
+        g = co.CommGroup(2, nvlink_gbps=50.0, window=64)
+        cyc = int(4 * MiB / 50.0)  # ns of wire time per chunk at 50 GB/s
+        # BufferCopy = 25% of the staged chunk cycle: copy = wire / 3
+        g.kw["mode"] = tr.PipelineMode(mode, prep_ns=0, buffer_copy_ns=cyc // 3)
+        co.send_recv(g, 0, 1, np.zeros(64 * 4 * MiB, np.uint8))
+        return g.sim.now
+    staged = run(tr.Mode.STAGED_COPY)
+    zero = run(tr.Mode.ZERO_COPY)
+    assert zero <= 0.8 * staged  # SPEC.md:235 (AC1 asks >= 15% throughput gain)
+
+
+def test_G8_G10_on_wc():
+    g = co.CommGroup(2, chunk_size=1024)
+    src = np.arange(4096, dtype=np.uint8)
+    co.send_recv(g, 0, 1, src)
+    c = g.conns[(0, 1)]
+    from oracle.verbs import WorkCompletion
+    with pytest.raises(tr.UnknownWr):  # duplicate Success
+        c.on_wc(WorkCompletion(999, WcStatus.SUCCESS, 0, 1024, 0, c.primary[0].qp_id), "Sender")
+    assert c.on_wc(WorkCompletion(1, WcStatus.RETRY_EXCEEDED, 0, 0, 1, c.primary[0].qp_id), "Sender") \
+        == tr.Action.TRIGGER_SWITCH  # G9
+
+
+def test_G14_G15_switch_pointers():
+    r = tr.ReceiverPointers(posted=10, received=8, done=6)
+    s = tr.SenderPointers(posted=10, transmitted=9, acked=5)
+    assert tr.switch_pointers(r, s) == 6
+    assert (r.received, s.acked, s.transmitted, s.posted) == (6, 6, 6, 6)
+    r = tr.ReceiverPointers(posted=4, received=4, done=4)
+    s = tr.SenderPointers(posted=4, transmitted=4, acked=4)
+    assert tr.switch_pointers(r, s) == 4  # done == total: nothing to resend
+
+
+def _fail_run(down_at, up_at=None, size=64 * MiB, chunk=4 * MiB, delta=20_000, period=10_000, probe_only=False):
+    f = FaultScript([(down_at, path_port(0, 1, 0), False)] + ([(up_at, path_port(0, 1, 0), True)] if up_at else []))
+    g = co.CommGroup(2, chunk_size=chunk, delta_ns=delta, probe_period_ns=period, faults=f,
+                     timeout_exponent=10 if probe_only else 0, retry_count=7 if probe_only else 0,
+                     cts_timeout_ns=delta if probe_only else 0)
+    src = np.random.default_rng(down_at).integers(0, 255, size, dtype=np.uint8)
+    out = co.send_recv(g, 0, 1, src)
+    return g, g.conns[(0, 1)], src, out
+
+
+def test_failover_sender_trigger_exactly_once():  # Fig. 7(a)
+    g, c, src, out = _fail_run(30_000)
+    assert (out == src).all()
+    assert c.switches[0][1] == "ToBackup" and c.switches[0][3] == "sender-wc"
+    assert c.delivered_sequence == list(range(16))
+
+
+def test_failover_receiver_cts_trigger():  # Fig. 7(b); SPEC.md:253 (retry budget >> delta)
+    g, c, src, out = _fail_run(30_000, probe_only=True, delta=10_000)
+    assert (out == src).all()
+    assert c.switches[0][3] == "receiver-cts"
+    lines = [l for l in g.sim.trace.lines() if ",cts_" in l]
+    assert any("cts_fail" in l for l in lines)
+
+
+def test_G11_innocent_stall_no_switch():
+    g = co.CommGroup(2, delta_ns=5_000)
+    src = np.arange(MiB, dtype=np.uint8)
+    out = co.send_recv(g, 0, 1, src, ready_at=50_000)  # sender blocked upstream for 50 us
+    c = g.conns[(0, 1)]
+    assert (out == src).all()
+    assert c.switches == []
+    assert any("cts_ok" in l for l in g.sim.trace.lines())
+
+
+def test_G13_below_delta_no_action():
+    g = co.CommGroup(2, delta_ns=1_000_000)
+    c = g.conn(0, 1)
+    r = g.region(0, np.zeros(4096, np.uint8))
+    c.send_message(r, g.region(1, np.zeros(4096, np.uint8)), 4096)
+    assert c.check_receiver_timeout(g.sim.now + 1_000_000 - 1) == tr.Action.NO_ACTION
+    g.sim.run()
+
+
+def test_G16_G17_switch_back_on_restore():
+    g, c, src, out = _fail_run(30_000, up_at=100_000, size=256 * MiB, period=25_000)
+    assert (out == src).all()
+    dirs = [s[1] for s in c.switches]
+    assert dirs == ["ToBackup", "ToPrimary"]
+    t_back = c.switches[1][0]
+    assert 100_000 < t_back <= 100_000 + 25_000 + 2 * 1000 + 1
+    assert c.delivered_sequence == list(range(64))
+
+
+def test_both_paths_dead_connection_failed():
+    f = FaultScript([(10_000, path_port(0, 1, 0), False), (10_000, path_port(0, 1, 1), False)])
+    g = co.CommGroup(2, faults=f)
+    with pytest.raises(tr.ConnectionFailed):
+        co.send_recv(g, 0, 1, np.zeros(64 * MiB, np.uint8))
+
+
+def test_G18_to_G24_monitor():
+    R = tr.MessageRecord
+    assert mo.per_message_throughput(MiB, 0, 50_000) == pytest.approx(20.97152e9)
+    with pytest.raises(mo.NonPositiveDuration):
+        mo.per_message_throughput(MiB, 5, 5)
+    w = [R(i, MiB, 0, 100_000) for i in range(4)]
+    assert mo.window_throughput(w, 4) == pytest.approx(41.94304e9)
+    with pytest.raises(mo.WindowNotFull):
+        mo.window_throughput(w[:3], 4)
+    one = [R(0, MiB, 10, 50_010)]
+    assert mo.window_throughput(one, 1) == mo.per_message_throughput(MiB, 10, 50_010)
+    steady = [R(i, MiB, i * 1000, (i + 1) * 1000) for i in range(20)]
+    assert all(s.value == pytest.approx(MiB / 1e-6) for s in mo.sample_series(steady, 8))
+    assert len(mo.sample_series(steady[:10], 8)) == 3
+    assert len(mo.sample_series(steady[:5], 8)) == 0
+
+
+def test_G25_G27_lagging_rank():
+    assert mo.detect_lagging_rank({0: 100, 1: 100, 2: 97, 3: 100}, 1) == 2
+    assert mo.detect_lagging_rank({0: 5, 1: 5, 2: 5}, 1) is None
+    assert mo.detect_lagging_rank({0: 50, 1: 50, 2: 49}, 2) is None
+
+
+def test_G28_G29_G30_alltoall():
+    with pytest.raises(co.GroupTooSmall):
+        co.alltoall(co.CommGroup(1), [np.zeros(8, np.uint8)], 8)
+    out = co.alltoall(co.CommGroup(2), [np.zeros(0, np.uint8)] * 2, 0)
+    assert all(o.nbytes == 0 for o in out)
+    a, b = np.arange(16, dtype=np.uint8), np.arange(16, 32, dtype=np.uint8)
+    out = co.alltoall(co.CommGroup(2), [a, b], 8)
+    assert (out[0] == np.concatenate([a[:8], b[:8]])).all()  # == bidirectional send/recv
+    assert (out[1] == np.concatenate([a[8:], b[8:]])).all()
+
+
+def test_G31_G32_gemm_duration():
+    assert pl.gemm_duration(10.0, {}) == 10.0
+    assert pl.gemm_duration(10.0, {"p2p": 0.25}) == pytest.approx(13.333333)
+    with pytest.raises(pl.NoSmAvailable):
+        pl.gemm_duration(10.0, {"p2p": 1.0})
+
+
+def test_G37_max_min():
+    from oracle.netsim import Flow
+    big = Link("big", 400e9, 0)
+    small = Link("small", 100e9, 0)
+    f1 = Flow(1, [big, small], 1, None, 0)
+    f2 = Flow(2, [big], 1, None, 0)
+    f3 = Flow(3, [big], 1, None, 0)
+    r = allocate_bandwidth([f1, f2, f3])
+    gbps = {k: v * 8 for k, v in r.items()}  # bytes/ns -> Gb/s
+    assert gbps[1] == pytest.approx(100) and gbps[2] == pytest.approx(150) and gbps[3] == pytest.approx(150)
+    r = allocate_bandwidth([Flow(4, [big], 1, None, 0), Flow(5, [big], 1, None, 0)])
+    assert all(v * 8 == pytest.approx(200) for v in r.values())
+
+
+def test_G38_down_window_delivers_nothing():
+    sim = Simulator()
+    net = Network(sim)
+    link = net.add_port(Link("p", 8e9, 0))  # 1 byte/ns
+    net.apply_fault("p", False, 4_000)
+    net.apply_fault("p", True, 19_000)
+    done = []
+    net.start_flow([link], 10_000, lambda t: done.append(t))
+    sim.run()
+    assert done == [10_000 + 15_000]
+
+
+def test_relay_choice():
+    assert relay_gpu(8, 3, 5) == 0
+    assert relay_gpu(8, 0, 1) == 2
+    assert relay_gpu(8, 0, 1, busy=[2]) == 3
+
+
+def test_alltoallv_matches_closed_form():
+    rng = np.random.default_rng(3)
+    n = 4
+    splits = [[int(v) for v in rng.integers(0, 40, n)] for _ in range(n)]
+    splits[1][2] = 0  # zero-count pair skipped (Appendix B9)
+    send = [rng.integers(0, 255, sum(s) * 32, dtype=np.uint8) for s in splits]
+    out = co.alltoallv(co.CommGroup(n, chunk_size=256), send, splits, co.counts_T(splits), 32)
+    exp = co.expected_alltoallv(send, splits, 32)
+    assert all((a == b).all() for a, b in zip(out, exp))
+
+
+def test_determinism_trace_hash():  # AC9
+    def run():
+        g, c, src, out = _fail_run(30_000)
+        return g.trace_sha256()
+    assert run() == run()
+
+
+@settings(max_examples=60, deadline=None)
+@given(size=st.integers(1024, 8 * MiB), fault_frac=st.floats(0.0, 1.2), chunk_pow=st.integers(14, 21),
+       restore=st.booleans(), seed=st.integers(0, 2**31))
+def test_AC3_fuzz_failover_exactly_once(size, fault_frac, chunk_pow, restore, seed):
+    """AC3 at desk scale: random sizes, fault times and chunking;
+    bytes equal and the done sequence is a gapless, duplicate-free 0..N-1."""
+    chunk = 1 << chunk_pow
+    wire_ns = int(size / 900.0) + 2000
+    down = int(wire_ns * fault_frac)
+    entries = [(down, path_port(0, 1, 0), False)]
+    if restore:
+        entries.append((down + wire_ns, path_port(0, 1, 0), True))
+    g = co.CommGroup(2, chunk_size=chunk, delta_ns=5_000, probe_period_ns=3_000, faults=FaultScript(entries))
+    src = np.random.default_rng(seed).integers(0, 255, size, dtype=np.uint8)
+    out = co.send_recv(g, 0, 1, src)
+    c = g.conns[(0, 1)]
+    assert (out == src).all()
+    assert c.delivered_sequence == list(range(tr.n_chunks(size, chunk)))
