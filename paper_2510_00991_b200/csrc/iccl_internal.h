@@ -66,6 +66,33 @@ struct alignas(64) KernelStamp {
 cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, KernelStamp* stamp, cudaStream_t st);
 // Force-load every kernel (see iccl_kernels.cu: lazy loading vs parked streams).
 cudaError_t preload_kernels();
+// K5: low-latency (LL) eager path for small messages.  8-byte lines
+// {4 B payload, 4 B sequence flag} written straight into a per-pair slot ring
+// in the receiver's GPU memory; one fused kernel per stream progresses every
+// LL op of a group concurrently (one CTA per op), so group members never wait
+// on each other through stream order.
+constexpr int kLLSlots = 4;               // slots per ordered pair (flow-control window)
+constexpr size_t kLLMaxBytes = 32 * 1024; // largest LL message
+constexpr size_t kLLLines = kLLMaxBytes / 4;
+constexpr int kLLMaxOps = 64;             // LL ops per launch
+struct LLDesc {
+  int kind;               // 0 send, 1 recv
+  uint32_t seq;           // 1-based message number on this ordered pair
+  uint64_t bytes;
+  char* buf;              // send: source; recv: destination
+  void* slot;             // uint2[kLLLines]: peer's slot (send) / my slot (recv)
+  unsigned int* credit;   // send: my credit word for the peer (local);
+                          // recv: the sender's credit word for me (peer-mapped)
+  unsigned int* done_flag;  // op's done slot in the control block (host-mapped)
+  uint32_t done_gen;
+};
+struct LLBatch {
+  int n;
+  unsigned int* error;    // host-mapped: set to 1 if a wait timed out
+  LLDesc d[kLLMaxOps];
+};
+cudaError_t launch_ll(const LLBatch& b, cudaStream_t st);
+
 // K4 stamp: which = 0 writes stamp->t1, which = 1 writes stamp->t2 (release).
 cudaError_t launch_stamp(KernelStamp* stamp, int which, cudaStream_t st);
 // Calibration: write %globaltimer into *out (host-mapped).

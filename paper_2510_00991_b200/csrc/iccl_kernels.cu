@@ -230,9 +230,84 @@ __global__ void __launch_bounds__(256) iccl_gather_rows_multi(const int4* __rest
   }
 }
 
+// K5: LL eager path.  Block b serves op b of the batch.  A send writes every
+// 4-byte word of its payload as an 8-byte {word, seq} line into the peer's
+// slot (one 8-byte store: data and flag become visible together, no fence);
+// a recv polls each of its lines until the flag equals seq, stores the word,
+// and when the whole block is done returns a credit to the sender.  Waits
+// give up after 10 s (error flag) instead of hanging the GPU.
+__device__ __forceinline__ bool ll_timed_out(unsigned long long t0) {
+  return globaltimer() - t0 > 10000000000ull;
+}
+
+__global__ void __launch_bounds__(256) iccl_ll_group(LLBatch b) {
+  const LLDesc& d = b.d[blockIdx.x];
+  const unsigned long long t0 = globaltimer();
+  const size_t lines = (d.bytes + 3) / 4;
+  uint2* slot = (uint2*)d.slot;
+  if (d.kind == 0) {
+    if (d.seq > (uint32_t)kLLSlots) {
+      if (threadIdx.x == 0) {
+        const uint32_t need = d.seq - kLLSlots;
+        uint32_t c;
+        do {
+          asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(c) : "l"(d.credit) : "memory");
+          if (ll_timed_out(t0)) {
+            *b.error = 1;
+            break;
+          }
+        } while ((int32_t)(c - need) < 0);
+      }
+      __syncthreads();
+    }
+    for (size_t i = threadIdx.x; i < lines; i += blockDim.x) {
+      uint32_t w = 0;
+      const size_t off = i * 4;
+      if (off + 4 <= d.bytes && ((uintptr_t)(d.buf + off) & 3) == 0) {
+        w = *(const uint32_t*)(d.buf + off);
+      } else {
+        for (int k = 0; k < 4 && off + k < d.bytes; k++) w |= (uint32_t)(unsigned char)d.buf[off + k] << (8 * k);
+      }
+      asm volatile("st.volatile.global.v2.u32 [%0], {%1, %2};" ::"l"(slot + i), "r"(w), "r"(d.seq) : "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && d.done_flag)
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(d.done_flag), "r"(d.done_gen) : "memory");
+  } else {
+    for (size_t i = threadIdx.x; i < lines; i += blockDim.x) {
+      uint32_t w, f;
+      do {
+        asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(w), "=r"(f) : "l"(slot + i) : "memory");
+        if (f != d.seq && ll_timed_out(t0)) {
+          *b.error = 1;
+          break;
+        }
+      } while (f != d.seq);
+      const size_t off = i * 4;
+      if (off + 4 <= d.bytes && ((uintptr_t)(d.buf + off) & 3) == 0) {
+        *(uint32_t*)(d.buf + off) = w;
+      } else {
+        for (int k = 0; k < 4 && off + k < d.bytes; k++) d.buf[off + k] = (char)(w >> (8 * k));
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(d.credit), "r"(d.seq) : "memory");
+      if (d.done_flag)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(d.done_flag), "r"(d.done_gen) : "memory");
+    }
+  }
+}
+
 bool smem_configured = false;
 
 }  // namespace
+
+cudaError_t launch_ll(const LLBatch& b, cudaStream_t st) {
+  if (b.n <= 0) return cudaSuccess;
+  iccl_ll_group<<<b.n, 256, 0, st>>>(b);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, KernelStamp* stamp, cudaStream_t st) {
   if (bytes == 0) return cudaSuccess;
@@ -268,7 +343,8 @@ cudaError_t preload_kernels() {
   cudaFuncAttributes a;
   const void* fns[] = {(const void*)iccl_copy_tma,   (const void*)iccl_copy_unaligned, (const void*)iccl_stamp,
                        (const void*)iccl_read_globaltimer, (const void*)iccl_gather_rows,
-                       (const void*)iccl_scatter_rows, (const void*)iccl_gather_rows_multi};
+                       (const void*)iccl_scatter_rows, (const void*)iccl_gather_rows_multi,
+                       (const void*)iccl_ll_group};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;

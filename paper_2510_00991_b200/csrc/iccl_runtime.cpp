@@ -53,7 +53,6 @@ constexpr uint64_t kMagic = 0x3030324242434349ull;  // "ICCLB200"
 constexpr int kSlots = 4096;                        // op slots per rank (ready/done flags)
 constexpr int kCtsDepth = 1024;                     // recv postings in flight per ordered pair
 constexpr int kMaxRanks = 64;
-constexpr int kMaxStreams = 8;
 constexpr int kGateWords = 1024;
 constexpr int kStampSlots = 4096;
 constexpr size_t kScratchBytes = 4096;
@@ -73,12 +72,28 @@ struct alignas(64) RankInfo {
   int32_t dev;
   char bus_id[32];
   cudaIpcMemHandle_t scratch_handle;
+  cudaIpcMemHandle_t ll_handle;
   std::atomic<uint64_t> op_count;  // opCount
+};
+
+// Six-pointer view of one op, published by the sender's
+// proxy into both endpoints' slots so either side's iccl_req_state sees it.
+struct XferPub {
+  uint32_t gen;       // op generation this record belongs to
+  int32_t kind;       // 0 send, 1 recv (written by the owner's API thread)
+  int32_t total;      // chunks
+  int32_t posted;     // sender posted == transmitted (handed to an engine)
+  int32_t done;       // contiguous delivered prefix: receiver done == sender acked
+  int32_t path;
+  int32_t switches;
+  int32_t pad;
+  uint64_t bytes;
 };
 
 struct alignas(64) RankFlags {
   uint32_t ready[kSlots];  // written by the owner's user stream
   uint32_t done[kSlots];   // written by the copy stream that completes the op
+  XferPub pub[kSlots];
 };
 
 struct alignas(64) CtsEntry {
@@ -137,6 +152,8 @@ struct OpDesc {
   size_t bytes;
   uint32_t slot, gen;
   uint64_t op_seq;
+  bool ll = false;   // small message on the LL kernel path (K5)
+  uint32_t ll_seq = 0;
 };
 
 struct ChunkRec {
@@ -237,6 +254,11 @@ struct iccl_comm {
   unsigned long long* gtimer = nullptr;
   int64_t gtimer_offset = 0;  // host_ns - globaltimer_ns
   char* scratch = nullptr;    // device scratch (probe target), exported to peers
+  // LL path (K5): slot rings for every source rank + credit words, in my HBM
+  char* ll_region = nullptr;
+  std::vector<char*> peer_ll;
+  std::vector<uint32_t> ll_sent, ll_recvd;
+  unsigned int* ll_error = nullptr;  // host-mapped
   // API state
   uint64_t op_seq = 0;
   int group_depth = 0;
@@ -326,6 +348,22 @@ static void put_events(iccl_comm* c, std::vector<ChunkRec>& recs) {
       c->event_pool.push_back(r.ev);
       r.ev = nullptr;
     }
+}
+
+static void publish_one(XferPub& p, uint32_t gen, const Xfer& x) {
+  p.total = x.nchunks;
+  p.posted = x.next_issue;
+  p.done = x.completed;
+  p.path = x.path;
+  p.switches = x.switches;
+  p.bytes = x.bytes;
+  __atomic_store_n(&p.gen, gen, __ATOMIC_RELEASE);
+}
+
+// Mirror the transfer's pointers into the sender's and the receiver's op slot.
+static void publish(iccl_comm* c, Channel& chn, const Xfer& x) {
+  publish_one(flags_of(c, c->rank)->pub[x.s_slot], x.s_gen, x);
+  publish_one(flags_of(c, chn.peer)->pub[x.r_done_slot], x.r_done_gen, x);
 }
 
 static int alloc_gate(iccl_comm* c) {
@@ -531,6 +569,7 @@ static iccl_result_t switch_path(iccl_comm* c, Channel& chn, int to, int trigger
     x.switches++;
     if (had_work && stale_gate >= 0) x.pending_gate = stale_gate;
     x.last_progress = now_ns();
+    publish(c, chn, x);
   }
   if (stale_gate >= 0) {
     // future work on the still-Down path waits on a fresh gate epoch; the old
@@ -659,6 +698,7 @@ static iccl_result_t progress_channel(iccl_comm* c, Channel& chn, bool* busy) {
       *busy = true;
     }
     if (&x == &chn.xfers.front()) rr->st.done.store(x.completed);
+    publish(c, chn, x);
   }
   // 3. retire completed xfers (their done writes are queued on the device)
   while (!chn.xfers.empty()) {
@@ -695,6 +735,7 @@ static iccl_result_t progress_channel(iccl_comm* c, Channel& chn, bool* busy) {
       x.next_issue++;
       outstanding++;
       *busy = true;
+      publish(c, chn, x);
     }
     if (x.next_issue < x.nchunks) break;
   }
@@ -796,6 +837,8 @@ static void proxy_loop(iccl_comm* c) {
       }
     }
     if (c->hdr->abort.load()) set_async(c, ICCL_ERR_ABORTED, "communicator aborted");
+    if (c->ll_error && __atomic_load_n(c->ll_error, __ATOMIC_ACQUIRE))
+      set_async(c, ICCL_ERR_TIMEOUT, "LL kernel wait exceeded 10 s (peer never posted the matching op)");
     if (busy) idle_since = now_ns();
   }
 }
@@ -890,12 +933,16 @@ static iccl_result_t do_post_cts(iccl_comm* c, int peer, void* buf, size_t bytes
   return ICCL_SUCCESS;
 }
 
-static iccl_result_t stream_markers(iccl_comm* c, cudaStream_t s, const std::vector<OpDesc>& ops) {
-  // WriteValue(ready) for every op, then WaitValue(done) for every op, batched.
+// Stream markers of copy-engine ops: phase 0 = WriteValue(ready) for every
+// op, phase 1 = WaitValue(done) for every op; LL kernels of the same group go
+// between the two phases (ready first, so no peer ever waits on our LL kernel
+// through our stream order).
+static iccl_result_t stream_markers(iccl_comm* c, cudaStream_t s, const std::vector<OpDesc>& ops, int phases = 3) {
   RankFlags* mine = flags_of(c, c->rank);
   std::vector<CUstreamBatchMemOpParams> p;
   p.reserve(2 * ops.size());
   for (const OpDesc& op : ops) {
+    if (!(phases & 1)) break;
     CUstreamBatchMemOpParams w;
     memset(&w, 0, sizeof(w));
     w.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
@@ -905,6 +952,7 @@ static iccl_result_t stream_markers(iccl_comm* c, cudaStream_t s, const std::vec
     p.push_back(w);
   }
   for (const OpDesc& op : ops) {
+    if (!(phases & 2)) break;
     CUstreamBatchMemOpParams w;
     memset(&w, 0, sizeof(w));
     w.waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
@@ -916,6 +964,44 @@ static iccl_result_t stream_markers(iccl_comm* c, cudaStream_t s, const std::vec
   for (size_t i = 0; i < p.size(); i += 128) {
     unsigned n = (unsigned)std::min<size_t>(128, p.size() - i);
     ICCL_CHECK_CU(driver()->cuStreamBatchMemOp((CUstream)s, n, p.data() + i, 0));
+  }
+  return ICCL_SUCCESS;
+}
+
+static size_t ll_slot_offset(int src, uint32_t seq) {
+  return ((size_t)src * kLLSlots + (seq - 1) % kLLSlots) * kLLLines * 8;
+}
+static size_t ll_credit_offset(int nranks, int peer) {
+  return (size_t)nranks * kLLSlots * kLLLines * 8 + (size_t)peer * 64;
+}
+
+// One fused K5 launch per (stream, group): every LL op of the group gets its
+// own CTA, so sends and recvs progress concurrently.
+static iccl_result_t launch_ll_ops(iccl_comm* c, cudaStream_t s, const std::vector<OpDesc>& ops) {
+  RankFlags* mine = flags_of(c, c->rank);
+  for (size_t i = 0; i < ops.size(); i += kLLMaxOps) {
+    LLBatch b;
+    memset(&b, 0, sizeof(b));
+    b.error = c->ll_error;
+    for (size_t j = i; j < ops.size() && b.n < kLLMaxOps; j++) {
+      const OpDesc& op = ops[j];
+      LLDesc& d = b.d[b.n++];
+      d.kind = op.kind;
+      d.seq = op.ll_seq;
+      d.bytes = op.bytes;
+      d.buf = (char*)op.src;
+      if (op.kind == 0) {
+        d.slot = c->peer_ll[op.peer] + ll_slot_offset(c->rank, op.ll_seq);
+        d.credit = (unsigned int*)(c->ll_region + ll_credit_offset(c->nranks, op.peer));
+      } else {
+        d.slot = c->ll_region + ll_slot_offset(op.peer, op.ll_seq);
+        d.credit = (unsigned int*)(c->peer_ll[op.peer] + ll_credit_offset(c->nranks, c->rank));
+      }
+      d.done_flag = &mine->done[op.slot];
+      d.done_gen = op.gen;
+    }
+    ICCL_CHECK_CUDA(launch_ll(b, s));
+    c->kernels_launched += 1;
   }
   return ICCL_SUCCESS;
 }
@@ -938,7 +1024,19 @@ static iccl_result_t enqueue_op(iccl_comm* c, int kind, const void* buf, size_t 
   op.bytes = bytes;
   iccl_result_t r = next_slot(c, &op.slot, &op.gen, &op.op_seq);
   if (r) return r;
-  if (kind == 1) {
+  {
+    XferPub& p = flags_of(c, c->rank)->pub[op.slot];
+    __atomic_store_n(&p.gen, 0u, __ATOMIC_RELEASE);
+    p.kind = kind;
+  }
+  // Small messages between different GPUs take the LL kernel path (K5) unless
+  // the copy-engine transport is forced; both sides classify by the same byte
+  // count, so the k-th LL send of a pair always meets the k-th LL recv.
+  op.ll = peer != c->rank && c->cfg.transport != ICCL_TRANSPORT_CE && bytes <= c->cfg.sm_small_bytes &&
+          bytes <= kLLMaxBytes && c->ll_region != nullptr;
+  if (op.ll) {
+    op.ll_seq = kind == 0 ? ++c->ll_sent[peer] : ++c->ll_recvd[peer];
+  } else if (kind == 1) {
     r = do_post_cts(c, peer, (void*)buf, bytes, op.slot, op.gen);
     if (r) return r;
   }
@@ -948,6 +1046,7 @@ static iccl_result_t enqueue_op(iccl_comm* c, int kind, const void* buf, size_t 
     c->group_ops.emplace_back(op, s);
     return ICCL_SUCCESS;
   }
+  if (op.ll) return launch_ll_ops(c, s, {op});
   r = stream_markers(c, s, {op});
   if (r) return r;
   if (kind == 0) {
@@ -1051,6 +1150,17 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
   me.dev = cuda_dev;
   cudaDeviceGetPCIBusId(me.bus_id, sizeof(me.bus_id), cuda_dev);
   ICCL_CHECK_CUDA(cudaIpcGetMemHandle(&me.scratch_handle, c->scratch));
+  {
+    size_t ll_bytes = ll_credit_offset(nranks, nranks);
+    ICCL_CHECK_CUDA(cudaMalloc((void**)&c->ll_region, ll_bytes));
+    ICCL_CHECK_CUDA(cudaMemset(c->ll_region, 0, ll_bytes));
+    ICCL_CHECK_CUDA(cudaIpcGetMemHandle(&me.ll_handle, c->ll_region));
+    c->ll_error = (unsigned int*)((char*)c->pinned + 56 * 1024);
+    c->ll_sent.assign(nranks, 0);
+    c->ll_recvd.assign(nranks, 0);
+    c->peer_ll.assign(nranks, nullptr);
+    ICCL_CHECK_CUDA(cudaDeviceSynchronize());
+  }
   if (rank == 0) {
     c->hdr->nranks = nranks;
     c->hdr->magic = kMagic;
@@ -1102,6 +1212,9 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
       void* ps = nullptr;
       ICCL_CHECK_CUDA(cudaIpcOpenMemHandle(&ps, c->ranks[p].scratch_handle, cudaIpcMemLazyEnablePeerAccess));
       chn.peer_scratch = (char*)ps + 16 * (1 + rank);
+      void* pl = nullptr;
+      ICCL_CHECK_CUDA(cudaIpcOpenMemHandle(&pl, c->ranks[p].ll_handle, cudaIpcMemLazyEnablePeerAccess));
+      c->peer_ll[p] = (char*)pl;
     }
   }
   // %globaltimer -> CLOCK_MONOTONIC offset for SM-path monitor stamps
@@ -1139,6 +1252,9 @@ static void teardown(iccl_comm* c) {
     for (auto& kv : chn.ipc) cudaIpcCloseMemHandle(kv.second);
     if (chn.peer != c->rank && chn.peer_scratch) cudaIpcCloseMemHandle(chn.peer_scratch - 16 * (1 + c->rank));
   }
+  for (size_t p = 0; p < c->peer_ll.size(); p++)
+    if (c->peer_ll[p] && (int)p != c->rank) cudaIpcCloseMemHandle(c->peer_ll[p]);
+  if (c->ll_region) cudaFree(c->ll_region);
   if (c->scratch) cudaFree(c->scratch);
   if (c->shm) {
     cudaHostUnregister(c->shm);
@@ -1159,6 +1275,15 @@ iccl_result_t iccl_comm_destroy(iccl_comm_t c) {
     if (now_ns() - t0 > 120ull * 1000000000ull) break;
     usleep(50);
   }
+  if (c->proxy.joinable()) {
+    c->stop.store(true);
+    c->qcv.notify_one();
+    c->proxy.join();
+  }
+  // Injected faults may still hold probes behind a closed gate; no data copy
+  // is gated any more (stale copies are flushed before their op completes),
+  // so open every gate and let the side streams drain.
+  for (int g = 0; g < kGateWords; g++) __atomic_store_n((uint32_t*)&c->gate_words[g], 1u, __ATOMIC_SEQ_CST);
   for (auto& sc : c->streams) cudaStreamSynchronize(sc.s);
   iccl_result_t r = c->hdr->abort.load() ? ICCL_SUCCESS : shm_barrier(c);
   teardown(c);
@@ -1264,16 +1389,19 @@ iccl_result_t iccl_group_end(iccl_comm_t c) {
   for (auto& p : ops)
     if (std::find(order.begin(), order.end(), p.second) == order.end()) order.push_back(p.second);
   for (cudaStream_t s : order) {
-    std::vector<OpDesc> v;
+    std::vector<OpDesc> ce, ll;
     for (auto& p : ops)
-      if (p.second == s) v.push_back(p.first);
-    iccl_result_t r = stream_markers(c, s, v);
+      if (p.second == s) (p.first.ll ? ll : ce).push_back(p.first);
+    iccl_result_t r = ICCL_SUCCESS;
+    if (!ce.empty()) r = stream_markers(c, s, ce, 1);  // ready
+    if (!r && !ll.empty()) r = launch_ll_ops(c, s, ll);
+    if (!r && !ce.empty()) r = stream_markers(c, s, ce, 2);  // done waits
     if (r) return r;
   }
   {
     std::lock_guard<std::mutex> g(c->qmu);
     for (auto& p : ops)
-      if (p.first.kind == 0) {
+      if (p.first.kind == 0 && !p.first.ll) {
         c->pending_xfers.fetch_add(1);
         c->inbox.push_back(p.first);
       }
@@ -1344,12 +1472,25 @@ iccl_result_t iccl_req_state(iccl_comm_t c, iccl_req_t req, iccl_xfer_state_t* s
   int done = 0;
   iccl_result_t r = iccl_req_test(c, req, &done);
   if (r) return r;
+  // Six pointers from the record the sender's proxy
+  // publishes.  Zero-copy: posted == transmitted on the sender, and the
+  // receiver's received == done (bytes land in the user buffer directly), so
+  // the six collapse to posted / done, with acked == done.
   memset(st, 0, sizeof(*st));
-  st->total_chunks = -1;
-  if (done) {
-    st->posted = st->transmitted = st->acked = st->r_posted = st->received = st->done = -1;  // complete
-    st->total_chunks = 0;
-  }
+  uint32_t slot = (uint32_t)(req >> 32), gen = (uint32_t)req;
+  const XferPub& p = flags_of(c, c->rank)->pub[slot];
+  bool have = __atomic_load_n(&p.gen, __ATOMIC_ACQUIRE) == gen;
+  st->role = p.kind;
+  st->total_chunks = have ? p.total : -1;
+  st->bytes = have ? p.bytes : 0;
+  int posted = have ? p.posted : 0, dn = have ? p.done : 0;
+  if (done && have) posted = dn = p.total;
+  st->posted = st->transmitted = posted;
+  st->acked = dn;
+  st->r_posted = have ? p.total : 0;
+  st->received = st->done = dn;
+  st->active_path = have ? p.path : 0;
+  st->switches = have ? p.switches : 0;
   return ICCL_SUCCESS;
 }
 

@@ -58,6 +58,38 @@ def alltoallv_uneven(comm, rank, world, row_bytes, splits, seed=7):
     return {"recv": dst.cpu().numpy().reshape(-1)}
 
 
+def ll_mixed(comm, rank, world, sizes, rounds=3):
+    """Small (LL kernel) and large (copy engine) messages interleaved in one
+    group per round, both directions, more LL messages per pair than LL slots."""
+    from paper_2510_00991_b200 import P2POp
+    dev = torch.device("cuda", rank)
+    peer = 1 - rank
+    out = {}
+    for rd in range(rounds):
+        ops, recvs = [], []
+        for i, n in enumerate(sizes):
+            s = to_dev(payload(n, seed=10_000 * rank + 100 * rd + i), dev)
+            r = torch.zeros(n + 3, dtype=torch.uint8, device=dev)[3:]  # misaligned destination
+            ops += [P2POp("isend", s, peer), P2POp("irecv", r, peer)]
+            recvs.append(r)
+        comm.batch_isend_irecv(ops)
+        torch.cuda.synchronize()
+        for i, r in enumerate(recvs):
+            out[f"r{rd}_{i}"] = r.cpu().numpy()
+    for i, n in enumerate(sizes):  # single (ungrouped) LL ops, ordered send/recv
+        s = to_dev(payload(n, seed=555 + i), dev)
+        r = torch.zeros(n, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            comm.send(s, 1)
+            comm.recv(r, 1)
+        else:
+            comm.recv(r, 0)
+            comm.send(s, 0)
+        torch.cuda.synchronize()
+        out[f"single_{i}"] = r.cpu().numpy()
+    return out
+
+
 def failover_pair(comm, rank, world, nbytes, fault_chunk, restore_us=0):
     """0 -> 1 with the primary copy path 0->1 Down at `fault_chunk` of the
     first send; the transfer must resume on the SM path at the breakpoint."""

@@ -271,6 +271,20 @@ def test_alltoallv_uneven_vs_oracle(need_gpus, tmp_path):
         assert np.array_equal(res[r]["recv"], exp[r])
 
 
+def test_pair_ll_small_messages(need_gpus, tmp_path):
+    need_gpus(2)
+    import gpu_scenarios as sc
+    sizes = [1, 3, 4, 7, 64, 1000, 4096, 32 * 1024, 32 * 1024 + 1, 300 * 1024, 5, 6, 8, 9]
+    res = run_ranks(2, sc.ll_mixed, tmp_path, sizes=sizes, config=dict(sm_small_bytes=32 * 1024))
+    for r in range(2):
+        peer = 1 - r
+        for rd in range(3):
+            for i, n in enumerate(sizes):
+                assert np.array_equal(res[r][f"r{rd}_{i}"], payload(n, seed=10_000 * peer + 100 * rd + i)), (r, rd, n)
+        for i, n in enumerate(sizes):
+            assert np.array_equal(res[r][f"single_{i}"], payload(n, seed=555 + i))
+
+
 def test_pair_failover_mid_message(need_gpus, tmp_path):
     need_gpus(2)
     import gpu_scenarios as sc
