@@ -428,7 +428,8 @@ def main():
     ap.add_argument("--bytes", type=int, default=256 * MiB)
     ap.add_argument("--transport", choices=["auto", "ce", "sm"], default="auto")
     ap.add_argument("--chunk-bytes", type=int, default=0)
-    ap.add_argument("--monitor", type=int, default=1)
+    # (not "--monitor": torchrun's parser would take that abbreviation as its own)
+    ap.add_argument("--iccl-monitor", dest="monitor", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -1,21 +1,25 @@
 #!/usr/bin/env python
 """Config 2: send/recv bandwidth + latency sweep, 8 B .. 1 GiB, 2 ranks on
-2 x B200: the ICCL copy-engine path, the ICCL SM path (K1) and same-box NCCL
-(torch.distributed, NCCL 2.28.9) — the comparison the paper makes
-(PAPER.md:640-666).
+2 x B200: the ICCL copy-engine path, the ICCL SM path (K1 / LL kernel) and
+same-box NCCL (torch.distributed, NCCL 2.28.9) — the comparison the paper
+makes.
 
-Bandwidth: K back-to-back 0->1 sends, per-op time = device time / K (max over
-ranks, nccl-tests style).  Latency: half the 0->1->0 ping-pong round trip on
-rank 0's stream, p50 over repetitions.
+Two regimes per size, both nccl-tests style (device time, max over ranks):
+* ``gpu``: the whole loop is enqueued behind a ~30 ms device sleep, so the
+  GPU runs the ops back to back — per-op device time, host API cost hidden;
+* ``api``: plain loop — includes the host cost of every call when the host
+  cannot run ahead.
+Bandwidth: K back-to-back 0->1 sends; latency: half the 0->1->0 ping-pong,
+from the difference of two loop lengths (cancels the start skew).
 
     python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \
-        benchmarks/p2p_sweep.py --impl iccl-ce --out gpurun_out/sweep_ce.jsonl
+        benchmarks/p2p_sweep.py --impl iccl-ce
 """
 import argparse
 import json
 import os
-import statistics
 import sys
+import time
 
 import torch
 import torch.distributed as dist
@@ -28,8 +32,10 @@ def main():
     ap.add_argument("--impl", choices=["iccl-ce", "iccl-sm", "iccl-auto", "nccl"], required=True)
     ap.add_argument("--min-pow", type=int, default=3)
     ap.add_argument("--max-pow", type=int, default=30)
+    ap.add_argument("--step", type=int, default=1)
     ap.add_argument("--out", default="")
     ap.add_argument("--chunk-bytes", type=int, default=0)
+    ap.add_argument("--ll-bytes", type=int, default=-1)
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -43,69 +49,79 @@ def main():
         cfg = iccl.IcclConfig.defaults(transport=args.impl.split("-")[1])
         if args.chunk_bytes:
             cfg.chunk_bytes = args.chunk_bytes
+        if args.ll_bytes >= 0:
+            cfg.sm_small_bytes = args.ll_bytes
         comm = iccl.init(rank, world, local, cfg)
 
     def send(t):
-        if comm:
-            comm.send(t, peer)
-        else:
-            dist.send(t, peer)
+        comm.send(t, peer) if comm else dist.send(t, peer)
 
     def recv(t):
-        if comm:
-            comm.recv(t, peer)
-        else:
-            dist.recv(t, peer)
+        comm.recv(t, peer) if comm else dist.recv(t, peer)
 
     maxb = 1 << args.max_pow
-    buf = torch.randint(0, 255, (maxb,), dtype=torch.uint8, device=dev)
+    g = torch.Generator(device=dev).manual_seed(7)
+    buf = torch.randint(0, 255, (maxb,), dtype=torch.uint8, device=dev, generator=g)
     rbuf = torch.zeros(maxb, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
-    out = []
-    for p in range(args.min_pow, args.max_pow + 1):
-        n = 1 << p
-        s, r = buf[:n], rbuf[:n]
-        iters = 200 if n <= (1 << 20) else (50 if n <= (64 << 20) else 20)
-        # bandwidth: rank 0 -> rank 1, back to back
-        for _ in range(5):
-            send(s) if rank == 0 else recv(r)
+    cycles_per_ms = 1.9e6  # ~1.9 GHz
+
+    def timed(fn, iters, pre_sleep):
         torch.cuda.synchronize()
         dist.barrier()
+        if pre_sleep:
+            torch.cuda._sleep(int(30 * cycles_per_ms))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(iters):
-            send(s) if rank == 0 else recv(r)
+            fn()
         e1.record(stream)
         torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1) / iters], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        bw_us = float(t.item()) * 1e3
-        # latency: ping-pong
-        lat = []
-        for rep in range(7):
-            dist.barrier()
-            torch.cuda.synchronize()
-            e0.record(stream)
-            k = max(5, iters // 5)
-            for _ in range(k):
-                if rank == 0:
-                    send(s)
-                    recv(r)
-                else:
-                    recv(r)
-                    send(s)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            lat.append(e0.elapsed_time(e1) * 1e3 / (2 * k))
-        ok = True
+        return e0.elapsed_time(e1) * 1e3  # us
+
+    def bw_loop(s, r):
+        return lambda: send(s) if rank == 0 else recv(r)
+
+    def pp_loop(s, r):
+        def f():
+            if rank == 0:
+                send(s)
+                recv(r)
+            else:
+                recv(r)
+                send(s)
+        return f
+
+    out = []
+    for p in range(args.min_pow, args.max_pow + 1, args.step):
+        n = 1 << p
+        s, r = buf[:n], rbuf[:n]
+        iters = 100 if n <= (4 << 20) else (30 if n <= (64 << 20) else 10)
+        for _ in range(3):
+            pp_loop(s, r)()
+        rec = {"impl": args.impl, "bytes": n}
+        for mode, pre in (("gpu", True), ("api", False)):
+            t = torch.tensor([timed(bw_loop(s, r), iters, pre) / iters], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            per_op = float(t.item())
+            k1, k2 = max(4, iters // 4), max(12, iters)
+            t1 = timed(pp_loop(s, r), k1, pre)
+            t2 = timed(pp_loop(s, r), k2, pre)
+            lat = (t2 - t1) / (2 * (k2 - k1))
+            rec[f"{mode}_us_per_op"] = round(per_op, 3)
+            rec[f"{mode}_GBps"] = round(n / per_op / 1e3, 2)
+            rec[f"{mode}_lat_us"] = round(lat, 3)
+        torch.cuda.synchronize()
         if rank == 1:
-            ok = bool(torch.equal(r, buf[:n]))  # same seed on both ranks? no: compare checksum below
-        rec = {"impl": args.impl, "bytes": n, "bw_us": round(bw_us, 3), "GBps": round(n / bw_us / 1e3, 2),
-               "lat_p50_us": round(statistics.median(lat), 3)}
+            ok = torch.equal(rbuf[:n], buf[:n])
+            okt = torch.tensor([1 if ok else 0], device=dev)
+        else:
+            okt = torch.tensor([1], device=dev)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        rec["bit_exact"] = bool(okt.item())
         out.append(rec)
         if rank == 0:
             print(json.dumps(rec), flush=True)
-        del ok
     if comm:
         st = comm.stats()
         if rank == 0:
@@ -117,6 +133,7 @@ def main():
                 fh.write(json.dumps(rec) + "\n")
     dist.barrier()
     dist.destroy_process_group()
+    del time
 
 
 if __name__ == "__main__":

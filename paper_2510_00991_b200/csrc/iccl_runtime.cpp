@@ -201,6 +201,7 @@ struct FaultState {
   bool down = false;
   int gate = -1;        // gate word index while down
   uint64_t down_at = 0;  // ns
+  std::vector<int> probe_gates;  // probes parked while down: released on Up
 };
 
 struct Channel {
@@ -215,6 +216,7 @@ struct Channel {
   std::unordered_map<uint64_t, char*> ipc;  // receiver buffer_id -> mapped base
   // probe state
   bool probe_out = false;
+  int probe_gate = -1;
   uint32_t probe_ticket_expect = 0;
   uint64_t probe_sent = 0;
   int probe_path = 0;
@@ -422,6 +424,14 @@ static int stream_for(iccl_comm* c, Channel& chn, int path, int engine, int k) {
   return cand[k % cand.size()];
 }
 
+static void fault_up(iccl_comm* c, FaultState& fs) {
+  fs.down = false;
+  release_gate(c, fs.gate);
+  fs.gate = -1;
+  for (int g : fs.probe_gates) release_gate(c, g);
+  fs.probe_gates.clear();
+}
+
 static void fire_time_faults(iccl_comm* c) {
   std::lock_guard<std::mutex> g(c->fault_mu);
   uint64_t t = now_ns();
@@ -436,9 +446,7 @@ static void fire_time_faults(iccl_comm* c) {
       fs.gate = alloc_gate(c);
       fs.down_at = t;
     } else if (f.f.up && fs.down) {
-      fs.down = false;
-      release_gate(c, fs.gate);
-      fs.gate = -1;
+      fault_up(c, fs);
     }
   }
 }
@@ -455,9 +463,7 @@ static void fire_chunk_faults(iccl_comm* c, Channel& chn, int op_index, int chun
       fs.gate = alloc_gate(c);
       fs.down_at = now_ns();
     } else if (f.f.up && fs.down) {
-      fs.down = false;
-      release_gate(c, fs.gate);
-      fs.gate = -1;
+      fault_up(c, fs);
     }
   }
 }
@@ -584,17 +590,32 @@ static iccl_result_t switch_path(iccl_comm* c, Channel& chn, int to, int trigger
   PairState& ps = ring_of(c, c->rank, chn.peer)->st;
   ps.active_path.store(to);
   ps.switches.fetch_add(1);
+  if (chn.probe_gate >= 0) release_gate(c, chn.probe_gate);  // abandon the outstanding probe
+  chn.probe_gate = -1;
   chn.probe_out = false;
   chn.last_probe = now_ns();
   push_switch_event(c, chn.peer, to, resume, trigger, detect);
   return ICCL_SUCCESS;
 }
 
+// A probe never stays parked on the device: while the path is Down it waits on
+// its own gate word, which the fault's Up releases (the probe then succeeds)
+// or the proxy releases when it gives up on the probe (result ignored), so no
+// device-wide synchronize can hang on an injected fault.
+static void retire_probe(iccl_comm* c, Channel& chn) {
+  if (chn.probe_gate >= 0) release_gate(c, chn.probe_gate);
+  chn.probe_gate = -1;
+  chn.probe_out = false;
+}
+
 static iccl_result_t send_probe(iccl_comm* c, Channel& chn, int path) {
   const int si = chn.probe_stream;
   StreamCtx& sc = c->streams[si];
+  chn.probe_gate = -1;
   if (chn.fault[path].down) {
-    iccl_result_t r = memop_wait(sc.s, &c->gate_words[chn.fault[path].gate], 1);
+    chn.probe_gate = alloc_gate(c);
+    chn.fault[path].probe_gates.push_back(chn.probe_gate);
+    iccl_result_t r = memop_wait(sc.s, &c->gate_words[chn.probe_gate], 1);
     if (r) return r;
   }
   // a 16-byte zero-payload-ish CTS over the suspect path into the peer's scratch
@@ -759,7 +780,7 @@ static iccl_result_t progress_channel(iccl_comm* c, Channel& chn, bool* busy) {
       } else if (chn.probe_path == chn.active_path) {
         StreamCtx& ps = c->streams[chn.probe_stream];
         if (cyc_geq(*ps.prog, chn.probe_ticket_expect)) {
-          chn.probe_out = false;  // CTS ok: innocent link
+          retire_probe(c, chn);  // CTS ok: innocent link
           x.last_progress = tnow;
         } else if (tnow - chn.probe_sent > delta) {
           // CTS failed: trigger the switch
@@ -781,8 +802,12 @@ static iccl_result_t monitor_failed_link(iccl_comm* c, Channel& chn) {
   StreamCtx& ps = c->streams[chn.probe_stream];
   if (chn.probe_out) {
     if (cyc_geq(*ps.prog, chn.probe_ticket_expect)) {
-      chn.probe_out = false;
-      if (chn.probe_path == 0 && !chn.fault[0].down) return switch_path(c, chn, 0, 2);
+      const bool primary_ok = chn.probe_path == 0;  // the probe crossed the primary path
+      retire_probe(c, chn);
+      if (primary_ok) return switch_path(c, chn, 0, 2);
+    } else if (t - chn.probe_sent > c->cfg.delta_us * 1000ull) {
+      retire_probe(c, chn);  // probe lost: the primary is still down
+      chn.last_probe = t;
     }
     return ICCL_SUCCESS;
   }
