@@ -85,7 +85,8 @@ typedef struct {
   uint64_t probe_period_us;   /* ICCL_PROBE_PERIOD_US monitor_failed_link period */
   uint64_t sm_small_bytes;    /* ICCL_SM_SMALL_BYTES  AUTO: messages <= this use the SM path    */
   int32_t proxy_cpu;          /* ICCL_PROXY_CPU       core to pin the proxy to, -1 = none        */
-  int32_t reserved[7];
+  int32_t relay_slot_mib;     /* ICCL_RELAY_SLOT_MIB  relay backup: staging slot per source (x2)  */
+  int32_t reserved[6];
 } iccl_config_t;
 
 /* Six progress pointers of one transfer (Fig. 6). */

@@ -36,7 +36,8 @@ class Config(C.Structure):
         ("probe_period_us", C.c_uint64),
         ("sm_small_bytes", C.c_uint64),
         ("proxy_cpu", C.c_int32),
-        ("reserved", C.c_int32 * 7),
+        ("relay_slot_mib", C.c_int32),
+        ("reserved", C.c_int32 * 6),
     ]
 
 

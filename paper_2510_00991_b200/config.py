@@ -33,6 +33,7 @@ class IcclConfig:
     probe_period_us: int = 0
     sm_small_bytes: int = 0
     proxy_cpu: int = -1
+    relay_slot_mib: int = 0
 
     @classmethod
     def defaults(cls, **overrides) -> "IcclConfig":
@@ -44,7 +45,8 @@ class IcclConfig:
                   monitor_window=c.monitor_window, monitor_enabled=bool(c.monitor_enabled),
                   backup_kind=inv_b.get(c.backup_kind, "sm"), transport=inv_t.get(c.transport, "auto"),
                   timeout_exponent=c.timeout_exponent, retry_count=c.retry_count, delta_us=c.delta_us,
-                  probe_period_us=c.probe_period_us, sm_small_bytes=c.sm_small_bytes, proxy_cpu=c.proxy_cpu)
+                  probe_period_us=c.probe_period_us, sm_small_bytes=c.sm_small_bytes, proxy_cpu=c.proxy_cpu,
+                  relay_slot_mib=c.relay_slot_mib)
         names = {f.name for f in fields(cls)}
         for k, v in overrides.items():
             if k not in names:
@@ -69,6 +71,7 @@ class IcclConfig:
         c.probe_period_us = int(self.probe_period_us)
         c.sm_small_bytes = int(self.sm_small_bytes)
         c.proxy_cpu = int(self.proxy_cpu)
+        c.relay_slot_mib = int(self.relay_slot_mib)
         return c
 
     def validate(self) -> "IcclConfig":

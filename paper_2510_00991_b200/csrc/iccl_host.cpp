@@ -107,6 +107,7 @@ iccl_result_t iccl_config_init(iccl_config_t* c) {
   c->probe_period_us = 500;      // monitor_failed_link period
   c->sm_small_bytes = 0;
   c->proxy_cpu = -1;
+  c->relay_slot_mib = 32;        // relay backup: 2 x 32 MiB staging per source on the relay GPU
   uint64_t u;
   int32_t i;
   if (env_u64("ICCL_CHUNK_BYTES", &u)) c->chunk_bytes = u;
@@ -123,6 +124,7 @@ iccl_result_t iccl_config_init(iccl_config_t* c) {
   if (env_u64("ICCL_PROBE_PERIOD_US", &u)) c->probe_period_us = u;
   if (env_u64("ICCL_SM_SMALL_BYTES", &u)) c->sm_small_bytes = u;
   if (env_i32("ICCL_PROXY_CPU", &i)) c->proxy_cpu = i;
+  if (env_i32("ICCL_RELAY_SLOT_MIB", &i)) c->relay_slot_mib = i;
   return ICCL_SUCCESS;
 }
 
@@ -142,6 +144,8 @@ iccl_result_t iccl_config_validate(const iccl_config_t* c) {
   ICCL_RETURN_IF(c->timeout_exponent < 0 || c->timeout_exponent > 31 || c->retry_count < 0 || c->retry_count > 7,
                  ICCL_ERR_INVALID_CONFIG, "timeout exponent in [0,31], retry count in [0,7]");
   ICCL_RETURN_IF(c->probe_period_us == 0, ICCL_ERR_INVALID_CONFIG, "probe period must be > 0");
+  ICCL_RETURN_IF(c->relay_slot_mib < 1 || c->relay_slot_mib > 1024, ICCL_ERR_INVALID_CONFIG,
+                 "relay_slot_mib must be in [1, 1024]");
   return ICCL_SUCCESS;
 }
 

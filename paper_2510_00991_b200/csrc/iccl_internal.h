@@ -81,8 +81,9 @@ struct LLDesc {
   uint64_t bytes;
   char* buf;              // send: source; recv: destination
   void* slot;             // uint2[kLLLines]: peer's slot (send) / my slot (recv)
-  unsigned int* credit;   // send: my credit word for the peer (local);
-                          // recv: the sender's credit word for me (peer-mapped)
+  unsigned int* credit;   // kLLSlots per-slot credit words (slot s: seq of the last message
+                          // read from it); send: mine for the peer (local), recv: the
+                          // sender's words for me (peer-mapped)
   unsigned int* done_flag;  // op's done slot in the control block (host-mapped)
   uint32_t done_gen;
 };

@@ -234,8 +234,11 @@ __global__ void __launch_bounds__(256) iccl_gather_rows_multi(const int4* __rest
 // 4-byte word of its payload as an 8-byte {word, seq} line into the peer's
 // slot (one 8-byte store: data and flag become visible together, no fence);
 // a recv polls each of its lines until the flag equals seq, stores the word,
-// and when the whole block is done returns a credit to the sender.  Waits
-// give up after 10 s (error flag) instead of hanging the GPU.
+// and when the whole block is done returns the slot's credit to the sender.
+// Credits are per slot (credit[(seq-1) % kLLSlots] = seq): the CTAs of one
+// launch finish in any order, so a single "last consumed" word could run
+// backwards and let a sender overwrite a slot whose previous message was not
+// read yet.  Waits give up after 10 s (error flag) instead of hanging the GPU.
 __device__ __forceinline__ bool ll_timed_out(unsigned long long t0) {
   return globaltimer() - t0 > 10000000000ull;
 }
@@ -249,9 +252,10 @@ __global__ void __launch_bounds__(256) iccl_ll_group(LLBatch b) {
     if (d.seq > (uint32_t)kLLSlots) {
       if (threadIdx.x == 0) {
         const uint32_t need = d.seq - kLLSlots;
+        const unsigned int* cw = d.credit + (d.seq - 1) % kLLSlots;
         uint32_t c;
         do {
-          asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(c) : "l"(d.credit) : "memory");
+          asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(c) : "l"(cw) : "memory");
           if (ll_timed_out(t0)) {
             *b.error = 1;
             break;
@@ -292,7 +296,8 @@ __global__ void __launch_bounds__(256) iccl_ll_group(LLBatch b) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(d.credit), "r"(d.seq) : "memory");
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(d.credit + (d.seq - 1) % kLLSlots), "r"(d.seq)
+                   : "memory");
       if (d.done_flag)
         asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(d.done_flag), "r"(d.done_gen) : "memory");
     }

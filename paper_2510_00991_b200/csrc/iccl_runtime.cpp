@@ -38,6 +38,7 @@
 #include <condition_variable>
 #include <cstring>
 #include <deque>
+#include <map>
 #include <mutex>
 #include <random>
 #include <string>
@@ -73,6 +74,8 @@ struct alignas(64) RankInfo {
   char bus_id[32];
   cudaIpcMemHandle_t scratch_handle;
   cudaIpcMemHandle_t ll_handle;
+  cudaIpcMemHandle_t relay_handle;  // staging slots of this rank as a relay (valid if relay_slot_bytes)
+  uint64_t relay_slot_bytes;
   std::atomic<uint64_t> op_count;  // opCount
 };
 
@@ -119,8 +122,31 @@ struct alignas(64) CtsRing {
   CtsEntry e[kCtsDepth];
 };
 
+// GPU-relay backup path (SURVEY.md §2.3 N9, §8e "Relay backup"): source s
+// pushes a piece into its staging slot on relay GPU r (hop 1, s's copy
+// engine), r's proxy forwards it into the destination's buffer (hop 2, r's
+// copy engine).  Per relay r and source s: two staging slots, a request ring
+// written by s's proxy, and two device-written piece counters.
+constexpr int kRelayDepth = 64;  // requests in flight per (relay, source)
+constexpr int kRelaySlots = 2;   // staging slots per (relay, source)
+
+struct alignas(64) RelayReq {
+  std::atomic<uint64_t> seq;  // 1-based piece number from this source; published last
+  int32_t dst;
+  uint32_t slot;
+  uint64_t bytes;
+  uint64_t buffer_id;    // destination allocation (owned by rank dst)
+  uint64_t base_offset;  // piece offset inside that allocation
+  cudaIpcMemHandle_t handle;
+};
+
+struct alignas(64) RelayCounter {
+  uint32_t v;  // cyclic piece counter, written by a copy stream (WriteValue), waited on with GEQ
+  uint32_t pad[15];
+};
+
 struct ShmLayout {
-  size_t off_ranks, off_flags, off_rings, total;
+  size_t off_ranks, off_flags, off_rings, off_relay, relay_box, total;
   explicit ShmLayout(int n) {
     size_t o = 4096;
     off_ranks = o;
@@ -131,6 +157,12 @@ struct ShmLayout {
     o = (o + 4095) & ~(size_t)4095;
     off_rings = o;
     o += sizeof(CtsRing) * n * n;
+    o = (o + 4095) & ~(size_t)4095;
+    // per relay rank: in[n], out[n] counters, then req[n][kRelayDepth]
+    off_relay = o;
+    relay_box = sizeof(RelayCounter) * 2 * n + sizeof(RelayReq) * n * kRelayDepth;
+    relay_box = (relay_box + 4095) & ~(size_t)4095;
+    o += relay_box * n;
     total = (o + 4095) & ~(size_t)4095;
   }
 };
@@ -143,7 +175,7 @@ struct UidBlob {
 static inline bool cyc_geq(uint32_t a, uint32_t b) { return (int32_t)(a - b) >= 0; }
 
 // ---------------------------------------------------------------- proxy-side structures
-enum Engine { ENG_CE = 0, ENG_SM = 1 };
+enum Engine { ENG_CE = 0, ENG_SM = 1, ENG_RELAY = 2 };
 
 struct OpDesc {
   int kind;  // 0 send, 1 recv
@@ -159,10 +191,13 @@ struct OpDesc {
 struct ChunkRec {
   int stream = -1;  // index into Channel::stream table
   cudaEvent_t ev = nullptr;  // recorded after the chunk: the WC the proxy polls
+  bool timed = false;        // ev is timing-enabled (monitor on, copy-engine path)
+  cudaEvent_t t1ev = nullptr;  // monitor: device event marking the chunk's start (not owned)
   uint64_t t1 = 0;
   int path = 0;
   int stamp = -1;
   bool done = false;
+  uint32_t relay_q = 0;  // relay path: the chunk's last piece number (its WC: relay out >= relay_q)
 };
 
 struct Xfer {
@@ -175,6 +210,11 @@ struct Xfer {
   uint32_t r_ready_slot = 0, r_ready_gen = 0, r_done_slot = 0, r_done_gen = 0;
   int nchunks = 0;
   size_t chunk = 0;
+  // receiver's buffer as exported in its CTS (the relay forwards into it)
+  uint64_t dst_buffer_id = 0, dst_base_offset = 0;
+  cudaIpcMemHandle_t dst_handle{};
+  int relay_r = -1;          // relay GPU carrying pieces of this op, if any
+  uint32_t relay_last_q = 0;  // last piece pushed through it (completion waits for its hop 2)
   int next_issue = 0;  // sender posted == transmitted (chunks handed to an engine)
   int completed = 0;   // contiguous prefix observed delivered: acked == receiver done
   int path = 0;
@@ -187,6 +227,11 @@ struct Xfer {
   int fault_ops_index = -1;
   std::vector<ChunkRec> rec;
   std::vector<cudaEvent_t> fences;  // events the completion must also wait for
+  // monitor on the copy-engine path: per stream, the last timing event this
+  // op recorded there (a chunk starts where the previous one on its stream
+  // ended, or at the op's anchor recorded right after the ready waits)
+  std::vector<std::pair<int, cudaEvent_t>> last_ev;
+  std::vector<cudaEvent_t> anchors;  // owned timing events (returned at retire)
 };
 
 struct StreamCtx {
@@ -212,6 +257,10 @@ struct Channel {
   std::vector<int> path_streams[2];
   int probe_stream = -1;
   int active_path = 0;
+  // on the backup because the primary failed (watchdog + probe): only then
+  // does monitor_failed_link probe the primary to switch back;
+  // an API switch_qp is sticky until the next API switch
+  bool failed_over = false;
   FaultState fault[2];
   std::unordered_map<uint64_t, char*> ipc;  // receiver buffer_id -> mapped base
   // probe state
@@ -223,6 +272,7 @@ struct Channel {
   uint64_t last_probe = 0;
   int sends_seen = 0;  // for chunk-triggered faults
   char* peer_scratch = nullptr;
+  int relay_rank = -1;  // relay GPU of the backup path: lowest rank not an endpoint (topology.py:140-151 tie-break)
 };
 
 struct Fault {
@@ -261,6 +311,14 @@ struct iccl_comm {
   std::vector<char*> peer_ll;
   std::vector<uint32_t> ll_sent, ll_recvd;
   unsigned int* ll_error = nullptr;  // host-mapped
+  // GPU relay (backup_kind RELAY, >= 3 ranks)
+  char* relay_buf = nullptr;         // my staging: [source][kRelaySlots] x relay_slot_bytes
+  size_t relay_slot_bytes = 0;
+  std::vector<char*> peer_relay;     // staging of relay rank r, mapped on first use
+  std::vector<uint32_t> relay_sent;  // pieces I pushed through relay r
+  std::vector<uint64_t> relay_next;  // next request I (as relay) expect from source s
+  std::vector<int> relay_serve;      // my forwarding stream per source (index into streams)
+  std::map<std::pair<int, uint64_t>, char*> relay_ipc;  // (dst rank, buffer id) -> mapped base
   // API state
   uint64_t op_seq = 0;
   int group_depth = 0;
@@ -288,7 +346,14 @@ struct iccl_comm {
   std::atomic<uint64_t> pending_xfers{0};
   std::atomic<uint64_t> kernels_launched{0}, copies_issued{0}, bytes_issued{0};
   std::vector<cudaEvent_t> event_pool;  // proxy-owned: chunk WC events
+  std::vector<cudaEvent_t> tevent_pool;  // proxy-owned: timing-enabled WC / anchor events (monitor)
   std::vector<cudaEvent_t> all_events;
+  // Device time base of the timing events: base_abs_ns is base_ev's time on
+  // the CLOCK_MONOTONIC scale; re-based to a recent anchor every second so
+  // cudaEventElapsedTime's float ms keeps sub-100 ns precision.
+  cudaEvent_t base_ev = nullptr;
+  int64_t base_abs_ns = 0;
+  std::deque<cudaEvent_t> old_bases;
 };
 
 namespace iccl {
@@ -344,12 +409,34 @@ static cudaEvent_t get_event(iccl_comm* c) {
   return e;
 }
 
-static void put_events(iccl_comm* c, std::vector<ChunkRec>& recs) {
-  for (ChunkRec& r : recs)
+static cudaEvent_t get_tevent(iccl_comm* c) {
+  if (c->tevent_pool.empty()) {
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    c->all_events.push_back(e);
+    return e;
+  }
+  cudaEvent_t e = c->tevent_pool.back();
+  c->tevent_pool.pop_back();
+  return e;
+}
+
+static void put_events(iccl_comm* c, Xfer& x) {
+  for (ChunkRec& r : x.rec)
     if (r.ev) {
-      c->event_pool.push_back(r.ev);
+      (r.timed ? c->tevent_pool : c->event_pool).push_back(r.ev);
       r.ev = nullptr;
     }
+  for (cudaEvent_t e : x.anchors) c->tevent_pool.push_back(e);
+  x.anchors.clear();
+  x.last_ev.clear();
+}
+
+// Absolute (CLOCK_MONOTONIC-scale) ns of a completed timing event.
+static uint64_t event_abs_ns(iccl_comm* c, cudaEvent_t e) {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, c->base_ev, e) != cudaSuccess) return 0;
+  return (uint64_t)(c->base_abs_ns + (int64_t)((double)ms * 1e6));
 }
 
 static void publish_one(XferPub& p, uint32_t gen, const Xfer& x) {
@@ -409,10 +496,106 @@ static int engine_for(iccl_comm* c, size_t bytes) {
   return bytes <= c->cfg.sm_small_bytes ? ENG_SM : ENG_CE;
 }
 
-// Path p of a channel: primary (0) uses the configured engine, backup (1) the other one.
-static int path_engine(iccl_comm* c, int path, size_t bytes) {
+// Path p of a channel: primary (0) uses the configured engine; backup (1)
+// the other one — or, for a copy-engine primary with backup_kind RELAY and a
+// third GPU available, two copy-engine hops through the relay GPU.
+static int path_engine(iccl_comm* c, const Channel& chn, int path, size_t bytes) {
   int prim = engine_for(c, bytes);
-  return path == 0 ? prim : (prim == ENG_CE ? ENG_SM : ENG_CE);
+  if (path == 0) return prim;
+  if (prim == ENG_CE && c->cfg.backup_kind == ICCL_BACKUP_RELAY && chn.relay_rank >= 0 && c->relay_buf)
+    return ENG_RELAY;
+  return prim == ENG_CE ? ENG_SM : ENG_CE;
+}
+
+// ---------------------------------------------------------------- GPU relay
+static RelayCounter* relay_in(iccl_comm* c, int r, int src) {
+  ShmLayout L(c->nranks);
+  return (RelayCounter*)((char*)c->shm + L.off_relay + L.relay_box * r) + src;
+}
+static RelayCounter* relay_out(iccl_comm* c, int r, int src) { return relay_in(c, r, src) + c->nranks; }
+static RelayReq* relay_req(iccl_comm* c, int r, int src, uint64_t q) {
+  ShmLayout L(c->nranks);
+  RelayReq* base = (RelayReq*)((char*)c->shm + L.off_relay + L.relay_box * r + sizeof(RelayCounter) * 2 * c->nranks);
+  return base + (size_t)src * kRelayDepth + (size_t)((q - 1) % kRelayDepth);
+}
+
+static size_t relay_pieces(iccl_comm* c, size_t n) { return (n + c->relay_slot_bytes - 1) / c->relay_slot_bytes; }
+
+// Hop 1 of one chunk: piece by piece into my staging slots on relay rr, each
+// followed by its in-counter write, plus a forwarding request for rr's proxy.
+// Returns ICCL_ERR_IN_PROGRESS (nothing issued) if rr's request ring is full.
+static iccl_result_t relay_push(iccl_comm* c, Channel& chn, Xfer& x, size_t off, size_t n, cudaStream_t s,
+                                ChunkRec& rc) {
+  const int rr = chn.relay_rank, me = c->rank;
+  const uint32_t out_now = __atomic_load_n(&relay_out(c, rr, me)->v, __ATOMIC_ACQUIRE);
+  if ((int32_t)(c->relay_sent[rr] + (uint32_t)relay_pieces(c, n) - out_now) > kRelayDepth) return ICCL_ERR_IN_PROGRESS;
+  if (!c->peer_relay[rr]) {
+    void* p = nullptr;
+    ICCL_CHECK_CUDA(cudaIpcOpenMemHandle(&p, c->ranks[rr].relay_handle, cudaIpcMemLazyEnablePeerAccess));
+    c->peer_relay[rr] = (char*)p;
+  }
+  const size_t slot_bytes = c->relay_slot_bytes;
+  for (size_t p = 0; p < n; p += slot_bytes) {
+    const size_t m = std::min(slot_bytes, n - p);
+    const uint32_t q = ++c->relay_sent[rr];
+    const uint32_t slot = (q - 1) % kRelaySlots;
+    // the slot is free once hop 2 of piece q - kRelaySlots has read it
+    if (q > (uint32_t)kRelaySlots) {
+      iccl_result_t r = memop_wait(s, &relay_out(c, rr, me)->v, q - kRelaySlots);
+      if (r) return r;
+    }
+    char* stage = c->peer_relay[rr] + ((size_t)me * kRelaySlots + slot) * slot_bytes;
+    ICCL_CHECK_CU(driver()->cuMemcpyDtoDAsync((CUdeviceptr)stage, (CUdeviceptr)(x.src + off + p), m, (CUstream)s));
+    iccl_result_t r = memop_write(s, &relay_in(c, rr, me)->v, q);
+    if (r) return r;
+    RelayReq* rq = relay_req(c, rr, me, q);
+    rq->dst = chn.peer;
+    rq->slot = slot;
+    rq->bytes = m;
+    rq->buffer_id = x.dst_buffer_id;
+    rq->base_offset = x.dst_base_offset + off + p;
+    rq->handle = x.dst_handle;
+    rq->seq.store(q, std::memory_order_release);
+    rc.relay_q = q;
+    c->copies_issued += 1;
+  }
+  x.relay_r = rr;
+  x.relay_last_q = rc.relay_q;
+  return ICCL_SUCCESS;
+}
+
+// Hop 2, on the relay: forward every published piece from every source into
+// its destination buffer, in order per source, on that source's stream.
+static iccl_result_t serve_relays(iccl_comm* c, bool* busy) {
+  if (!c->relay_buf) return ICCL_SUCCESS;
+  for (int src = 0; src < c->nranks; src++) {
+    if (src == c->rank) continue;
+    for (;;) {
+      const uint64_t q = c->relay_next[src];
+      RelayReq* rq = relay_req(c, c->rank, src, q);
+      if (rq->seq.load(std::memory_order_acquire) != q) break;
+      auto key = std::make_pair((int)rq->dst, rq->buffer_id);
+      auto it = c->relay_ipc.find(key);
+      if (it == c->relay_ipc.end()) {
+        void* p = nullptr;
+        cudaIpcMemHandle_t h = rq->handle;
+        ICCL_CHECK_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        it = c->relay_ipc.emplace(key, (char*)p).first;
+      }
+      cudaStream_t st = c->streams[c->relay_serve[src]].s;
+      const char* stage = c->relay_buf + ((size_t)src * kRelaySlots + rq->slot) * c->relay_slot_bytes;
+      iccl_result_t r = memop_wait(st, &relay_in(c, c->rank, src)->v, (uint32_t)q);
+      if (r) return r;
+      ICCL_CHECK_CU(driver()->cuMemcpyDtoDAsync((CUdeviceptr)(it->second + rq->base_offset), (CUdeviceptr)stage,
+                                                rq->bytes, (CUstream)st));
+      r = memop_write(st, &relay_out(c, c->rank, src)->v, (uint32_t)q);
+      if (r) return r;
+      c->relay_next[src] = q + 1;
+      c->copies_issued += 1;
+      *busy = true;
+    }
+  }
+  return ICCL_SUCCESS;
 }
 
 static int stream_for(iccl_comm* c, Channel& chn, int path, int engine, int k) {
@@ -470,7 +653,15 @@ static void fire_chunk_faults(iccl_comm* c, Channel& chn, int op_index, int chun
 
 static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
   const int path = x.path;
-  const int eng = path_engine(c, path, x.bytes);
+  const int eng = path_engine(c, chn, path, x.bytes);
+  const size_t off = (size_t)k * x.chunk;
+  const size_t n = std::min(x.chunk, x.bytes - off);
+  if (eng == ENG_RELAY) {
+    // the relay's request ring must have room for every piece of the chunk
+    const uint32_t out_now = __atomic_load_n(&relay_out(c, chn.relay_rank, c->rank)->v, __ATOMIC_ACQUIRE);
+    if ((int32_t)(c->relay_sent[chn.relay_rank] + (uint32_t)relay_pieces(c, n) - out_now) > kRelayDepth)
+      return ICCL_ERR_IN_PROGRESS;
+  }
   const int si = stream_for(c, chn, path, eng, k);
   StreamCtx& sc = c->streams[si];
   const int bit = 1 << (si % 32);
@@ -483,44 +674,73 @@ static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
     r = memop_wait(sc.s, &theirs->ready[x.r_ready_slot], x.r_ready_gen);
     if (r) return r;
     x.waited[path] |= bit;
+    if (eng == ENG_CE && c->monitor_enabled.load(std::memory_order_relaxed)) {
+      // monitor anchor: the stream is released here, so an event at this point
+      // sits at a drain the copy pays anyway (no extra chunk boundary)
+      cudaEvent_t a = get_tevent(c);
+      x.anchors.push_back(a);
+      ICCL_CHECK_CUDA(cudaEventRecord(a, sc.s));
+      x.last_ev.emplace_back(si, a);
+    }
   }
   if (x.fault_ops_index >= 0) fire_chunk_faults(c, chn, x.fault_ops_index, k, path);
   if (chn.fault[path].down) {
     iccl_result_t r = memop_wait(sc.s, &c->gate_words[chn.fault[path].gate], 1);
     if (r) return r;
   }
-  const size_t off = (size_t)k * x.chunk;
-  const size_t n = std::min(x.chunk, x.bytes - off);
   ChunkRec& rc = x.rec[k];
   rc.t1 = now_ns();
+  rc.relay_q = 0;
   rc.path = path;
   rc.stream = si;
   rc.done = false;
   rc.stamp = -1;
-  // Monitor on: the chunk's WR/WC pair is stamped on the device (K4) with
-  // %globaltimer and the t2 stamp doubles as the WC the proxy polls.  Monitor
-  // off: the WC is an event record (no kernel: the copy-engine path uses 0 SMs).
+  // Monitor on, SM path: K1 itself stamps the chunk's WR/WC pair with
+  // %globaltimer (K4 epilogue) and the t2 stamp doubles as the WC the proxy
+  // polls.  Copy-engine path: the WC is an event after the chunk — with the
+  // monitor on a timing event, whose device time (and the previous event on
+  // the stream, the chunk's start) give t1/t2 with no kernel at all, so the
+  // path stays at 0 SMs.  (A stream memop here would cost a full copy-engine
+  // drain per chunk: probes/p2p_probe3.)
+  const bool mon = c->monitor_enabled.load(std::memory_order_relaxed);
   KernelStamp* st = nullptr;
-  if (c->monitor_enabled.load(std::memory_order_relaxed)) {
+  if (mon && eng == ENG_SM) {
     rc.stamp = c->next_stamp++ % kStampSlots;
     st = &c->stamps[rc.stamp];
     memset((void*)st, 0, sizeof(KernelStamp));
   }
+  rc.t1ev = nullptr;
+  if (mon && eng == ENG_CE) {
+    for (auto& le : x.last_ev)
+      if (le.first == si) rc.t1ev = le.second;
+  }
   if (eng == ENG_CE) {
-    if (st) ICCL_CHECK_CUDA(launch_stamp(st, 0, sc.s));
     ICCL_CHECK_CU(driver()->cuMemcpyDtoDAsync((CUdeviceptr)(x.dst + off), (CUdeviceptr)(x.src + off), n, (CUstream)sc.s));
-    if (st) ICCL_CHECK_CUDA(launch_stamp(st, 1, sc.s));
+    c->copies_issued += 1;
+  } else if (eng == ENG_RELAY) {
+    // two copy-engine hops through the relay GPU; the WC is the relay's
+    // out-counter reaching the chunk's last piece (no event, no kernel)
+    iccl_result_t r = relay_push(c, chn, x, off, n, sc.s, rc);
+    if (r) return r;
   } else {
     ICCL_CHECK_CUDA(launch_copy(x.src + off, x.dst + off, n, c->cfg.sm_cap, st, sc.s));
+    c->copies_issued += 1;
   }
-  c->kernels_launched += st ? (eng == ENG_CE ? 2 : 1) : (eng == ENG_SM ? 1 : 0);
-  c->copies_issued += 1;
+  c->kernels_launched += eng == ENG_SM ? 1 : 0;
   c->bytes_issued += n;
-  // Without stamps the WC is an event after the chunk.  (A stream memop here
-  // would cost a full copy-engine drain per chunk: probes/p2p_probe3.)
-  if (!st) {
-    if (!rc.ev) rc.ev = get_event(c);
+  if (!st && eng != ENG_RELAY) {
+    const bool timed = mon && eng == ENG_CE;
+    if (rc.ev && rc.timed != timed) {
+      (rc.timed ? c->tevent_pool : c->event_pool).push_back(rc.ev);
+      rc.ev = nullptr;
+    }
+    if (!rc.ev) rc.ev = timed ? get_tevent(c) : get_event(c);
+    rc.timed = timed;
     ICCL_CHECK_CUDA(cudaEventRecord(rc.ev, sc.s));
+    if (timed) {
+      for (auto& le : x.last_ev)
+        if (le.first == si) le.second = rc.ev;
+    }
   }
   iccl_result_t r = ICCL_SUCCESS;
   if (k == x.nchunks - 1) {
@@ -536,6 +756,11 @@ static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
       }
     }
     for (cudaEvent_t fe : x.fences) ICCL_CHECK_CUDA(cudaStreamWaitEvent(sc.s, fe, 0));
+    if (x.relay_r >= 0) {
+      // every piece that went through the relay must have been forwarded
+      r = memop_wait(sc.s, &relay_out(c, x.relay_r, c->rank)->v, x.relay_last_q);
+      if (r) return r;
+    }
     r = memop_write(sc.s, &theirs->done[x.r_done_slot], x.r_done_gen);
     if (r) return r;
     r = memop_write(sc.s, &mine->done[x.s_slot], x.s_gen);
@@ -586,6 +811,7 @@ static iccl_result_t switch_path(iccl_comm* c, Channel& chn, int to, int trigger
     if (!any_pending) release_gate(c, stale_gate);
   }
   chn.active_path = to;
+  chn.failed_over = (to == 1 && trigger == 1);
   c->active_path_pub[chn.peer].store(to);
   PairState& ps = ring_of(c, c->rank, chn.peer)->st;
   ps.active_path.store(to);
@@ -634,7 +860,32 @@ static void record_monitor(iccl_comm* c, Channel& chn, Xfer& x, int k, uint64_t 
   iccl_mon_rec_t m{};
   m.t1_ns = rc.t1;
   m.t2_ns = t2_host;
-  if (rc.stamp >= 0) {
+  if (rc.timed && rc.t1ev) {
+    // copy-engine path: device times of the chunk's start / end events
+    uint64_t a = event_abs_ns(c, rc.t1ev), b = event_abs_ns(c, rc.ev);
+    if (a && b && b >= a) {
+      m.t1_ns = a;
+      m.t2_ns = b;
+    }
+    // keep the float-ms elapsed time short: re-base once a second
+    if (b > (uint64_t)c->base_abs_ns + 1000000000ull) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, c->base_ev, rc.ev) == cudaSuccess) {
+        cudaEvent_t nb = rc.ev;  // ownership moves to the time base
+        rc.ev = nullptr;
+        rc.timed = false;
+        // a later chunk of this op may still name the old base as its start
+        // event: recycle it only two re-bases (>= 2 s) later
+        c->old_bases.push_back(c->base_ev);
+        if (c->old_bases.size() > 2) {
+          c->tevent_pool.push_back(c->old_bases.front());
+          c->old_bases.pop_front();
+        }
+        c->base_ev = nb;
+        c->base_abs_ns += (int64_t)((double)ms * 1e6);
+      }
+    }
+  } else if (rc.stamp >= 0) {
     KernelStamp* st = &c->stamps[rc.stamp];
     unsigned long long t1 = st->t1, t2 = st->t2;
     if (t1 && t2 && t2 > t1) {
@@ -682,6 +933,9 @@ static iccl_result_t progress_channel(iccl_comm* c, Channel& chn, bool* busy) {
     x.r_ready_gen = e.ready_gen;
     x.r_done_slot = e.done_slot;
     x.r_done_gen = e.done_gen;
+    x.dst_buffer_id = e.buffer_id;
+    x.dst_base_offset = e.base_offset;
+    x.dst_handle = e.handle;
     x.chunk = (size_t)c->cfg.chunk_bytes;
     x.nchunks = (int)((x.bytes + x.chunk - 1) / x.chunk);
     x.rec.resize(x.nchunks);
@@ -702,7 +956,9 @@ static iccl_result_t progress_channel(iccl_comm* c, Channel& chn, bool* busy) {
   for (Xfer& x : chn.xfers) {
     while (x.completed < x.next_issue) {
       ChunkRec& rc = x.rec[x.completed];
-      if (rc.stamp >= 0) {
+      if (rc.relay_q) {
+        if (!cyc_geq(__atomic_load_n(&relay_out(c, x.relay_r, c->rank)->v, __ATOMIC_ACQUIRE), rc.relay_q)) break;
+      } else if (rc.stamp >= 0) {
         if (__atomic_load_n(&c->stamps[rc.stamp].t2, __ATOMIC_ACQUIRE) == 0) break;
       } else {
         cudaError_t q = cudaEventQuery(rc.ev);
@@ -740,7 +996,7 @@ static iccl_result_t progress_channel(iccl_comm* c, Channel& chn, bool* busy) {
       for (cudaEvent_t fe : x.fences) cudaEventDestroy(fe);
       x.fences.clear();
     }
-    put_events(c, x.rec);
+    put_events(c, x);
     chn.xfers.pop_front();
     c->pending_xfers.fetch_sub(1);
     *busy = true;
@@ -750,15 +1006,20 @@ static iccl_result_t progress_channel(iccl_comm* c, Channel& chn, bool* busy) {
   for (Xfer& x : chn.xfers) outstanding += x.next_issue - x.completed;
   for (Xfer& x : chn.xfers) {
     if (x.path != chn.active_path) continue;
+    bool stalled = false;
     while (x.next_issue < x.nchunks && outstanding < c->cfg.window) {
       r = issue_chunk(c, chn, x, x.next_issue);
+      if (r == ICCL_ERR_IN_PROGRESS) {  // relay ring full: retry on a later pass
+        stalled = true;
+        break;
+      }
       if (r) return r;
       x.next_issue++;
       outstanding++;
       *busy = true;
       publish(c, chn, x);
     }
-    if (x.next_issue < x.nchunks) break;
+    if (stalled || x.next_issue < x.nchunks) break;
   }
   // 5. watchdog + probe (check_receiver_timeout)
   if (!chn.xfers.empty()) {
@@ -797,7 +1058,7 @@ static iccl_result_t progress_channel(iccl_comm* c, Channel& chn, bool* busy) {
 // monitor_failed_link: while on the backup, probe the
 // primary every probe period; a probe that completes switches back.
 static iccl_result_t monitor_failed_link(iccl_comm* c, Channel& chn) {
-  if (chn.active_path != 1) return ICCL_SUCCESS;
+  if (chn.active_path != 1 || !chn.failed_over) return ICCL_SUCCESS;
   const uint64_t t = now_ns();
   StreamCtx& ps = c->streams[chn.probe_stream];
   if (chn.probe_out) {
@@ -833,7 +1094,9 @@ static void proxy_loop(iccl_comm* c) {
     {
       std::unique_lock<std::mutex> lk(c->qmu);
       if (c->inbox.empty() && c->pending_xfers.load() == 0 && now_ns() - idle_since > 200000) {
-        c->qcv.wait_for(lk, std::chrono::microseconds(500));
+        // a relay GPU has no pending sends of its own: nap shorter so its
+        // forwarding (hop 2) starts within ~50 us of a request
+        c->qcv.wait_for(lk, std::chrono::microseconds(c->relay_buf ? 50 : 500));
       }
       batch.swap(c->inbox);
     }
@@ -860,6 +1123,10 @@ static void proxy_loop(iccl_comm* c) {
         set_async(c, r, std::string("proxy: ") + last_error());
         break;
       }
+    }
+    {
+      iccl_result_t r = serve_relays(c, &busy);
+      if (r) set_async(c, r, std::string("relay: ") + last_error());
     }
     if (c->hdr->abort.load()) set_async(c, ICCL_ERR_ABORTED, "communicator aborted");
     if (c->ll_error && __atomic_load_n(c->ll_error, __ATOMIC_ACQUIRE))
@@ -1186,6 +1453,17 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
     c->peer_ll.assign(nranks, nullptr);
     ICCL_CHECK_CUDA(cudaDeviceSynchronize());
   }
+  c->relay_sent.assign(nranks, 0);
+  c->relay_next.assign(nranks, 1);
+  c->peer_relay.assign(nranks, nullptr);
+  me.relay_slot_bytes = 0;
+  if (conf.backup_kind == ICCL_BACKUP_RELAY && nranks >= 3) {
+    c->relay_slot_bytes = (size_t)conf.relay_slot_mib << 20;
+    const size_t bytes = (size_t)nranks * kRelaySlots * c->relay_slot_bytes;
+    ICCL_CHECK_CUDA(cudaMalloc((void**)&c->relay_buf, bytes));
+    ICCL_CHECK_CUDA(cudaIpcGetMemHandle(&me.relay_handle, c->relay_buf));
+    me.relay_slot_bytes = c->relay_slot_bytes;
+  }
   if (rank == 0) {
     c->hdr->nranks = nranks;
     c->hdr->magic = kMagic;
@@ -1230,6 +1508,14 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
     int sm = mk_stream(ENG_SM);
     chn.path_streams[0].push_back(sm);
     chn.path_streams[1].push_back(sm);
+    if (c->relay_buf && p != rank) {
+      for (int q = 0; q < nranks; q++)
+        if (q != rank && q != p) {
+          chn.relay_rank = q;  // lowest-index GPU that is not an endpoint
+          break;
+        }
+      chn.path_streams[1].push_back(mk_stream(ENG_RELAY));
+    }
     chn.probe_stream = mk_stream(ENG_CE);
     if (p == rank) {
       chn.peer_scratch = c->scratch + 2048;
@@ -1242,15 +1528,26 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
       c->peer_ll[p] = (char*)pl;
     }
   }
+  if (c->relay_buf) {
+    c->relay_serve.assign(nranks, -1);
+    for (int q = 0; q < nranks; q++)
+      if (q != rank) c->relay_serve[q] = mk_stream(ENG_RELAY);
+  }
   // %globaltimer -> CLOCK_MONOTONIC offset for SM-path monitor stamps
   {
     cudaStream_t s = c->streams[0].s;
     *c->gtimer = 0;
     uint64_t h0 = now_ns();
     ICCL_CHECK_CUDA(launch_read_globaltimer(c->gtimer, s));
+    // time base of the monitor's timing events: recorded right behind the
+    // %globaltimer read, so both stamp kinds share one clock (to ~1 us)
+    ICCL_CHECK_CUDA(cudaEventCreate(&c->base_ev));
+    c->all_events.push_back(c->base_ev);
+    ICCL_CHECK_CUDA(cudaEventRecord(c->base_ev, s));
     ICCL_CHECK_CUDA(cudaStreamSynchronize(s));
     uint64_t h1 = now_ns();
     c->gtimer_offset = (int64_t)((h0 + h1) / 2) - (int64_t)(*c->gtimer);
+    c->base_abs_ns = (int64_t)(*c->gtimer) + c->gtimer_offset;
   }
   r = shm_barrier(c);
   if (r) return r;
@@ -1279,6 +1576,10 @@ static void teardown(iccl_comm* c) {
   }
   for (size_t p = 0; p < c->peer_ll.size(); p++)
     if (c->peer_ll[p] && (int)p != c->rank) cudaIpcCloseMemHandle(c->peer_ll[p]);
+  for (char* p : c->peer_relay)
+    if (p) cudaIpcCloseMemHandle(p);
+  for (auto& kv : c->relay_ipc) cudaIpcCloseMemHandle(kv.second);
+  if (c->relay_buf) cudaFree(c->relay_buf);
   if (c->ll_region) cudaFree(c->ll_region);
   if (c->scratch) cudaFree(c->scratch);
   if (c->shm) {
@@ -1300,6 +1601,9 @@ iccl_result_t iccl_comm_destroy(iccl_comm_t c) {
     if (now_ns() - t0 > 120ull * 1000000000ull) break;
     usleep(50);
   }
+  // every rank's sends retired (their relayed pieces included) before any
+  // proxy stops: a relay GPU serves forwarding requests until here
+  iccl_result_t r0 = c->hdr->abort.load() ? ICCL_SUCCESS : shm_barrier(c);
   if (c->proxy.joinable()) {
     c->stop.store(true);
     c->qcv.notify_one();
@@ -1311,6 +1615,7 @@ iccl_result_t iccl_comm_destroy(iccl_comm_t c) {
   for (int g = 0; g < kGateWords; g++) __atomic_store_n((uint32_t*)&c->gate_words[g], 1u, __ATOMIC_SEQ_CST);
   for (auto& sc : c->streams) cudaStreamSynchronize(sc.s);
   iccl_result_t r = c->hdr->abort.load() ? ICCL_SUCCESS : shm_barrier(c);
+  if (r == ICCL_SUCCESS) r = r0;
   teardown(c);
   delete c;
   return r == ICCL_ERR_ABORTED ? ICCL_SUCCESS : r;

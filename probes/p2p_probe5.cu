@@ -166,6 +166,47 @@ int main(int argc, char** argv) {
     std::sort(v.begin(), v.end());
     printf("  mode %d: %.1f us per 64 MiB copy (%.1f GB/s)\n", mode, v[v.size() / 2], (64 << 20) / v[v.size() / 2] / 1e3); fflush(stdout);
   }
+  SECTION("4. full op chain one-way (us): user WriteValue(ready) x2 -> copy stream waits both, CE copy, WriteValue(done) x2 -> user waits done");
+  {
+    cudaStream_t c0, c1;
+    CK(cudaSetDevice(0)); CK(cudaStreamCreateWithFlags(&c0, cudaStreamNonBlocking));
+    CK(cudaSetDevice(1)); CK(cudaStreamCreateWithFlags(&c1, cudaStreamNonBlocking));
+    char *b0, *b1; CK(cudaSetDevice(0)); CK(cudaMalloc(&b0, 1 << 20)); CK(cudaSetDevice(1)); CK(cudaMalloc(&b1, 1 << 20));
+    // flags: r0 r1 (ready of rank0/1 for the current op), e0 e1 (done)
+    struct Pl { const char* name; CUdeviceptr r0, r1, e0, e1; };
+    Pl pls[] = {{"host flags", (CUdeviceptr)(hf + 256), (CUdeviceptr)(hf + 320), (CUdeviceptr)(hf + 384), (CUdeviceptr)(hf + 448)},
+                {"device flags (owner-local)", (CUdeviceptr)(d0 + 256), (CUdeviceptr)(d1 + 256), (CUdeviceptr)(d0 + 320), (CUdeviceptr)(d1 + 320)}};
+    for (size_t sz : {(size_t)8, (size_t)65536, (size_t)1 << 20}) {
+      for (auto& pl : pls) {
+        CK(cudaSetDevice(0)); CK(cudaMemset(d0, 0, 4096)); CK(cudaSetDevice(1)); CK(cudaMemset(d1, 0, 4096));
+        memset(hf, 0, 4096); CK(cudaDeviceSynchronize()); CK(cudaSetDevice(0)); CK(cudaDeviceSynchronize());
+        const int N = 200;
+        CK(cudaEventRecord(a, s0));
+        uint32_t g = 0;
+        for (int i = 1; i <= N; i++) {
+          for (int dir = 0; dir < 2; dir++) {  // 0: 0->1 copy by c0, 1: 1->0 copy by c1
+            g++;
+            CK(cudaSetDevice(0)); CKD(cuStreamWriteValue32((CUstream)s0, pl.r0, g, 0));
+            CK(cudaSetDevice(1)); CKD(cuStreamWriteValue32((CUstream)s1, pl.r1, g, 0));
+            int d = dir == 0 ? 0 : 1;
+            cudaStream_t cs = d == 0 ? c0 : c1;
+            CK(cudaSetDevice(d));
+            CKD(cuStreamWaitValue32((CUstream)cs, pl.r0, g, CU_STREAM_WAIT_VALUE_GEQ));
+            CKD(cuStreamWaitValue32((CUstream)cs, pl.r1, g, CU_STREAM_WAIT_VALUE_GEQ));
+            CK(cudaMemcpyAsync(d == 0 ? b1 : b0, d == 0 ? b0 : b1, sz, cudaMemcpyDefault, cs));
+            CKD(cuStreamWriteValue32((CUstream)cs, pl.e1, g, 0));
+            CKD(cuStreamWriteValue32((CUstream)cs, pl.e0, g, 0));
+            CK(cudaSetDevice(0)); CKD(cuStreamWaitValue32((CUstream)s0, pl.e0, g, CU_STREAM_WAIT_VALUE_GEQ));
+            CK(cudaSetDevice(1)); CKD(cuStreamWaitValue32((CUstream)s1, pl.e1, g, CU_STREAM_WAIT_VALUE_GEQ));
+          }
+          if (i == N) { CK(cudaSetDevice(0)); CK(cudaEventRecord(b, s0)); }
+        }
+        CK(cudaSetDevice(0)); CK(cudaEventSynchronize(b));
+        float ms; CK(cudaEventElapsedTime(&ms, a, b));
+        printf("  %zu B %s: %.2f us per op\n", sz, pl.name, ms * 1e3 / N / 2); fflush(stdout);
+      }
+    }
+  }
   SECTION("done");
   return 0;
 }

@@ -117,3 +117,28 @@ def failover_pair(comm, rank, world, nbytes, fault_chunk, restore_us=0):
         out["resume"] = np.array([e["resume_chunk"] for e in ev], np.int32)
         out["detect_ns"] = np.array([e["detect_ns"] for e in ev], np.int64)
     return out
+
+
+def relay_ring(comm, rank, world, nbytes, iters=2):
+    """Every pair of the ring shift forced onto the backup path (relay GPU)
+    through the API switch (switch_qp ToBackup), then back to the primary."""
+    from paper_2510_00991_b200 import P2POp
+    dev = torch.device("cuda", rank)
+    to, frm = (rank + 1) % world, (rank - 1) % world
+    comm.switch_qp(to, "ToBackup")
+    out = {}
+    for it in range(iters):
+        src = to_dev(payload(nbytes, seed=70 + 10 * it + rank), dev)
+        dst = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+        comm.batch_isend_irecv([P2POp("isend", src, to), P2POp("irecv", dst, frm)])
+        torch.cuda.synchronize()
+        out[f"recv{it}"] = dst.cpu().numpy()
+    out["path"] = np.array([0 if comm.active_path(to) == "primary" else 1], np.int32)
+    out["relay_copies"] = np.array([comm.stats()["copies_issued"]], np.int64)
+    comm.switch_qp(to, "ToPrimary")
+    src = to_dev(payload(nbytes, seed=90 + rank), dev)
+    dst = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+    comm.batch_isend_irecv([P2POp("isend", src, to), P2POp("irecv", dst, frm)])
+    torch.cuda.synchronize()
+    out["recv_back"] = dst.cpu().numpy()
+    return out

@@ -294,3 +294,34 @@ def test_pair_failover_mid_message(need_gpus, tmp_path):
     assert np.array_equal(res[1]["recv"], _oracle_sendrecv(payload(n, seed=99)))
     assert list(res[0]["switch_to"])[:1] == [1]
     assert res[0]["resume"][0] == 5
+
+
+def test_relay_failover_mid_message(need_gpus, tmp_path):
+    """Backup = GPU relay (two copy-engine hops through the lowest-index
+    non-endpoint GPU): primary 0->1 Down at chunk 3,
+    resume through GPU 2 at the breakpoint, bit-exact."""
+    need_gpus(3)
+    import torch
+    import gpu_scenarios as sc
+    n = 48 * MiB + 80
+    res = run_ranks(torch.cuda.device_count(), sc.failover_pair, tmp_path, nbytes=n, fault_chunk=3,
+                    config=dict(chunk_bytes=4 * MiB, delta_us=300, window=4, backup_kind="relay", relay_slot_mib=3))
+    assert np.array_equal(res[1]["recv"], _oracle_sendrecv(payload(n, seed=99)))
+    assert list(res[0]["switch_to"])[:1] == [1]
+    assert res[0]["resume"][0] == 3
+
+
+def test_relay_ring_api_switch(need_gpus, tmp_path):
+    need_gpus(3)
+    import torch
+    import gpu_scenarios as sc
+    w = torch.cuda.device_count()
+    n = 20 * MiB + 16
+    res = run_ranks(w, sc.relay_ring, tmp_path, nbytes=n,
+                    config=dict(chunk_bytes=8 * MiB, backup_kind="relay", relay_slot_mib=2))
+    for r in range(w):
+        frm = (r - 1) % w
+        for it in range(2):
+            assert np.array_equal(res[r][f"recv{it}"], payload(n, seed=70 + 10 * it + frm))
+        assert np.array_equal(res[r]["recv_back"], payload(n, seed=90 + frm))
+        assert int(res[r]["path"][0]) == 1
