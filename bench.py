@@ -445,7 +445,7 @@ def main():
     # (not "--monitor": torchrun's parser would take that abbreviation as its own)
     ap.add_argument("--iccl-monitor", dest="monitor", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-pieces", type=int, default=8, help="pipeline pieces of the e2e (host buffer) step")
+    ap.add_argument("--e2e-pieces", type=int, default=16, help="pipeline pieces of the e2e (host buffer) step")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

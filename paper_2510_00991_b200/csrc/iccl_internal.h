@@ -105,13 +105,6 @@ cudaError_t launch_gather_rows(const void* src, void* dst, const int64_t* idx, i
                                int ctas, cudaStream_t st);
 cudaError_t launch_scatter_rows(const void* src, void* dst, const int64_t* idx, int64_t n_rows, int64_t row_bytes,
                                 int ctas, cudaStream_t st);
-// Fused pack + push: rows gathered by idx and written straight into up to
-// 64 destination buffers (peer-mapped), segment s covering output rows
-// [seg_start[s], seg_start[s+1]) written at dst_ptrs[s] + (i - seg_start[s]) * row_bytes.
-cudaError_t launch_gather_rows_multi(const void* src, void* const* dst_ptrs, const int64_t* seg_start, int n_seg,
-                                     const int64_t* idx, int64_t n_rows, int64_t row_bytes, int ctas,
-                                     cudaStream_t st);
-
 }  // namespace iccl
 
 namespace iccl {

@@ -11,9 +11,7 @@
 // K4  stamps          %globaltimer t1 at the first CTA's start and t2 at the
 //                     last CTA's end, written to a host-mapped KernelStamp
 //                     the proxy turns into a monitor record.
-// K2  gather rows     MoE dispatch pack: dst[i] = src[idx[i]] (16 B vectors),
-//                     optionally straight into several peer buffers (fused
-//                     pack + push).
+// K2  gather rows     MoE dispatch pack: dst[i] = src[idx[i]] (16 B vectors).
 // K3  scatter rows    MoE combine unpack: dst[idx[i]] = src[i].
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -176,58 +174,53 @@ __global__ void iccl_read_globaltimer(unsigned long long* out) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(out), "l"(t) : "memory");
 }
 
-// K2: one warp per row, 16 B per lane per step (coalesced 512 B per warp step).
+__device__ __forceinline__ int4 ld_nc(const int4* p) {
+  int4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+// streaming store: evict-first in L2, so the rows being written do not push
+// out data that is re-read (K2's token matrix is read k times)
+__device__ __forceinline__ void st_cs(int4* p, int4 v) {
+  asm volatile("st.global.cs.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// One warp moves one row: 16 B per lane per step (512 B coalesced per warp
+// step), four independent loads in flight per lane before their stores.
+__device__ __forceinline__ void warp_copy_row(const int4* __restrict__ s, int4* __restrict__ d, int64_t row16,
+                                              int lane) {
+  int64_t c = lane;
+  for (; c + 96 < row16; c += 128) {
+    const int4 v0 = ld_nc(s + c), v1 = ld_nc(s + c + 32), v2 = ld_nc(s + c + 64), v3 = ld_nc(s + c + 96);
+    st_cs(d + c, v0);
+    st_cs(d + c + 32, v1);
+    st_cs(d + c + 64, v2);
+    st_cs(d + c + 96, v3);
+  }
+  for (; c < row16; c += 32) st_cs(d + c, ld_nc(s + c));
+}
+
+// K2: dispatch pack, dst row r <- src row idx[r].
 __global__ void __launch_bounds__(256) iccl_gather_rows(const int4* __restrict__ src, int4* __restrict__ dst,
                                                        const int64_t* __restrict__ idx, int64_t n_rows,
                                                        int64_t row16) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = warp; r < n_rows; r += nwarps) {
-    const int4* s = src + idx[r] * row16;
-    int4* d = dst + r * row16;
-    for (int64_t c = lane; c < row16; c += 32) d[c] = s[c];
-  }
+  for (int64_t r = warp; r < n_rows; r += nwarps) warp_copy_row(src + idx[r] * row16, dst + r * row16, row16, lane);
 }
 
-// K3: inverse permutation (combine unpack).
+// K3: inverse permutation (combine unpack), dst row idx[r] <- src row r.
 __global__ void __launch_bounds__(256) iccl_scatter_rows(const int4* __restrict__ src, int4* __restrict__ dst,
                                                         const int64_t* __restrict__ idx, int64_t n_rows,
                                                         int64_t row16) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = warp; r < n_rows; r += nwarps) {
-    const int4* s = src + r * row16;
-    int4* d = dst + idx[r] * row16;
-    for (int64_t c = lane; c < row16; c += 32) d[c] = s[c];
-  }
-}
-
-struct MultiDst {
-  int4* ptr[64];
-  int64_t start[65];
-};
-
-// K2 fused with the push: output row r belongs to segment s (binary search
-// over <= 64 segment starts) and lands in that segment's (peer) buffer.
-__global__ void __launch_bounds__(256) iccl_gather_rows_multi(const int4* __restrict__ src, MultiDst md, int n_seg,
-                                                             const int64_t* __restrict__ idx, int64_t n_rows,
-                                                             int64_t row16) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = warp; r < n_rows; r += nwarps) {
-    int lo = 0, hi = n_seg - 1;
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (md.start[mid] <= r) lo = mid;
-      else hi = mid - 1;
-    }
-    const int4* s = src + idx[r] * row16;
-    int4* d = md.ptr[lo] + (r - md.start[lo]) * row16;
-    for (int64_t c = lane; c < row16; c += 32) d[c] = s[c];
-  }
+  for (int64_t r = warp; r < n_rows; r += nwarps) warp_copy_row(src + r * row16, dst + idx[r] * row16, row16, lane);
 }
 
 // K5: LL eager path.  Block b serves op b of the batch.  A send writes every
@@ -348,7 +341,7 @@ cudaError_t preload_kernels() {
   cudaFuncAttributes a;
   const void* fns[] = {(const void*)iccl_copy_tma,   (const void*)iccl_copy_unaligned, (const void*)iccl_stamp,
                        (const void*)iccl_read_globaltimer, (const void*)iccl_gather_rows,
-                       (const void*)iccl_scatter_rows, (const void*)iccl_gather_rows_multi,
+                       (const void*)iccl_scatter_rows,
                        (const void*)iccl_ll_group};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
@@ -394,23 +387,6 @@ cudaError_t launch_scatter_rows(const void* src, void* dst, const int64_t* idx, 
   if ((row_bytes & 15) || ((uintptr_t)src & 15) || ((uintptr_t)dst & 15)) return cudaErrorInvalidValue;
   iccl_scatter_rows<<<rows_grid(n_rows, ctas), 256, 0, st>>>((const int4*)src, (int4*)dst, idx, n_rows,
                                                              row_bytes / 16);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_gather_rows_multi(const void* src, void* const* dst_ptrs, const int64_t* seg_start, int n_seg,
-                                     const int64_t* idx, int64_t n_rows, int64_t row_bytes, int ctas,
-                                     cudaStream_t st) {
-  if (n_rows == 0) return cudaSuccess;
-  if (n_seg < 1 || n_seg > 64 || (row_bytes & 15)) return cudaErrorInvalidValue;
-  MultiDst md;
-  for (int i = 0; i < n_seg; i++) {
-    md.ptr[i] = (int4*)dst_ptrs[i];
-    md.start[i] = seg_start[i];
-    if ((uintptr_t)dst_ptrs[i] & 15) return cudaErrorInvalidValue;
-  }
-  md.start[n_seg] = seg_start[n_seg];
-  iccl_gather_rows_multi<<<rows_grid(n_rows, ctas), 256, 0, st>>>((const int4*)src, md, n_seg, idx, n_rows,
-                                                                  row_bytes / 16);
   return cudaGetLastError();
 }
 

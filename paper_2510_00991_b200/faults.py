@@ -59,6 +59,7 @@ class FaultScript:
                     raise InvalidArgument("time-triggered fault entries must be sorted by time")
                 last_t = e.t_us
             key = (e.src, e.dst, e.path)
-            if state.get(key, True) == e.up:
+            # a script may open with Up: it restores a path a previous script left Down
+            if key in state and state[key] == e.up:
                 raise InvalidArgument(f"Down/Up must alternate on path {key}")
             state[key] = e.up
