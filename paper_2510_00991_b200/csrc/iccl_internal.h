@@ -66,15 +66,22 @@ struct alignas(64) KernelStamp {
 cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, KernelStamp* stamp, cudaStream_t st);
 // Force-load every kernel (see iccl_kernels.cu: lazy loading vs parked streams).
 cudaError_t preload_kernels();
-// K5: low-latency (LL) eager path for small messages.  8-byte lines
-// {4 B payload, 4 B sequence flag} written straight into a per-pair slot ring
-// in the receiver's GPU memory; one fused kernel per stream progresses every
-// LL op of a group concurrently (one CTA per op), so group members never wait
-// on each other through stream order.
-constexpr int kLLSlots = 4;               // slots per ordered pair (flow-control window)
-constexpr size_t kLLMaxBytes = 32 * 1024; // largest LL message
+// K5: low-latency (LL) eager path for small and mid-size messages.  8-byte
+// lines {4 B payload, 4 B sequence flag} written straight into a per-pair
+// slot ring in the receiver's GPU memory; one fused kernel per stream
+// progresses every LL op of a group concurrently, each op on 1..kLLMaxBlk
+// CTAs scaled by its size (kLLLinesPerBlk lines per CTA), so group members
+// never wait on each other through stream order.  The last CTA of an op
+// (per-op arrival counter, reset by that CTA) writes its done flag and, on
+// the receive side, returns the slot's credit.
+constexpr int kLLSlots = 4;                 // slots per ordered pair (flow-control window)
+constexpr size_t kLLMaxBytes = 256 * 1024;  // largest LL message
 constexpr size_t kLLLines = kLLMaxBytes / 4;
-constexpr int kLLMaxOps = 64;             // LL ops per launch
+constexpr int kLLMaxOps = 64;               // LL ops per launch
+constexpr int kLLMaxBlk = 16;               // CTAs per op
+constexpr size_t kLLLinesPerBlk = 2048;     // 8 lines per thread at 256 threads
+constexpr int kLLMaxBlocksPerLaunch = 1024;
+constexpr int kLLCounters = 4096;           // per-op arrival counters (ring)
 struct LLDesc {
   int kind;               // 0 send, 1 recv
   uint32_t seq;           // 1-based message number on this ordered pair
@@ -86,6 +93,9 @@ struct LLDesc {
                           // sender's words for me (peer-mapped)
   unsigned int* done_flag;  // op's done slot in the control block (host-mapped)
   uint32_t done_gen;
+  uint32_t first_blk;     // first CTA of this op in the launch
+  uint32_t nblk;          // CTAs of this op
+  unsigned int* counter;  // arrival counter of this op (local HBM, 0 between uses)
 };
 struct LLBatch {
   int n;

@@ -237,10 +237,20 @@ __device__ __forceinline__ bool ll_timed_out(unsigned long long t0) {
 }
 
 __global__ void __launch_bounds__(256) iccl_ll_group(LLBatch b) {
-  const LLDesc& d = b.d[blockIdx.x];
+  __shared__ int s_op;
+  if (threadIdx.x == 0) {
+    int op = 0;
+    while (op + 1 < b.n && blockIdx.x >= b.d[op + 1].first_blk) op++;
+    s_op = op;
+  }
+  __syncthreads();
+  const LLDesc& d = b.d[s_op];
+  const uint32_t part = blockIdx.x - d.first_blk;
   const unsigned long long t0 = globaltimer();
   const size_t lines = (d.bytes + 3) / 4;
+  const size_t lo = lines * part / d.nblk, hi = lines * (part + 1) / d.nblk;
   uint2* slot = (uint2*)d.slot;
+  __shared__ bool s_last;
   if (d.kind == 0) {
     if (d.seq > (uint32_t)kLLSlots) {
       if (threadIdx.x == 0) {
@@ -257,7 +267,7 @@ __global__ void __launch_bounds__(256) iccl_ll_group(LLBatch b) {
       }
       __syncthreads();
     }
-    for (size_t i = threadIdx.x; i < lines; i += blockDim.x) {
+    for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
       uint32_t w = 0;
       const size_t off = i * 4;
       if (off + 4 <= d.bytes && ((uintptr_t)(d.buf + off) & 3) == 0) {
@@ -268,10 +278,15 @@ __global__ void __launch_bounds__(256) iccl_ll_group(LLBatch b) {
       asm volatile("st.volatile.global.v2.u32 [%0], {%1, %2};" ::"l"(slot + i), "r"(w), "r"(d.seq) : "memory");
     }
     __syncthreads();
-    if (threadIdx.x == 0 && d.done_flag)
-      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(d.done_flag), "r"(d.done_gen) : "memory");
+    if (threadIdx.x == 0) {
+      // last CTA of the op: every CTA read its part of the source
+      s_last = d.nblk == 1 || atomicAdd(d.counter, 1u) == d.nblk - 1;
+      if (s_last && d.nblk > 1) atomicExch(d.counter, 0u);
+      if (s_last && d.done_flag)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(d.done_flag), "r"(d.done_gen) : "memory");
+    }
   } else {
-    for (size_t i = threadIdx.x; i < lines; i += blockDim.x) {
+    for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
       uint32_t w, f;
       do {
         asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(w), "=r"(f) : "l"(slot + i) : "memory");
@@ -289,10 +304,18 @@ __global__ void __launch_bounds__(256) iccl_ll_group(LLBatch b) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(d.credit + (d.seq - 1) % kLLSlots), "r"(d.seq)
-                   : "memory");
-      if (d.done_flag)
-        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(d.done_flag), "r"(d.done_gen) : "memory");
+      __threadfence();
+      s_last = d.nblk == 1 || atomicAdd(d.counter, 1u) == d.nblk - 1;
+      if (s_last) {
+        if (d.nblk > 1) {
+          atomicExch(d.counter, 0u);
+          __threadfence();  // the other CTAs' payload stores are ordered before the credit / done
+        }
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(d.credit + (d.seq - 1) % kLLSlots), "r"(d.seq)
+                     : "memory");
+        if (d.done_flag)
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(d.done_flag), "r"(d.done_gen) : "memory");
+      }
     }
   }
 }
@@ -303,7 +326,8 @@ bool smem_configured = false;
 
 cudaError_t launch_ll(const LLBatch& b, cudaStream_t st) {
   if (b.n <= 0) return cudaSuccess;
-  iccl_ll_group<<<b.n, 256, 0, st>>>(b);
+  const unsigned blocks = b.d[b.n - 1].first_blk + b.d[b.n - 1].nblk;
+  iccl_ll_group<<<blocks, 256, 0, st>>>(b);
   return cudaGetLastError();
 }
 

@@ -311,6 +311,8 @@ struct iccl_comm {
   std::vector<char*> peer_ll;
   std::vector<uint32_t> ll_sent, ll_recvd;
   unsigned int* ll_error = nullptr;  // host-mapped
+  unsigned int* ll_counters = nullptr;  // kLLCounters per-op arrival counters (device)
+  uint32_t ll_ctr_next = 0;
   // GPU relay (backup_kind RELAY, >= 3 ranks)
   char* relay_buf = nullptr;         // my staging: [source][kRelaySlots] x relay_slot_bytes
   size_t relay_slot_bytes = 0;
@@ -1268,15 +1270,21 @@ static size_t ll_credit_offset(int nranks, int peer) {
 }
 
 // One fused K5 launch per (stream, group): every LL op of the group gets its
-// own CTA, so sends and recvs progress concurrently.
+// own CTAs (1..kLLMaxBlk by size), so sends and recvs progress concurrently.
 static iccl_result_t launch_ll_ops(iccl_comm* c, cudaStream_t s, const std::vector<OpDesc>& ops) {
   RankFlags* mine = flags_of(c, c->rank);
-  for (size_t i = 0; i < ops.size(); i += kLLMaxOps) {
+  size_t i = 0;
+  while (i < ops.size()) {
     LLBatch b;
     memset(&b, 0, sizeof(b));
     b.error = c->ll_error;
-    for (size_t j = i; j < ops.size() && b.n < kLLMaxOps; j++) {
-      const OpDesc& op = ops[j];
+    uint32_t blocks = 0;
+    for (; i < ops.size() && b.n < kLLMaxOps; i++) {
+      const OpDesc& op = ops[i];
+      const size_t lines = (op.bytes + 3) / 4;
+      const uint32_t nblk = (uint32_t)std::min<size_t>(kLLMaxBlk, std::max<size_t>(1, (lines + kLLLinesPerBlk - 1) /
+                                                                                          kLLLinesPerBlk));
+      if (b.n > 0 && blocks + nblk > (uint32_t)kLLMaxBlocksPerLaunch) break;
       LLDesc& d = b.d[b.n++];
       d.kind = op.kind;
       d.seq = op.ll_seq;
@@ -1291,6 +1299,10 @@ static iccl_result_t launch_ll_ops(iccl_comm* c, cudaStream_t s, const std::vect
       }
       d.done_flag = &mine->done[op.slot];
       d.done_gen = op.gen;
+      d.first_blk = blocks;
+      d.nblk = nblk;
+      d.counter = c->ll_counters + (c->ll_ctr_next++ % kLLCounters);
+      blocks += nblk;
     }
     ICCL_CHECK_CUDA(launch_ll(b, s));
     c->kernels_launched += 1;
@@ -1448,6 +1460,8 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
     ICCL_CHECK_CUDA(cudaMemset(c->ll_region, 0, ll_bytes));
     ICCL_CHECK_CUDA(cudaIpcGetMemHandle(&me.ll_handle, c->ll_region));
     c->ll_error = (unsigned int*)((char*)c->pinned + 56 * 1024);
+    ICCL_CHECK_CUDA(cudaMalloc((void**)&c->ll_counters, kLLCounters * sizeof(unsigned int)));
+    ICCL_CHECK_CUDA(cudaMemset(c->ll_counters, 0, kLLCounters * sizeof(unsigned int)));
     c->ll_sent.assign(nranks, 0);
     c->ll_recvd.assign(nranks, 0);
     c->peer_ll.assign(nranks, nullptr);
@@ -1581,6 +1595,7 @@ static void teardown(iccl_comm* c) {
   for (auto& kv : c->relay_ipc) cudaIpcCloseMemHandle(kv.second);
   if (c->relay_buf) cudaFree(c->relay_buf);
   if (c->ll_region) cudaFree(c->ll_region);
+  if (c->ll_counters) cudaFree(c->ll_counters);
   if (c->scratch) cudaFree(c->scratch);
   if (c->shm) {
     cudaHostUnregister(c->shm);

@@ -271,11 +271,15 @@ def test_alltoallv_uneven_vs_oracle(need_gpus, tmp_path):
         assert np.array_equal(res[r]["recv"], exp[r])
 
 
-def test_pair_ll_small_messages(need_gpus, tmp_path):
+@pytest.mark.parametrize("ll_max", [32 * 1024, 256 * 1024])
+def test_pair_ll_small_messages(need_gpus, tmp_path, ll_max):
+    """LL path (K5) mixed with copy-engine ops in one group, more LL messages
+    per pair than slots; at 256 KiB ops span up to 16 CTAs each."""
     need_gpus(2)
     import gpu_scenarios as sc
-    sizes = [1, 3, 4, 7, 64, 1000, 4096, 32 * 1024, 32 * 1024 + 1, 300 * 1024, 5, 6, 8, 9]
-    res = run_ranks(2, sc.ll_mixed, tmp_path, sizes=sizes, config=dict(sm_small_bytes=32 * 1024))
+    sizes = [1, 3, 4, 7, 64, 1000, 4096, 32 * 1024, 32 * 1024 + 1, 300 * 1024, 5, 6, 8, 9, 64 * 1024 + 5,
+             200 * 1024 + 3, 256 * 1024]
+    res = run_ranks(2, sc.ll_mixed, tmp_path, sizes=sizes, config=dict(sm_small_bytes=ll_max))
     for r in range(2):
         peer = 1 - r
         for rd in range(3):
