@@ -341,7 +341,7 @@ def run_alltoallv(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     import paper_2510_00991_b200 as iccl
-    from paper_2510_00991_b200.moe import gather_rows, plan_dispatch, scatter_rows
+    from paper_2510_00991_b200.moe import expand_rows, plan_dispatch, scatter_rows
     cfg = iccl.IcclConfig.defaults(monitor_enabled=bool(args.monitor), transport=args.transport)
     comm = iccl.init(rank, world, local, cfg)
     T, k, E, H = 4096, 8, 64, 7168
@@ -366,7 +366,7 @@ def run_alltoallv(args):
     row = H * 2
 
     def step():
-        gather_rows(tokens, plan.token_of_row, packed)                       # K2 pack
+        expand_rows(tokens, plan.pos, k, packed)                              # K2 pack
         comm.alltoallv(recv, packed, plan.recv_counts, plan.send_counts)     # dispatch
         comm.alltoallv(back, recv, plan.send_counts, plan.recv_counts)       # combine
         scatter_rows(back, plan.order, out)                                  # K3 unpack

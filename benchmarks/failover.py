@@ -53,7 +53,7 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     import paper_2510_00991_b200 as iccl
     from bench import moe_routing
-    from paper_2510_00991_b200.moe import gather_rows, plan_dispatch, scatter_rows
+    from paper_2510_00991_b200.moe import expand_rows, plan_dispatch, scatter_rows
 
     src_r = args.src if args.src >= 0 else (3 if world > 5 else world - 1)
     dst_r = args.dst if args.dst >= 0 else (5 if world > 5 else (src_r + 2) % world if world > 2 else 1 - src_r)
@@ -81,7 +81,7 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step():
-        gather_rows(tokens, plan.token_of_row, packed)
+        expand_rows(tokens, plan.pos, k, packed)
         comm.alltoallv(recv, packed, plan.recv_counts, plan.send_counts)
         comm.alltoallv(back, recv, plan.send_counts, plan.recv_counts)
         scatter_rows(back, plan.order, out)
@@ -160,11 +160,11 @@ def main():
                 if bad:
                     info[4] = (bad[0].time - t_inj) / 1e3
                     info[5] = min(s.value for s in bad) / med
-            prim = [r for r in recs if r.path == 0 and r.t2 > r.t1]
-            back = [r for r in recs if r.path == 1 and r.t2 > r.t1 and r.peer == dst_r]
-            if prim and back:
-                bp = sum(r.size for r in prim) / (sum(r.t2 - r.t1 for r in prim) * 1e-9) / 1e9
-                bb = sum(r.size for r in back) / (sum(r.t2 - r.t1 for r in back) * 1e-9) / 1e9
+            prim_recs = [r for r in pre_recs + recs if r.path == 0 and r.t2 > r.t1 and r.peer != src_r]
+            back_recs = [r for r in recs if r.path == 1 and r.t2 > r.t1 and r.peer == dst_r]
+            if prim_recs and back_recs:
+                bp = sum(r.size for r in prim_recs) / (sum(r.t2 - r.t1 for r in prim_recs) * 1e-9) / 1e9
+                bb = sum(r.size for r in back_recs) / (sum(r.t2 - r.t1 for r in back_recs) * 1e-9) / 1e9
                 info[6], info[7] = bp, bb
     dist.all_reduce(info, op=dist.ReduceOp.SUM)
     res["switched"] = bool(info[0].item() > 0)

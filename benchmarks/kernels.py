@@ -104,8 +104,22 @@ def main():
             t = timed(lambda: gather_rows(tok, idx, packed), args.reps, s)
             ok = torch.equal(packed, tok[idx])
             alg = 2 * rows * row + rows * 8
-            out.append({"kernel": "K2 iccl_gather_rows", "rows": rows, "row_bytes": row, "us": round(t * 1e6, 2),
+            out.append({"alg_bytes": "T*k rows read (L2 may serve repeats) + T*k written + 8 B/row index",
+                        "kernel": "K2 iccl_gather_rows", "rows": rows, "row_bytes": row, "us": round(t * 1e6, 2),
                         "achieved_GBps": round(alg / t / 1e9, 1), "peak": hbm, "bound": "hbm",
+                        "frac": round(alg / t / 1e9 / hbm, 4), "bit_exact": ok})
+        if not only or "k2" in only:
+            # expand form (what moe_dispatch runs): each token read once, written k times
+            from paper_2510_00991_b200 import expand_rows
+            order = torch.randperm(rows, device="cuda", generator=g)
+            pos = torch.empty_like(order)
+            pos[order] = torch.arange(rows, device="cuda")
+            t = timed(lambda: expand_rows(tok, pos, k, packed), args.reps, s)
+            ok = torch.equal(packed, tok[torch.div(order, k, rounding_mode="floor")])
+            alg = T * row + rows * row + rows * 8
+            out.append({"kernel": "K2 iccl_expand_rows", "rows": rows, "row_bytes": row, "us": round(t * 1e6, 2),
+                        "achieved_GBps": round(alg / t / 1e9, 1), "peak": hbm, "bound": "hbm",
+                        "alg_bytes": "T rows read + T*k rows written + 8 B/row index",
                         "frac": round(alg / t / 1e9 / hbm, 4), "bit_exact": ok})
         if not only or "k3" in only:
             perm = torch.randperm(rows, device="cuda", generator=g)

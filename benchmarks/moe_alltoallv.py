@@ -1,0 +1,110 @@
+#!/usr/bin/env python
+"""Config 4 comparison: MoE expert-parallel dispatch + combine alltoallv,
+ICCL copy-engine path vs same-box NCCL (torch ``all_to_all_single``), the
+comparison the paper makes for alltoall (NCCL holds 24.7% of
+the SMs at 8x8).
+
+T=4096 tokens per rank, top-8 of 64 experts (8 per rank at 8 ranks), hidden
+7168 bf16 (14,336 B per row), skewed routing p_e ~ (e+1)^-0.8,
+so the splits are uneven.  One step = dispatch alltoallv + combine alltoallv
+(the reverse, same counts); the round trip must return every row bit for bit.
+
+Bound: t* = 2 x max_i max(egress_i, ingress_i) / 770 GB/s (NVLink per
+direction, measured peer-copy peak; the self segment is a local copy).
+
+    python -m torch.distributed.run --nproc-per-node 4 --master-addr 127.0.0.1 \
+        benchmarks/moe_alltoallv.py --impl iccl
+"""
+import argparse
+import json
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--impl", choices=["iccl", "nccl"], required=True)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    args = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    from bench import moe_routing
+    T, k, E, H = 4096, 8, 64, 7168
+    row = 2 * H
+    experts = moe_routing(rank, world, T, k, E, dev)
+    dest = torch.div(experts.reshape(-1), E // world, rounding_mode="floor")
+    send = torch.bincount(dest, minlength=world)
+    recv = torch.empty_like(send)
+    dist.all_to_all_single(recv, send)
+    sc, rc = send.tolist(), recv.tolist()
+    g = torch.Generator(device=dev).manual_seed(3000 + rank)
+    packed = torch.randint(-32768, 32767, (sum(sc), H), dtype=torch.int16, device=dev, generator=g)
+    inbox = torch.empty(sum(rc), H, dtype=torch.int16, device=dev)
+    back = torch.empty_like(packed)
+    comm = None
+    if args.impl == "iccl":
+        import paper_2510_00991_b200 as iccl
+        comm = iccl.init(rank, world, local, iccl.IcclConfig.defaults())
+
+    def step():
+        if comm:
+            comm.alltoallv(inbox, packed, rc, sc)
+            comm.alltoallv(back, inbox, sc, rc)
+        else:
+            dist.all_to_all_single(inbox, packed, rc, sc)
+            dist.all_to_all_single(back, inbox, sc, rc)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ok = torch.equal(back, packed)
+    s0 = comm.stats() if comm else None
+    dist.barrier()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev, dtype=torch.float64)
+    eg = (sum(sc) - sc[rank]) * row
+    ig = (sum(rc) - rc[rank]) * row
+    lim = torch.tensor([max(eg, ig)], device=dev, dtype=torch.float64)
+    tot = torch.tensor([2.0 * (eg + ig) / 2], device=dev, dtype=torch.float64)  # NVLink bytes per step
+    okt = torch.tensor([1.0 if ok else 0.0], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(lim, op=dist.ReduceOp.MAX)
+    dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+    ms = float(t.item())
+    t_star = 2 * float(lim.item()) / 770e9
+    res = {"bench": "moe_alltoallv", "impl": args.impl, "n_gpus": world, "ms_per_step": round(ms, 4),
+           "nvlink_GBps_total": round(float(tot.item()) / (ms * 1e-3) / 1e9, 1),
+           "t_star_ms": round(t_star * 1e3, 4), "frac_of_bound": round(t_star / (ms * 1e-3), 4),
+           "max_rank_egress_or_ingress_MiB": round(float(lim.item()) / 2**20, 1),
+           "bit_exact_roundtrip": bool(okt.item() > 0), "send_rows_rank0": sc,
+           "step": "dispatch alltoallv + combine alltoallv (same counts, reversed)"}
+    if comm:
+        s1 = comm.stats()
+        res["kernels_launched"] = s1["kernels_launched"] - s0["kernels_launched"]
+        comm.destroy()
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -210,6 +210,12 @@ iccl_result_t iccl_gather_rows(const void* src, void* dst, const int64_t* idx, i
                                int ctas, cudaStream_t stream);
 iccl_result_t iccl_scatter_rows(const void* src, void* dst, const int64_t* idx, int64_t n_rows, int64_t row_bytes,
                                 int ctas, cudaStream_t stream);
+/* Dispatch pack in expand form: dst row pos[t*k + j] <- src row t for every
+ * source row t < n_src_rows and j < k (each source row read once, written k
+ * times; pos is the inverse of the gather index).  Same result as
+ * iccl_gather_rows with idx[pos[t*k + j]] = t. */
+iccl_result_t iccl_expand_rows(const void* src, void* dst, const int64_t* pos, int64_t n_src_rows, int32_t k,
+                               int64_t row_bytes, int ctas, cudaStream_t stream);
 /* SM copy kernel (K1) on its own, for measurement and for callers that want
  * the SM path explicitly: copies bytes src -> dst with <= ctas CTAs. */
 iccl_result_t iccl_copy_sm(const void* src, void* dst, size_t bytes, int ctas, cudaStream_t stream);

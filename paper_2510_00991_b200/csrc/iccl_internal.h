@@ -113,6 +113,9 @@ cudaError_t launch_read_globaltimer(unsigned long long* out, cudaStream_t st);
 // dst_rows[idx[i]] <- src_rows[i] (scatter).  Rows are 16-byte multiples.
 cudaError_t launch_gather_rows(const void* src, void* dst, const int64_t* idx, int64_t n_rows, int64_t row_bytes,
                                int ctas, cudaStream_t st);
+// K2 expand form: dst_rows[pos[t*k + j]] <- src_rows[t] for j < k (each source row read once).
+cudaError_t launch_expand_rows(const void* src, void* dst, const int64_t* pos, int64_t n_src, int k,
+                               int64_t row_bytes, int ctas, cudaStream_t st);
 cudaError_t launch_scatter_rows(const void* src, void* dst, const int64_t* idx, int64_t n_rows, int64_t row_bytes,
                                 int ctas, cudaStream_t st);
 }  // namespace iccl

@@ -213,6 +213,38 @@ __global__ void __launch_bounds__(256) iccl_gather_rows(const int4* __restrict__
   for (int64_t r = warp; r < n_rows; r += nwarps) warp_copy_row(src + idx[r] * row16, dst + r * row16, row16, lane);
 }
 
+// K2 (expand form): dispatch pack reading every token once: warp per token
+// t, each 16 B column chunk loaded once and stored to its k packed rows
+// dst[pos[t*k + j]].  DRAM traffic = T rows read + T*k rows written, versus
+// T*k reads for the gather form (measured: the gather's re-reads miss L2,
+// profiles/r01/ncu/k2k3_full_summary.csv).
+__global__ void __launch_bounds__(256) iccl_expand_rows(const int4* __restrict__ src, int4* __restrict__ dst,
+                                                       const int64_t* __restrict__ pos, int64_t n_src, int k,
+                                                       int64_t row16) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = warp; t < n_src; t += nwarps) {
+    const int4* s = src + t * row16;
+    const int64_t* p = pos + t * k;
+    int64_t c = lane;
+    for (; c + 96 < row16; c += 128) {
+      const int4 v0 = ld_nc(s + c), v1 = ld_nc(s + c + 32), v2 = ld_nc(s + c + 64), v3 = ld_nc(s + c + 96);
+      for (int j = 0; j < k; j++) {
+        int4* d = dst + p[j] * row16;
+        st_cs(d + c, v0);
+        st_cs(d + c + 32, v1);
+        st_cs(d + c + 64, v2);
+        st_cs(d + c + 96, v3);
+      }
+    }
+    for (; c < row16; c += 32) {
+      const int4 v = ld_nc(s + c);
+      for (int j = 0; j < k; j++) st_cs(dst + p[j] * row16 + c, v);
+    }
+  }
+}
+
 // K3: inverse permutation (combine unpack), dst row idx[r] <- src row r.
 __global__ void __launch_bounds__(256) iccl_scatter_rows(const int4* __restrict__ src, int4* __restrict__ dst,
                                                         const int64_t* __restrict__ idx, int64_t n_rows,
@@ -365,7 +397,7 @@ cudaError_t preload_kernels() {
   cudaFuncAttributes a;
   const void* fns[] = {(const void*)iccl_copy_tma,   (const void*)iccl_copy_unaligned, (const void*)iccl_stamp,
                        (const void*)iccl_read_globaltimer, (const void*)iccl_gather_rows,
-                       (const void*)iccl_scatter_rows,
+                       (const void*)iccl_scatter_rows, (const void*)iccl_expand_rows,
                        (const void*)iccl_ll_group};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
@@ -402,6 +434,15 @@ cudaError_t launch_gather_rows(const void* src, void* dst, const int64_t* idx, i
   if ((row_bytes & 15) || ((uintptr_t)src & 15) || ((uintptr_t)dst & 15)) return cudaErrorInvalidValue;
   iccl_gather_rows<<<rows_grid(n_rows, ctas), 256, 0, st>>>((const int4*)src, (int4*)dst, idx, n_rows,
                                                             row_bytes / 16);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_expand_rows(const void* src, void* dst, const int64_t* pos, int64_t n_src, int k,
+                               int64_t row_bytes, int ctas, cudaStream_t st) {
+  if (n_src == 0 || k == 0) return cudaSuccess;
+  if ((row_bytes & 15) || ((uintptr_t)src & 15) || ((uintptr_t)dst & 15)) return cudaErrorInvalidValue;
+  iccl_expand_rows<<<rows_grid(n_src, ctas), 256, 0, st>>>((const int4*)src, (int4*)dst, pos, n_src, k,
+                                                           row_bytes / 16);
   return cudaGetLastError();
 }
 

@@ -1892,6 +1892,14 @@ iccl_result_t iccl_scatter_rows(const void* src, void* dst, const int64_t* idx, 
   return ICCL_SUCCESS;
 }
 
+iccl_result_t iccl_expand_rows(const void* src, void* dst, const int64_t* pos, int64_t n_src, int32_t k,
+                               int64_t row_bytes, int ctas, cudaStream_t s) {
+  if ((n_src > 0 && k > 0 && (!src || !dst || !pos)) || n_src < 0 || k < 0 || row_bytes <= 0)
+    return ICCL_ERR_INVALID_ARGUMENT;
+  ICCL_CHECK_CUDA(launch_expand_rows(src, dst, pos, n_src, k, row_bytes, ctas > 0 ? ctas : 148 * 8, s));
+  return ICCL_SUCCESS;
+}
+
 iccl_result_t iccl_copy_sm(const void* src, void* dst, size_t bytes, int ctas, cudaStream_t s) {
   if (bytes > 0 && (!src || !dst)) return ICCL_ERR_INVALID_ARGUMENT;
   ICCL_CHECK_CUDA(launch_copy(src, dst, bytes, ctas > 0 ? ctas : 16, nullptr, s));

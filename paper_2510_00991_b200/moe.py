@@ -39,6 +39,19 @@ def gather_rows(src: torch.Tensor, idx: torch.Tensor, out: Optional[torch.Tensor
     return out
 
 
+def expand_rows(src: torch.Tensor, pos: torch.Tensor, k: int, out: torch.Tensor, ctas: int = 0,
+                stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """out[pos[t*k + j]] = src[t] for j < k (K2, expand form: every source row
+    read once and written k times — the dispatch pack without the gather's
+    k-fold re-reads)."""
+    if pos.dtype != torch.int64 or not pos.is_cuda or pos.numel() != src.shape[0] * k:
+        raise InvalidArgument("pos must be a CUDA int64 tensor of src rows x k entries")
+    row = out[0].numel() * out.element_size() if out.shape[0] else 16
+    raise_for(lib.iccl_expand_rows(C.c_void_p(src.data_ptr()), C.c_void_p(out.data_ptr()), C.c_void_p(pos.data_ptr()),
+                                   src.shape[0], int(k), row, int(ctas), _sh(stream)), "iccl_expand_rows")
+    return out
+
+
 def scatter_rows(src: torch.Tensor, idx: torch.Tensor, out: torch.Tensor, ctas: int = 0,
                  stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
     """out[idx[i]] = src[i] (K3)."""
@@ -55,6 +68,7 @@ def scatter_rows(src: torch.Tensor, idx: torch.Tensor, out: torch.Tensor, ctas: 
 class DispatchPlan:
     order: torch.Tensor          # [T*k] int64: flattened (token, k) index of each packed row
     token_of_row: torch.Tensor   # [T*k] int64: token index of each packed row
+    pos: torch.Tensor            # [T*k] int64: packed row of each flattened (token, k) pair (inverse of order)
     send_counts: List[int]       # rows to each rank
     recv_counts: List[int]       # rows from each rank
 
@@ -72,13 +86,17 @@ def plan_dispatch(expert_ids: torch.Tensor, n_experts: int, world: int, counts_e
     order = torch.sort(key, stable=True).indices
     counts = torch.bincount(dest, minlength=world).tolist()
     recv = counts_exchange(counts)
-    return DispatchPlan(order, torch.div(order, k, rounding_mode="floor"), counts, recv)
+    pos = torch.empty_like(order)
+    pos[order] = torch.arange(order.numel(), device=order.device)
+    return DispatchPlan(order, torch.div(order, k, rounding_mode="floor"), pos, counts, recv)
 
 
 def moe_dispatch(comm, tokens: torch.Tensor, plan: DispatchPlan, packed: Optional[torch.Tensor] = None,
                  recv: Optional[torch.Tensor] = None, stream=None):
     """tokens [T, H] -> rows received from every rank, grouped by source."""
-    packed = gather_rows(tokens, plan.token_of_row, packed, stream=stream)
+    if packed is None:
+        packed = torch.empty((plan.order.numel(),) + tuple(tokens.shape[1:]), dtype=tokens.dtype, device=tokens.device)
+    expand_rows(tokens, plan.pos, plan.order.numel() // tokens.shape[0], packed, stream=stream)
     if recv is None:
         recv = torch.empty((sum(plan.recv_counts),) + tuple(tokens.shape[1:]), dtype=tokens.dtype,
                            device=tokens.device)

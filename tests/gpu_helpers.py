@@ -27,8 +27,14 @@ def free_port() -> int:
 
 
 def _worker(rank, world, port, fn, outdir, kwargs):
+    import faulthandler
+    import sys
     import torch
     import torch.distributed as dist
+    # a hung rank leaves its Python stacks behind for the parent's error report
+    log = open(os.path.join(outdir, f"rank{rank}.log"), "w")
+    sys.stdout = sys.stderr = log
+    faulthandler.dump_traceback_later(kwargs.pop("_hang_s", 100), exit=True, file=log)
     try:
         torch.cuda.set_device(rank)
         store = dist.TCPStore("127.0.0.1", port, world, rank == 0, wait_for_workers=True)
@@ -45,7 +51,7 @@ def _worker(rank, world, port, fn, outdir, kwargs):
         raise
 
 
-def run_ranks(world: int, fn, tmpdir, timeout: float = 240.0, **kwargs):
+def run_ranks(world: int, fn, tmpdir, timeout: float = 120.0, **kwargs):
     """Run fn(comm, rank, world, **kwargs) -> dict of numpy arrays on `world`
     GPUs, one process each; returns the per-rank dicts."""
     import torch.multiprocessing as mp
@@ -64,6 +70,9 @@ def run_ranks(world: int, fn, tmpdir, timeout: float = 240.0, **kwargs):
         ef = os.path.join(str(tmpdir), f"rank{r}.err")
         if os.path.exists(ef):
             errs.append(open(ef).read())
+        if p.exitcode not in (0, None) and not os.path.exists(ef):
+            lf = os.path.join(str(tmpdir), f"rank{r}.log")
+            errs.append(f"rank {r} exit code {p.exitcode}:\n" + (open(lf).read()[-6000:] if os.path.exists(lf) else ""))
     if errs:
         raise AssertionError("\n".join(errs))
     return [dict(np.load(os.path.join(str(tmpdir), f"rank{r}.npz"))) for r in range(world)]

@@ -112,6 +112,15 @@ def test_k2_k3_gather_scatter(torch_cuda):
     g = gather_rows(s, i)
     torch.cuda.synchronize()
     assert np.array_equal(g.cpu().numpy(), src[idx])
+    from paper_2510_00991_b200 import expand_rows
+    k = 3
+    order = rng.permutation(rows * k)
+    pos = np.empty_like(order)
+    pos[order] = np.arange(rows * k)
+    e = torch.zeros(rows * k, H, dtype=torch.uint8, device="cuda")
+    expand_rows(s, torch.from_numpy(pos).cuda(), k, e)
+    torch.cuda.synchronize()
+    assert np.array_equal(e.cpu().numpy(), src[order // k])
     perm = rng.permutation(rows)
     out = torch.zeros_like(s)
     scatter_rows(s, torch.from_numpy(perm).cuda(), out)
