@@ -112,17 +112,20 @@ def main():
         step()
     # off / armed, ABAB-interleaved (3 rounds) to cancel drift
     never = iccl.FaultScript().down(src_r, dst_r, chunk=1 << 30, op_index=1 << 20)
-    t_off, t_armed = [], []
+    t_off, t_mon, t_armed = [], [], []
     for _ in range(3):
         comm.monitor.enable(False)
         comm.set_faults(iccl.FaultScript())
         t_off.append(timed(args.steps))
         comm.monitor.enable(True, 8)
+        t_mon.append(timed(args.steps))
         comm.set_faults(never)
         t_armed.append(timed(args.steps))
-    pre_recs = comm.monitor.drain()  # armed-phase records: the pre-fault baseline of the window series
+    pre_recs = comm.monitor.drain()  # monitor-phase records: the pre-fault baseline of the window series
     res["t_off_ms"] = round(statistics.median(t_off), 4)
+    res["t_monitor_ms"] = round(statistics.median(t_mon), 4)
     res["t_armed_ms"] = round(statistics.median(t_armed), 4)
+    res["monitor_overhead"] = round(statistics.median(t_mon) / statistics.median(t_off) - 1, 4)
     res["monitor_failover_overhead"] = round(statistics.median(t_armed) / statistics.median(t_off) - 1, 4)
     res["bit_exact_armed"] = all_ok()
 

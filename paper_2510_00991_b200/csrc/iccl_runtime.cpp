@@ -11,8 +11,11 @@
 //                                         on the caller's stream: 0 SMs, no callbacks
 //   User Buffer Registration (:410-412)   IPC export of the caller's allocation, cached
 //                                         by CU_POINTER_ATTRIBUTE_BUFFER_ID
-//   CTS                     recv-posted entry in the sender's CTS ring of
-//                                         the shared control block (shm)
+//   CTS / RTS               each side's posting (buffer IPC handle, op slot)
+//                                         in the pair's rendezvous ring (shm); the side
+//                                         that arrives second issues the copies from its
+//                                         own API call: push by the sender, pull by the
+//                                         receiver
 //   WR post / WC        chunk copy enqueue / device-written progress
 //                                         word observed by the proxy
 //   primary QP / backup QP (:461)         copy-engine path / SM-kernel path (K1)
@@ -22,9 +25,17 @@
 //   RNIC port down         injected gate: cuStreamWaitValue32 on a host
 //                                         word placed before chunks on the primary path
 //
-// Data moves zero-copy: the sender's copy engine (or K1) writes straight into
-// the receiver's tensor through an IPC mapping — no FIFO, no staging copy
-// (PAPER.md:214-217, 240-243).
+// Data moves zero-copy: a copy engine (or K1) moves the bytes straight from
+// the sender's tensor into the receiver's tensor through an IPC mapping — no
+// FIFO, no staging copy.
+//
+// Why the API thread issues the copies (and the proxy only observes, monitors
+// and re-issues on failover): while any thread of the process sits in a
+// synchronous CUDA call (e.g. a pageable cudaMemcpy) on a stream parked behind
+// one of our ops, every other CUDA call of the process blocks — memcpy,
+// kernel launch, stream memop, event record alike (probes/p2p_probe6).  A
+// proxy that still had to enqueue the copy would deadlock with such a user;
+// all device work an op needs is therefore enqueued before the API returns.
 #include <errno.h>
 #include <fcntl.h>
 #include <pthread.h>
@@ -50,9 +61,20 @@
 
 namespace iccl {
 
+// ICCL_DEBUG=1: the proxy traces every device call it makes (stderr), so a
+// stuck proxy shows the call it is blocked in.
+static const bool g_debug = getenv("ICCL_DEBUG") && atoi(getenv("ICCL_DEBUG")) > 0;
+#define ICCL_TRACE(...)                    \
+  do {                                     \
+    if (::iccl::g_debug) {                 \
+      fprintf(stderr, "[iccl] " __VA_ARGS__); \
+      fputc('\n', stderr);                 \
+    }                                      \
+  } while (0)
+
 constexpr uint64_t kMagic = 0x3030324242434349ull;  // "ICCLB200"
 constexpr int kSlots = 4096;                        // op slots per rank (ready/done flags)
-constexpr int kCtsDepth = 1024;                     // recv postings in flight per ordered pair
+constexpr int kRzvDepth = 1024;                     // rendezvous entries per ordered pair
 constexpr int kMaxRanks = 64;
 constexpr int kGateWords = 1024;
 constexpr int kStampSlots = 4096;
@@ -99,27 +121,34 @@ struct alignas(64) RankFlags {
   XferPub pub[kSlots];
 };
 
-struct alignas(64) CtsEntry {
-  std::atomic<uint64_t> seq;  // 1-based index of this recv on the pair; published last
+// One side's posting of the k-th op of an ordered pair (RTS from the sender,
+// CTS from the receiver).
+struct RzvSide {
   uint64_t bytes;
-  uint64_t buffer_id;
-  uint64_t base_offset;
-  uint64_t direct_ptr;  // self-sends: plain pointer
-  uint32_t ready_slot, ready_gen, done_slot, done_gen;
+  uint64_t buffer_id;    // CU_POINTER_ATTRIBUTE_BUFFER_ID of the allocation (0: self pair, use direct_ptr)
+  uint64_t base_offset;  // offset of the tensor inside that allocation
+  uint64_t direct_ptr;   // the tensor's pointer in its owner's address space
+  uint32_t slot, gen;    // the owner's op slot: ready / done flags and six-pointer record
   cudaIpcMemHandle_t handle;
 };
 
-// Per ordered pair src->dst: recv postings by dst, consumed by src's proxy;
-// the sender proxy mirrors the receiver-side pointers for iccl_req_state.
-struct alignas(64) PairState {
-  std::atomic<uint64_t> consumed;
-  std::atomic<uint64_t> cur_seq;
-  std::atomic<int32_t> total, done, active_path, switches;
+// Rendezvous of the k-th send and the k-th recv of an ordered pair: each side
+// writes its half, then bumps `arrivals`; the side that sees 2g+1 (g = k /
+// depth) arrived second and issues the transfer.
+struct alignas(64) RzvEntry {
+  std::atomic<uint64_t> arrivals;
+  RzvSide side[2];  // 0 sender, 1 receiver
 };
 
-struct alignas(64) CtsRing {
+// Per ordered pair src->dst: the active path (shared by whichever side
+// issues) and the rendezvous ring.
+struct alignas(64) PairState {
+  std::atomic<int32_t> active_path, switches;
+};
+
+struct alignas(64) RzvRing {
   PairState st;
-  CtsEntry e[kCtsDepth];
+  RzvEntry e[kRzvDepth];
 };
 
 // GPU-relay backup path (SURVEY.md §2.3 N9, §8e "Relay backup"): source s
@@ -156,7 +185,7 @@ struct ShmLayout {
     o += sizeof(RankFlags) * n;
     o = (o + 4095) & ~(size_t)4095;
     off_rings = o;
-    o += sizeof(CtsRing) * n * n;
+    o += sizeof(RzvRing) * n * n;
     o = (o + 4095) & ~(size_t)4095;
     // per relay rank: in[n], out[n] counters, then req[n][kRelayDepth]
     off_relay = o;
@@ -201,13 +230,15 @@ struct ChunkRec {
 };
 
 struct Xfer {
-  uint64_t op_seq = 0;
-  uint64_t cts_seq = 0;
-  const char* src = nullptr;
-  char* dst = nullptr;
+  uint64_t op_seq = 0;   // the issuer's op number (monitor records)
+  uint64_t pair_seq = 0;  // k: the k-th op of the ordered pair src_rank -> dst_rank
+  int src_rank = 0, dst_rank = 0;
+  int chan = -1;  // issuing channel (2 * peer + dir)
+  const char* src = nullptr;  // sender's tensor (local, or IPC-mapped when the receiver pulls)
+  char* dst = nullptr;        // receiver's tensor (local, or IPC-mapped when the sender pushes)
   size_t bytes = 0;
-  uint32_t s_slot = 0, s_gen = 0;
-  uint32_t r_ready_slot = 0, r_ready_gen = 0, r_done_slot = 0, r_done_gen = 0;
+  uint32_t s_slot = 0, s_gen = 0;  // sender's op slot
+  uint32_t r_ready_slot = 0, r_ready_gen = 0, r_done_slot = 0, r_done_gen = 0;  // receiver's
   int nchunks = 0;
   size_t chunk = 0;
   // receiver's buffer as exported in its CTS (the relay forwards into it)
@@ -249,20 +280,21 @@ struct FaultState {
   std::vector<int> probe_gates;  // probes parked while down: released on Up
 };
 
+// One direction of traffic with one peer, as seen by the issuing side:
+// dir 0 = push (I send to peer), dir 1 = pull (peer sends to me).  The
+// transfers I issue for that ordered pair live here.
 struct Channel {
   int peer = -1;
-  std::deque<OpDesc> sends;  // waiting for the receiver's CTS
-  uint64_t next_cts = 1;
-  std::deque<Xfer> xfers;    // matched, in issue order
+  int dir = 0;
+  int src = -1, dst = -1;  // ranks of the ordered pair
+  std::deque<Xfer> xfers;    // issued by this rank, in issue order
   std::vector<int> path_streams[2];
   int probe_stream = -1;
-  int active_path = 0;
   // on the backup because the primary failed (watchdog + probe): only then
   // does monitor_failed_link probe the primary to switch back;
   // an API switch_qp is sticky until the next API switch
   bool failed_over = false;
   FaultState fault[2];
-  std::unordered_map<uint64_t, char*> ipc;  // receiver buffer_id -> mapped base
   // probe state
   bool probe_out = false;
   int probe_gate = -1;
@@ -270,8 +302,8 @@ struct Channel {
   uint64_t probe_sent = 0;
   int probe_path = 0;
   uint64_t last_probe = 0;
-  int sends_seen = 0;  // for chunk-triggered faults
-  char* peer_scratch = nullptr;
+  uint64_t fault_seq_base = 0;  // pair op count at iccl_fault_set (chunk-triggered faults count from here)
+  char* peer_scratch = nullptr;  // 16 B probe target on the peer
   int relay_rank = -1;  // relay GPU of the backup path: lowest rank not an endpoint (topology.py:140-151 tie-break)
 };
 
@@ -294,15 +326,15 @@ struct iccl_comm {
   ShmHeader* hdr = nullptr;
   RankInfo* ranks = nullptr;
   RankFlags* flags = nullptr;
-  CtsRing* rings = nullptr;
+  RzvRing* rings = nullptr;
   int bar_sense = 0;
   // private pinned host memory (progress words, gates, probe words, stamps)
   uint32_t* pinned = nullptr;
   size_t pinned_bytes = 0;
   volatile uint32_t* gate_words = nullptr;
-  int next_gate = 0;
+  std::atomic<int> next_gate{0};
   KernelStamp* stamps = nullptr;
-  int next_stamp = 0;
+  std::atomic<int> next_stamp{0};
   unsigned long long* gtimer = nullptr;
   int64_t gtimer_offset = 0;  // host_ns - globaltimer_ns
   char* scratch = nullptr;    // device scratch (probe target), exported to peers
@@ -320,31 +352,35 @@ struct iccl_comm {
   std::vector<uint32_t> relay_sent;  // pieces I pushed through relay r
   std::vector<uint64_t> relay_next;  // next request I (as relay) expect from source s
   std::vector<int> relay_serve;      // my forwarding stream per source (index into streams)
-  std::map<std::pair<int, uint64_t>, char*> relay_ipc;  // (dst rank, buffer id) -> mapped base
   // API state
   uint64_t op_seq = 0;
+  std::vector<uint64_t> pair_sends, pair_recvs;  // non-LL ops posted per peer (rendezvous index k)
+  std::vector<std::unordered_map<uint64_t, char*>> peer_ipc;  // per peer: its buffer id -> mapped base
+  std::vector<char*> peer_scratch_base;                       // IPC-opened peer scratch blocks
   int group_depth = 0;
   std::vector<std::pair<OpDesc, cudaStream_t>> group_ops;
   std::unordered_map<uint64_t, cudaIpcMemHandle_t> export_cache;
   // proxy
-  std::vector<Channel> ch;
+  std::vector<Channel> ch;  // 2 per peer: [2 * peer + dir]
   std::vector<StreamCtx> streams;
   std::thread proxy;
   std::atomic<bool> stop{false};
   std::mutex qmu;
   std::condition_variable qcv;
-  std::vector<OpDesc> inbox;
+  std::vector<Xfer> handoff;  // issued by the API thread, tracked by the proxy
   std::mutex mon_mu;
   std::deque<iccl_mon_rec_t> mon;
   std::deque<iccl_switch_event_t> sw_events;
   std::atomic<int> monitor_enabled{0};
   std::atomic<int> async_err{ICCL_SUCCESS};
   std::string async_msg;
-  std::mutex fault_mu;
+  std::mutex fault_mu;  // fault script + per-channel fault / gate state (API thread and proxy)
+  std::mutex ev_mu;     // event pools (API thread and proxy)
+  std::mutex relay_mu;  // relay piece counters (API thread and proxy)
+  std::mutex ipc_mu;    // peer_ipc (API thread and the relay server)
   std::vector<Fault> faults;
   uint64_t faults_t0 = 0;
-  std::atomic<int> path_req[kMaxRanks];  // API-requested switches: -1 none, else target path
-  std::atomic<int> active_path_pub[kMaxRanks];
+  std::atomic<int> path_req[2 * kMaxRanks];  // API-requested switches per channel: -1 none, else target path
   std::atomic<uint64_t> pending_xfers{0};
   std::atomic<uint64_t> kernels_launched{0}, copies_issued{0}, bytes_issued{0};
   std::vector<cudaEvent_t> event_pool;  // proxy-owned: chunk WC events
@@ -361,11 +397,17 @@ struct iccl_comm {
 namespace iccl {
 
 static RankFlags* flags_of(iccl_comm* c, int r) { return &c->flags[r]; }
-static CtsRing* ring_of(iccl_comm* c, int src, int dst) { return &c->rings[src * c->nranks + dst]; }
+static RzvRing* ring_of(iccl_comm* c, int src, int dst) { return &c->rings[src * c->nranks + dst]; }
+static PairState& pair_of(iccl_comm* c, int src, int dst) { return ring_of(c, src, dst)->st; }
 
 static void set_async(iccl_comm* c, iccl_result_t e, const std::string& msg) {
   int expected = ICCL_SUCCESS;
-  if (c->async_err.compare_exchange_strong(expected, e)) c->async_msg = msg;
+  if (c->async_err.compare_exchange_strong(expected, e)) {
+    c->async_msg = msg;
+    // like NCCL's WARN: the first asynchronous error of a communicator is
+    // printed once, since the API thread may be blocked on the stream
+    fprintf(stderr, "[iccl_b200 rank %d] async error %s: %s\n", c->rank, iccl_get_error_string(e), msg.c_str());
+  }
 }
 
 // sense-reversing barrier over the shm header
@@ -391,15 +433,18 @@ static iccl_result_t shm_barrier(iccl_comm* c, double timeout_s = 120.0) {
 
 // ---------------------------------------------------------------- proxy helpers
 static iccl_result_t memop_write(cudaStream_t s, volatile void* addr, uint32_t v) {
+  ICCL_TRACE("write %p <- %u on %p", (void*)addr, v, (void*)s);
   ICCL_CHECK_CU(driver()->cuStreamWriteValue32((CUstream)s, (CUdeviceptr)addr, v, CU_STREAM_WRITE_VALUE_DEFAULT));
   return ICCL_SUCCESS;
 }
 static iccl_result_t memop_wait(cudaStream_t s, volatile void* addr, uint32_t v) {
+  ICCL_TRACE("wait %p >= %u on %p", (void*)addr, v, (void*)s);
   ICCL_CHECK_CU(driver()->cuStreamWaitValue32((CUstream)s, (CUdeviceptr)addr, v, CU_STREAM_WAIT_VALUE_GEQ));
   return ICCL_SUCCESS;
 }
 
 static cudaEvent_t get_event(iccl_comm* c) {
+  std::lock_guard<std::mutex> g(c->ev_mu);
   if (c->event_pool.empty()) {
     cudaEvent_t e = nullptr;
     cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
@@ -412,6 +457,7 @@ static cudaEvent_t get_event(iccl_comm* c) {
 }
 
 static cudaEvent_t get_tevent(iccl_comm* c) {
+  std::lock_guard<std::mutex> g(c->ev_mu);
   if (c->tevent_pool.empty()) {
     cudaEvent_t e = nullptr;
     cudaEventCreate(&e);
@@ -424,6 +470,7 @@ static cudaEvent_t get_tevent(iccl_comm* c) {
 }
 
 static void put_events(iccl_comm* c, Xfer& x) {
+  std::lock_guard<std::mutex> g(c->ev_mu);
   for (ChunkRec& r : x.rec)
     if (r.ev) {
       (r.timed ? c->tevent_pool : c->event_pool).push_back(r.ev);
@@ -452,9 +499,9 @@ static void publish_one(XferPub& p, uint32_t gen, const Xfer& x) {
 }
 
 // Mirror the transfer's pointers into the sender's and the receiver's op slot.
-static void publish(iccl_comm* c, Channel& chn, const Xfer& x) {
-  publish_one(flags_of(c, c->rank)->pub[x.s_slot], x.s_gen, x);
-  publish_one(flags_of(c, chn.peer)->pub[x.r_done_slot], x.r_done_gen, x);
+static void publish(iccl_comm* c, const Xfer& x) {
+  publish_one(flags_of(c, x.src_rank)->pub[x.s_slot], x.s_gen, x);
+  publish_one(flags_of(c, x.dst_rank)->pub[x.r_done_slot], x.r_done_gen, x);
 }
 
 static int alloc_gate(iccl_comm* c) {
@@ -476,19 +523,34 @@ static void push_switch_event(iccl_comm* c, int peer, int to, int resume, int tr
   if (c->sw_events.size() > 65536) c->sw_events.pop_front();
 }
 
-static iccl_result_t open_peer_buffer(iccl_comm* c, Channel& chn, const CtsEntry& e, char** out) {
+// Base of rank `owner`'s allocation `buffer_id` in my address space, opened
+// over CUDA IPC once and cached (the analog of User Buffer Registration,
+// PAPER.md:410-412).  Shared by the API thread and the relay server.
+static iccl_result_t map_peer_allocation(iccl_comm* c, int owner, uint64_t buffer_id, cudaIpcMemHandle_t handle,
+                                         char** base) {
+  std::lock_guard<std::mutex> g(c->ipc_mu);
+  auto& cache = c->peer_ipc[owner];
+  auto it = cache.find(buffer_id);
+  if (it == cache.end()) {
+    void* p = nullptr;
+    ICCL_CHECK_CUDA(cudaIpcOpenMemHandle(&p, handle, cudaIpcMemLazyEnablePeerAccess));
+    it = cache.emplace(buffer_id, (char*)p).first;
+  }
+  *base = it->second;
+  return ICCL_SUCCESS;
+}
+
+// The other side's tensor in my address space: its own pointer for a self
+// pair, else inside its IPC-mapped allocation.
+static iccl_result_t open_peer_buffer(iccl_comm* c, Channel& chn, const RzvSide& e, char** out) {
   if (chn.peer == c->rank) {
     *out = (char*)(uintptr_t)e.direct_ptr;
     return ICCL_SUCCESS;
   }
-  auto it = chn.ipc.find(e.buffer_id);
-  if (it == chn.ipc.end()) {
-    void* p = nullptr;
-    cudaIpcMemHandle_t h = e.handle;
-    ICCL_CHECK_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
-    it = chn.ipc.emplace(e.buffer_id, (char*)p).first;
-  }
-  *out = it->second + e.base_offset;
+  char* base = nullptr;
+  iccl_result_t r = map_peer_allocation(c, chn.peer, e.buffer_id, e.handle, &base);
+  if (r) return r;
+  *out = base + e.base_offset;
   return ICCL_SUCCESS;
 }
 
@@ -528,6 +590,7 @@ static size_t relay_pieces(iccl_comm* c, size_t n) { return (n + c->relay_slot_b
 // Returns ICCL_ERR_IN_PROGRESS (nothing issued) if rr's request ring is full.
 static iccl_result_t relay_push(iccl_comm* c, Channel& chn, Xfer& x, size_t off, size_t n, cudaStream_t s,
                                 ChunkRec& rc) {
+  std::lock_guard<std::mutex> g(c->relay_mu);
   const int rr = chn.relay_rank, me = c->rank;
   const uint32_t out_now = __atomic_load_n(&relay_out(c, rr, me)->v, __ATOMIC_ACQUIRE);
   if ((int32_t)(c->relay_sent[rr] + (uint32_t)relay_pieces(c, n) - out_now) > kRelayDepth) return ICCL_ERR_IN_PROGRESS;
@@ -576,19 +639,14 @@ static iccl_result_t serve_relays(iccl_comm* c, bool* busy) {
       const uint64_t q = c->relay_next[src];
       RelayReq* rq = relay_req(c, c->rank, src, q);
       if (rq->seq.load(std::memory_order_acquire) != q) break;
-      auto key = std::make_pair((int)rq->dst, rq->buffer_id);
-      auto it = c->relay_ipc.find(key);
-      if (it == c->relay_ipc.end()) {
-        void* p = nullptr;
-        cudaIpcMemHandle_t h = rq->handle;
-        ICCL_CHECK_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
-        it = c->relay_ipc.emplace(key, (char*)p).first;
-      }
+      char* dbase = nullptr;
+      iccl_result_t r0 = map_peer_allocation(c, rq->dst, rq->buffer_id, rq->handle, &dbase);
+      if (r0) return r0;
       cudaStream_t st = c->streams[c->relay_serve[src]].s;
       const char* stage = c->relay_buf + ((size_t)src * kRelaySlots + rq->slot) * c->relay_slot_bytes;
       iccl_result_t r = memop_wait(st, &relay_in(c, c->rank, src)->v, (uint32_t)q);
       if (r) return r;
-      ICCL_CHECK_CU(driver()->cuMemcpyDtoDAsync((CUdeviceptr)(it->second + rq->base_offset), (CUdeviceptr)stage,
+      ICCL_CHECK_CU(driver()->cuMemcpyDtoDAsync((CUdeviceptr)(dbase + rq->base_offset), (CUdeviceptr)stage,
                                                 rq->bytes, (CUstream)st));
       r = memop_write(st, &relay_out(c, c->rank, src)->v, (uint32_t)q);
       if (r) return r;
@@ -617,29 +675,38 @@ static void fault_up(iccl_comm* c, FaultState& fs) {
   fs.probe_gates.clear();
 }
 
+// A fault on directed path src -> dst applies on both endpoints (either may
+// issue the pair's next transfer): on every channel of this rank that can
+// issue over that path (one push or one pull channel; both for a self pair).
+static void apply_fault(iccl_comm* c, FaultState& fs, bool up, uint64_t t) {
+  if (!up && !fs.down) {
+    fs.down = true;
+    fs.gate = alloc_gate(c);
+    fs.down_at = t;
+  } else if (up && fs.down) {
+    fault_up(c, fs);
+  }
+}
+
 static void fire_time_faults(iccl_comm* c) {
   std::lock_guard<std::mutex> g(c->fault_mu);
   uint64_t t = now_ns();
   for (auto& f : c->faults) {
-    if (f.fired || f.f.trigger_kind != 0 || f.f.src != c->rank) continue;
+    if (f.fired || f.f.trigger_kind != 0) continue;
+    if (f.f.src != c->rank && f.f.dst != c->rank) continue;
     if (t - c->faults_t0 < f.f.t_us * 1000ull) continue;
     f.fired = true;
-    Channel& chn = c->ch[f.f.dst];
-    FaultState& fs = chn.fault[f.f.path & 1];
-    if (!f.f.up && !fs.down) {
-      fs.down = true;
-      fs.gate = alloc_gate(c);
-      fs.down_at = t;
-    } else if (f.f.up && fs.down) {
-      fault_up(c, fs);
-    }
+    for (Channel& chn : c->ch)
+      if (chn.src == f.f.src && chn.dst == f.f.dst) apply_fault(c, chn.fault[f.f.path & 1], f.f.up, t);
   }
 }
 
+// Chunk-triggered: fires when this rank issues chunk `chunk` of the
+// op_index-th transfer of the pair (counted from iccl_fault_set).  Caller
+// holds fault_mu.
 static void fire_chunk_faults(iccl_comm* c, Channel& chn, int op_index, int chunk, int path) {
-  std::lock_guard<std::mutex> g(c->fault_mu);
   for (auto& f : c->faults) {
-    if (f.fired || f.f.trigger_kind != 1 || f.f.src != c->rank || f.f.dst != chn.peer) continue;
+    if (f.fired || f.f.trigger_kind != 1 || f.f.src != chn.src || f.f.dst != chn.dst) continue;
     if (f.f.op_index != op_index || f.f.chunk != chunk || (f.f.path & 1) != path) continue;
     f.fired = true;
     FaultState& fs = chn.fault[path];
@@ -658,22 +725,16 @@ static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
   const int eng = path_engine(c, chn, path, x.bytes);
   const size_t off = (size_t)k * x.chunk;
   const size_t n = std::min(x.chunk, x.bytes - off);
-  if (eng == ENG_RELAY) {
-    // the relay's request ring must have room for every piece of the chunk
-    const uint32_t out_now = __atomic_load_n(&relay_out(c, chn.relay_rank, c->rank)->v, __ATOMIC_ACQUIRE);
-    if ((int32_t)(c->relay_sent[chn.relay_rank] + (uint32_t)relay_pieces(c, n) - out_now) > kRelayDepth)
-      return ICCL_ERR_IN_PROGRESS;
-  }
   const int si = stream_for(c, chn, path, eng, k);
   StreamCtx& sc = c->streams[si];
   const int bit = 1 << (si % 32);
-  RankFlags* mine = flags_of(c, c->rank);
-  RankFlags* theirs = flags_of(c, chn.peer);
+  RankFlags* sender = flags_of(c, x.src_rank);
+  RankFlags* receiver = flags_of(c, x.dst_rank);
   if (!(x.waited[path] & bit)) {
     // hostFunc#1 analog: the copy may start only once both user streams reached the op
-    iccl_result_t r = memop_wait(sc.s, &mine->ready[x.s_slot], x.s_gen);
+    iccl_result_t r = memop_wait(sc.s, &sender->ready[x.s_slot], x.s_gen);
     if (r) return r;
-    r = memop_wait(sc.s, &theirs->ready[x.r_ready_slot], x.r_ready_gen);
+    r = memop_wait(sc.s, &receiver->ready[x.r_ready_slot], x.r_ready_gen);
     if (r) return r;
     x.waited[path] |= bit;
     if (eng == ENG_CE && c->monitor_enabled.load(std::memory_order_relaxed)) {
@@ -685,10 +746,13 @@ static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
       x.last_ev.emplace_back(si, a);
     }
   }
-  if (x.fault_ops_index >= 0) fire_chunk_faults(c, chn, x.fault_ops_index, k, path);
-  if (chn.fault[path].down) {
-    iccl_result_t r = memop_wait(sc.s, &c->gate_words[chn.fault[path].gate], 1);
-    if (r) return r;
+  {
+    std::lock_guard<std::mutex> g(c->fault_mu);
+    if (x.fault_ops_index >= 0) fire_chunk_faults(c, chn, x.fault_ops_index, k, path);
+    if (chn.fault[path].down) {
+      iccl_result_t r = memop_wait(sc.s, &c->gate_words[chn.fault[path].gate], 1);
+      if (r) return r;
+    }
   }
   ChunkRec& rc = x.rec[k];
   rc.t1 = now_ns();
@@ -707,7 +771,7 @@ static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
   const bool mon = c->monitor_enabled.load(std::memory_order_relaxed);
   KernelStamp* st = nullptr;
   if (mon && eng == ENG_SM) {
-    rc.stamp = c->next_stamp++ % kStampSlots;
+    rc.stamp = c->next_stamp.fetch_add(1) % kStampSlots;
     st = &c->stamps[rc.stamp];
     memset((void*)st, 0, sizeof(KernelStamp));
   }
@@ -717,7 +781,9 @@ static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
       if (le.first == si) rc.t1ev = le.second;
   }
   if (eng == ENG_CE) {
+    ICCL_TRACE("copy op %llu chunk %d: %zu B on %p", (unsigned long long)x.op_seq, k, n, (void*)sc.s);
     ICCL_CHECK_CU(driver()->cuMemcpyDtoDAsync((CUdeviceptr)(x.dst + off), (CUdeviceptr)(x.src + off), n, (CUstream)sc.s));
+    ICCL_TRACE("copy issued");
     c->copies_issued += 1;
   } else if (eng == ENG_RELAY) {
     // two copy-engine hops through the relay GPU; the WC is the relay's
@@ -738,7 +804,9 @@ static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
     }
     if (!rc.ev) rc.ev = timed ? get_tevent(c) : get_event(c);
     rc.timed = timed;
+    ICCL_TRACE("event record");
     ICCL_CHECK_CUDA(cudaEventRecord(rc.ev, sc.s));
+    ICCL_TRACE("event recorded");
     if (timed) {
       for (auto& le : x.last_ev)
         if (le.first == si) le.second = rc.ev;
@@ -763,9 +831,9 @@ static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
       r = memop_wait(sc.s, &relay_out(c, x.relay_r, c->rank)->v, x.relay_last_q);
       if (r) return r;
     }
-    r = memop_write(sc.s, &theirs->done[x.r_done_slot], x.r_done_gen);
+    r = memop_write(sc.s, &receiver->done[x.r_done_slot], x.r_done_gen);
     if (r) return r;
-    r = memop_write(sc.s, &mine->done[x.s_slot], x.s_gen);
+    r = memop_write(sc.s, &sender->done[x.s_slot], x.s_gen);
     if (r) return r;
     x.done_enqueued = true;
   }
@@ -777,12 +845,17 @@ static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
 // and transmitted retreat to it; stale in-flight work on the abandoned path is
 // fenced so completion waits for it.
 static iccl_result_t switch_path(iccl_comm* c, Channel& chn, int to, int trigger) {
-  if (chn.active_path == to) return ICCL_SUCCESS;
-  const int from = chn.active_path;
+  PairState& ps = pair_of(c, chn.src, chn.dst);
+  bool moves = false;
+  for (Xfer& x : chn.xfers) moves |= x.path != to;
+  if (!moves && ps.active_path.load() == to) return ICCL_SUCCESS;
+  const int from = to ^ 1;
+  std::unique_lock<std::mutex> lk(c->fault_mu);
   uint64_t detect = chn.fault[from].down ? now_ns() - chn.fault[from].down_at : 0;
   int resume = -1;
   int stale_gate = chn.fault[from].down ? chn.fault[from].gate : -1;
   for (Xfer& x : chn.xfers) {
+    if (x.path == to) continue;
     // fence: an event after everything already queued on the abandoned path
     bool had_work = x.next_issue > x.completed || x.done_enqueued;
     if (had_work) {
@@ -802,7 +875,7 @@ static iccl_result_t switch_path(iccl_comm* c, Channel& chn, int to, int trigger
     x.switches++;
     if (had_work && stale_gate >= 0) x.pending_gate = stale_gate;
     x.last_progress = now_ns();
-    publish(c, chn, x);
+    publish(c, x);
   }
   if (stale_gate >= 0) {
     // future work on the still-Down path waits on a fresh gate epoch; the old
@@ -812,10 +885,8 @@ static iccl_result_t switch_path(iccl_comm* c, Channel& chn, int to, int trigger
     for (Xfer& x : chn.xfers) any_pending |= (x.pending_gate == stale_gate);
     if (!any_pending) release_gate(c, stale_gate);
   }
-  chn.active_path = to;
+  lk.unlock();
   chn.failed_over = (to == 1 && trigger == 1);
-  c->active_path_pub[chn.peer].store(to);
-  PairState& ps = ring_of(c, c->rank, chn.peer)->st;
   ps.active_path.store(to);
   ps.switches.fetch_add(1);
   if (chn.probe_gate >= 0) release_gate(c, chn.probe_gate);  // abandon the outstanding probe
@@ -840,14 +911,22 @@ static iccl_result_t send_probe(iccl_comm* c, Channel& chn, int path) {
   const int si = chn.probe_stream;
   StreamCtx& sc = c->streams[si];
   chn.probe_gate = -1;
-  if (chn.fault[path].down) {
-    chn.probe_gate = alloc_gate(c);
-    chn.fault[path].probe_gates.push_back(chn.probe_gate);
-    iccl_result_t r = memop_wait(sc.s, &c->gate_words[chn.probe_gate], 1);
-    if (r) return r;
+  {
+    std::lock_guard<std::mutex> g(c->fault_mu);
+    if (chn.fault[path].down) {
+      chn.probe_gate = alloc_gate(c);
+      chn.fault[path].probe_gates.push_back(chn.probe_gate);
+      iccl_result_t r = memop_wait(sc.s, &c->gate_words[chn.probe_gate], 1);
+      if (r) return r;
+    }
   }
-  // a 16-byte zero-payload-ish CTS over the suspect path into the peer's scratch
-  ICCL_CHECK_CU(driver()->cuMemcpyDtoDAsync((CUdeviceptr)chn.peer_scratch, (CUdeviceptr)c->scratch, 16, (CUstream)sc.s));
+  // a 16-byte CTS over the suspect path: into the peer's scratch (push
+  // channel) or out of it (pull channel)
+  if (chn.dir == 0)
+    ICCL_CHECK_CU(driver()->cuMemcpyDtoDAsync((CUdeviceptr)chn.peer_scratch, (CUdeviceptr)c->scratch, 16, (CUstream)sc.s));
+  else
+    ICCL_CHECK_CU(driver()->cuMemcpyDtoDAsync((CUdeviceptr)(c->scratch + 2048 + 16 * chn.peer),
+                                              (CUdeviceptr)chn.peer_scratch, 16, (CUstream)sc.s));
   chn.probe_ticket_expect = ++sc.ticket;
   iccl_result_t r = memop_write(sc.s, sc.prog, chn.probe_ticket_expect);
   if (r) return r;
@@ -880,6 +959,7 @@ static void record_monitor(iccl_comm* c, Channel& chn, Xfer& x, int k, uint64_t 
         // event: recycle it only two re-bases (>= 2 s) later
         c->old_bases.push_back(c->base_ev);
         if (c->old_bases.size() > 2) {
+          std::lock_guard<std::mutex> g(c->ev_mu);
           c->tevent_pool.push_back(c->old_bases.front());
           c->old_bases.pop_front();
         }
@@ -899,59 +979,17 @@ static void record_monitor(iccl_comm* c, Channel& chn, Xfer& x, int k, uint64_t 
   m.peer = chn.peer;
   m.path = rc.path;
   m.chunk = k;
-  m.dir = 0;
+  m.dir = chn.dir;
   m.op_seq = x.op_seq;
   std::lock_guard<std::mutex> g(c->mon_mu);
   c->mon.push_back(m);
   if (c->mon.size() > (1u << 20)) c->mon.pop_front();
 }
 
-// One proxy pass over a channel.  Returns true if anything moved.
+// One proxy pass over a channel: completions, retirement, re-issue after a
+// path switch, watchdog.  Sets *busy if anything moved.
 static iccl_result_t progress_channel(iccl_comm* c, Channel& chn, bool* busy) {
   iccl_result_t r;
-  // 1. match sends with the receiver's CTS (recv postings for rank->peer live in ring(rank, peer))
-  CtsRing* rr = ring_of(c, c->rank, chn.peer);
-  while (!chn.sends.empty()) {
-    CtsEntry& e = rr->e[(chn.next_cts - 1) % kCtsDepth];
-    if (e.seq.load(std::memory_order_acquire) != chn.next_cts) break;
-    OpDesc op = chn.sends.front();
-    chn.sends.pop_front();
-    if (e.bytes != op.bytes) {
-      set_async(c, ICCL_ERR_SIZE_MISMATCH,
-                "send of " + std::to_string(op.bytes) + " B to rank " + std::to_string(chn.peer) +
-                    " matched a recv of " + std::to_string(e.bytes) + " B");
-      return ICCL_ERR_SIZE_MISMATCH;
-    }
-    Xfer x;
-    x.op_seq = op.op_seq;
-    x.cts_seq = chn.next_cts;
-    x.src = op.src;
-    r = open_peer_buffer(c, chn, e, &x.dst);
-    if (r) return r;
-    x.bytes = op.bytes;
-    x.s_slot = op.slot;
-    x.s_gen = op.gen;
-    x.r_ready_slot = e.ready_slot;
-    x.r_ready_gen = e.ready_gen;
-    x.r_done_slot = e.done_slot;
-    x.r_done_gen = e.done_gen;
-    x.dst_buffer_id = e.buffer_id;
-    x.dst_base_offset = e.base_offset;
-    x.dst_handle = e.handle;
-    x.chunk = (size_t)c->cfg.chunk_bytes;
-    x.nchunks = (int)((x.bytes + x.chunk - 1) / x.chunk);
-    x.rec.resize(x.nchunks);
-    x.path = chn.active_path;
-    x.last_progress = now_ns();
-    x.fault_ops_index = chn.sends_seen++;
-    chn.next_cts++;
-    rr->st.consumed.store(chn.next_cts - 1, std::memory_order_release);
-    rr->st.cur_seq.store(x.cts_seq);
-    rr->st.total.store(x.nchunks);
-    rr->st.done.store(0);
-    chn.xfers.push_back(std::move(x));
-    *busy = true;
-  }
   if (chn.xfers.empty()) return ICCL_SUCCESS;
   // 2. completions: advance each xfer's contiguous delivered prefix (acked / done)
   const uint64_t tnow = now_ns();
@@ -976,8 +1014,7 @@ static iccl_result_t progress_channel(iccl_comm* c, Channel& chn, bool* busy) {
       x.last_progress = tnow;
       *busy = true;
     }
-    if (&x == &chn.xfers.front()) rr->st.done.store(x.completed);
-    publish(c, chn, x);
+    publish(c, x);
   }
   // 3. retire completed xfers (their done writes are queued on the device)
   while (!chn.xfers.empty()) {
@@ -993,8 +1030,7 @@ static iccl_result_t progress_channel(iccl_comm* c, Channel& chn, bool* busy) {
     if (!x.fences.empty()) {
       // fences may only be destroyed after the device consumed them; the
       // done flag write follows them on the same stream
-      RankFlags* mine = flags_of(c, c->rank);
-      if (!cyc_geq(mine->done[x.s_slot], x.s_gen)) break;
+      if (!cyc_geq(flags_of(c, x.src_rank)->done[x.s_slot], x.s_gen)) break;
       for (cudaEvent_t fe : x.fences) cudaEventDestroy(fe);
       x.fences.clear();
     }
@@ -1003,11 +1039,11 @@ static iccl_result_t progress_channel(iccl_comm* c, Channel& chn, bool* busy) {
     c->pending_xfers.fetch_sub(1);
     *busy = true;
   }
-  // 4. issue within the window (posted - acked <= window)
+  // 4. re-issue after a path switch (posted - acked <= window); the API
+  // thread issued every chunk of the original attempt itself
   int outstanding = 0;
   for (Xfer& x : chn.xfers) outstanding += x.next_issue - x.completed;
   for (Xfer& x : chn.xfers) {
-    if (x.path != chn.active_path) continue;
     bool stalled = false;
     while (x.next_issue < x.nchunks && outstanding < c->cfg.window) {
       r = issue_chunk(c, chn, x, x.next_issue);
@@ -1019,16 +1055,15 @@ static iccl_result_t progress_channel(iccl_comm* c, Channel& chn, bool* busy) {
       x.next_issue++;
       outstanding++;
       *busy = true;
-      publish(c, chn, x);
+      publish(c, x);
     }
     if (stalled || x.next_issue < x.nchunks) break;
   }
   // 5. watchdog + probe (check_receiver_timeout)
   if (!chn.xfers.empty()) {
     Xfer& x = chn.xfers.front();
-    RankFlags* mine = flags_of(c, c->rank);
-    RankFlags* theirs = flags_of(c, chn.peer);
-    bool elig = cyc_geq(mine->ready[x.s_slot], x.s_gen) && cyc_geq(theirs->ready[x.r_ready_slot], x.r_ready_gen);
+    bool elig = cyc_geq(flags_of(c, x.src_rank)->ready[x.s_slot], x.s_gen) &&
+                cyc_geq(flags_of(c, x.dst_rank)->ready[x.r_ready_slot], x.r_ready_gen);
     if (!elig) {
       x.last_progress = tnow;  // innocent stall upstream: the sender's data is not ready
     } else if (!x.eligible) {
@@ -1038,16 +1073,16 @@ static iccl_result_t progress_channel(iccl_comm* c, Channel& chn, bool* busy) {
     const uint64_t delta = c->cfg.delta_us * 1000ull;
     if (elig && x.completed < x.next_issue && tnow - x.last_progress > delta) {
       if (!chn.probe_out) {
-        r = send_probe(c, chn, chn.active_path);
+        r = send_probe(c, chn, x.path);
         if (r) return r;
-      } else if (chn.probe_path == chn.active_path) {
+      } else if (chn.probe_path == x.path) {
         StreamCtx& ps = c->streams[chn.probe_stream];
         if (cyc_geq(*ps.prog, chn.probe_ticket_expect)) {
           retire_probe(c, chn);  // CTS ok: innocent link
           x.last_progress = tnow;
         } else if (tnow - chn.probe_sent > delta) {
           // CTS failed: trigger the switch
-          r = switch_path(c, chn, chn.active_path ^ 1, 1);
+          r = switch_path(c, chn, x.path ^ 1, 1);
           if (r) return r;
           *busy = true;
         }
@@ -1060,7 +1095,7 @@ static iccl_result_t progress_channel(iccl_comm* c, Channel& chn, bool* busy) {
 // monitor_failed_link: while on the backup, probe the
 // primary every probe period; a probe that completes switches back.
 static iccl_result_t monitor_failed_link(iccl_comm* c, Channel& chn) {
-  if (chn.active_path != 1 || !chn.failed_over) return ICCL_SUCCESS;
+  if (!chn.failed_over || pair_of(c, chn.src, chn.dst).active_path.load() != 1) return ICCL_SUCCESS;
   const uint64_t t = now_ns();
   StreamCtx& ps = c->streams[chn.probe_stream];
   if (chn.probe_out) {
@@ -1089,24 +1124,23 @@ static void proxy_loop(iccl_comm* c) {
     CPU_SET(c->cfg.proxy_cpu, &set);
     pthread_setaffinity_np(pthread_self(), sizeof(set), &set);
   }
-  std::vector<OpDesc> batch;
+  std::vector<Xfer> batch;
   uint64_t idle_since = now_ns();
   while (!c->stop.load(std::memory_order_relaxed)) {
     bool busy = false;
     {
       std::unique_lock<std::mutex> lk(c->qmu);
-      if (c->inbox.empty() && c->pending_xfers.load() == 0 && now_ns() - idle_since > 200000) {
-        // a relay GPU has no pending sends of its own: nap shorter so its
+      if (c->handoff.empty() && c->pending_xfers.load() == 0 && now_ns() - idle_since > 200000) {
+        // a relay GPU has no transfers of its own: nap shorter so its
         // forwarding (hop 2) starts within ~50 us of a request
         c->qcv.wait_for(lk, std::chrono::microseconds(c->relay_buf ? 50 : 500));
       }
-      batch.swap(c->inbox);
+      batch.swap(c->handoff);
     }
-    for (OpDesc& op : batch) {
-      if (op.kind == 0) {
-        c->ch[op.peer].sends.push_back(op);
-        busy = true;
-      }
+    for (Xfer& x : batch) {
+      Channel& chn = c->ch[x.chan];
+      chn.xfers.push_back(std::move(x));
+      busy = true;
     }
     batch.clear();
     if (c->async_err.load() != ICCL_SUCCESS) {
@@ -1114,9 +1148,9 @@ static void proxy_loop(iccl_comm* c) {
       continue;
     }
     fire_time_faults(c);
-    for (int p = 0; p < c->nranks; p++) {
-      Channel& chn = c->ch[p];
-      int req = c->path_req[p].exchange(-1);
+    for (int ci = 0; ci < 2 * c->nranks; ci++) {
+      Channel& chn = c->ch[ci];
+      int req = c->path_req[ci].exchange(-1);
       iccl_result_t r = ICCL_SUCCESS;
       if (req >= 0) r = switch_path(c, chn, req, 0);
       if (!r) r = progress_channel(c, chn, &busy);
@@ -1135,14 +1169,6 @@ static void proxy_loop(iccl_comm* c) {
       set_async(c, ICCL_ERR_TIMEOUT, "LL kernel wait exceeded 10 s (peer never posted the matching op)");
     if (busy) idle_since = now_ns();
   }
-}
-
-static void push_op(iccl_comm* c, const OpDesc& op) {
-  {
-    std::lock_guard<std::mutex> g(c->qmu);
-    c->inbox.push_back(op);
-  }
-  c->qcv.notify_one();
 }
 
 // Reserve the next op slot; a slot is reused only after its previous op completed.
@@ -1169,61 +1195,125 @@ static iccl_result_t next_slot(iccl_comm* c, uint32_t* slot, uint32_t* gen, uint
 
 }  // namespace iccl
 
-// per-comm receiver-side posting counters (kept out of shm: only this rank posts)
-struct RecvCounters {
-  std::vector<uint64_t> posted;
-};
-static std::mutex g_rc_mu;
-static std::unordered_map<iccl_comm*, RecvCounters> g_rc;
-
-static iccl_result_t do_post_cts(iccl_comm* c, int peer, void* buf, size_t bytes, uint32_t slot, uint32_t gen) {
-  CtsRing* ring = ring_of(c, peer, c->rank);
-  uint64_t k;
-  {
-    std::lock_guard<std::mutex> g(g_rc_mu);
-    k = ++g_rc[c].posted[peer];
+// Export the allocation holding `buf` over CUDA IPC (cached by buffer id) so
+// the peer can map it: the zero-copy registration of SPEC.md:126-129.
+static iccl_result_t export_buffer(iccl_comm* c, const void* buf, RzvSide* side) {
+  CUdeviceptr base = 0;
+  size_t asize = 0;
+  ICCL_CHECK_CU(driver()->cuMemGetAddressRange(&base, &asize, (CUdeviceptr)buf));
+  unsigned long long bid = 0;
+  ICCL_CHECK_CU(driver()->cuPointerGetAttribute(&bid, CU_POINTER_ATTRIBUTE_BUFFER_ID, (CUdeviceptr)buf));
+  auto it = c->export_cache.find(bid);
+  if (it == c->export_cache.end()) {
+    cudaIpcMemHandle_t h;
+    cudaError_t err = cudaIpcGetMemHandle(&h, (void*)base);
+    if (err != cudaSuccess) {
+      set_last_error(std::string("cannot export the buffer for zero-copy (") + cudaGetErrorString(err) +
+                     "); allocate it with cudaMalloc / the torch caching allocator without expandable segments");
+      return ICCL_ERR_UNREGISTERED_REGION;
+    }
+    it = c->export_cache.emplace(bid, h).first;
   }
-  // wait for room: the sender's proxy must have consumed posting k - depth
+  side->handle = it->second;
+  side->buffer_id = bid;
+  side->base_offset = (uint64_t)((CUdeviceptr)buf - base);
+  return ICCL_SUCCESS;
+}
+
+// Rendezvous of the k-th op of an ordered pair (SPEC.md:194's RTS / CTS):
+// post my half, then arbitrate.  The side that arrives second has both
+// halves and issues every chunk of the transfer right here, from the API
+// thread — a push by the sender or a pull by the receiver — behind stream
+// waits on both user streams' ready flags; the first side's stream is
+// released by the done flag the issuer's copy stream writes.  The proxy then
+// only tracks the transfer.  Returns with nothing issued if I came first.
+static iccl_result_t rzv_post(iccl_comm* c, const OpDesc& op) {
+  const int peer = op.peer, kind = op.kind;
+  const int src = kind == 0 ? c->rank : peer, dst = kind == 0 ? peer : c->rank;
+  const uint64_t k = kind == 0 ? c->pair_sends[peer]++ : c->pair_recvs[peer]++;
+  RzvEntry& e = ring_of(c, src, dst)->e[k % kRzvDepth];
+  const uint64_t g = k / kRzvDepth;
+  // the entry is reused once both sides arrived for its previous generation
   uint64_t t0 = now_ns();
-  while (k > (uint64_t)kCtsDepth && ring->st.consumed.load(std::memory_order_acquire) + kCtsDepth < k) {
+  while (e.arrivals.load(std::memory_order_acquire) < 2 * g) {
     if (c->async_err.load() != ICCL_SUCCESS) return (iccl_result_t)c->async_err.load();
+    if (c->hdr->abort.load()) return ICCL_ERR_ABORTED;
     if (now_ns() - t0 > 60ull * 1000000000ull) {
-      set_last_error("CTS ring full for 60 s");
+      set_last_error("more than 1024 unmatched ops on a pair for 60 s");
       return ICCL_ERR_TIMEOUT;
     }
     sched_yield();
   }
-  CtsEntry& e = ring->e[(k - 1) % kCtsDepth];
-  e.bytes = bytes;
-  e.ready_slot = slot;
-  e.ready_gen = gen;
-  e.done_slot = slot;
-  e.done_gen = gen;
-  e.direct_ptr = (uint64_t)(uintptr_t)buf;
-  e.buffer_id = 0;
-  e.base_offset = 0;
+  RzvSide& mine = e.side[kind];
+  mine.bytes = op.bytes;
+  mine.slot = op.slot;
+  mine.gen = op.gen;
+  mine.direct_ptr = (uint64_t)(uintptr_t)op.src;
+  mine.buffer_id = 0;
+  mine.base_offset = 0;
   if (peer != c->rank) {
-    CUdeviceptr base = 0;
-    size_t asize = 0;
-    ICCL_CHECK_CU(driver()->cuMemGetAddressRange(&base, &asize, (CUdeviceptr)buf));
-    unsigned long long bid = 0;
-    ICCL_CHECK_CU(driver()->cuPointerGetAttribute(&bid, CU_POINTER_ATTRIBUTE_BUFFER_ID, (CUdeviceptr)buf));
-    auto it = c->export_cache.find(bid);
-    if (it == c->export_cache.end()) {
-      cudaIpcMemHandle_t h;
-      cudaError_t err = cudaIpcGetMemHandle(&h, (void*)base);
-      if (err != cudaSuccess) {
-        set_last_error(std::string("cannot export recv buffer for zero-copy (") + cudaGetErrorString(err) +
-                       "); allocate it with cudaMalloc / the torch caching allocator without expandable segments");
-        return ICCL_ERR_UNREGISTERED_REGION;
-      }
-      it = c->export_cache.emplace(bid, h).first;
-    }
-    e.handle = it->second;
-    e.buffer_id = bid;
-    e.base_offset = (uint64_t)((CUdeviceptr)buf - base);
+    iccl_result_t r = export_buffer(c, op.src, &mine);
+    if (r) return r;
   }
-  e.seq.store(k, std::memory_order_release);
+  const uint64_t prev = e.arrivals.fetch_add(1, std::memory_order_acq_rel);
+  if (prev != 2 * g + 1) return ICCL_SUCCESS;  // first: the peer issues when it arrives
+  const RzvSide& snd = e.side[0];
+  const RzvSide& rcv = e.side[1];
+  if (snd.bytes != rcv.bytes) {
+    // release both streams so nothing hangs, and report the mismatch
+    __atomic_store_n(&flags_of(c, src)->done[snd.slot], snd.gen, __ATOMIC_SEQ_CST);
+    __atomic_store_n(&flags_of(c, dst)->done[rcv.slot], rcv.gen, __ATOMIC_SEQ_CST);
+    std::string msg = "send of " + std::to_string(snd.bytes) + " B from rank " + std::to_string(src) +
+                      " matched a recv of " + std::to_string(rcv.bytes) + " B on rank " + std::to_string(dst);
+    set_async(c, ICCL_ERR_SIZE_MISMATCH, msg);
+    set_last_error(msg);
+    return ICCL_ERR_SIZE_MISMATCH;
+  }
+  const int ci = 2 * peer + kind;
+  Channel& chn = c->ch[ci];
+  Xfer x;
+  x.op_seq = op.op_seq;
+  x.pair_seq = k;
+  x.src_rank = src;
+  x.dst_rank = dst;
+  x.chan = ci;
+  char* other = nullptr;
+  iccl_result_t r = open_peer_buffer(c, chn, e.side[kind ^ 1], &other);
+  if (r) return r;
+  x.src = kind == 0 ? op.src : other;
+  x.dst = kind == 0 ? other : (char*)op.src;
+  x.bytes = op.bytes;
+  x.s_slot = snd.slot;
+  x.s_gen = snd.gen;
+  x.r_ready_slot = x.r_done_slot = rcv.slot;
+  x.r_ready_gen = x.r_done_gen = rcv.gen;
+  x.dst_buffer_id = rcv.buffer_id;
+  x.dst_base_offset = rcv.base_offset;
+  x.dst_handle = rcv.handle;
+  x.chunk = (size_t)c->cfg.chunk_bytes;
+  x.nchunks = (int)((x.bytes + x.chunk - 1) / x.chunk);
+  x.rec.resize(x.nchunks);
+  x.path = pair_of(c, src, dst).active_path.load();
+  x.last_progress = now_ns();
+  {
+    std::lock_guard<std::mutex> gl(c->fault_mu);
+    x.fault_ops_index = (int)(k - chn.fault_seq_base);
+  }
+  ICCL_TRACE("issue %s of op %llu: pair %d->%d #%llu, %zu B, %d chunk(s), path %d", kind == 0 ? "push" : "pull",
+             (unsigned long long)op.op_seq, src, dst, (unsigned long long)k, x.bytes, x.nchunks, x.path);
+  while (x.next_issue < x.nchunks) {
+    r = issue_chunk(c, chn, x, x.next_issue);
+    if (r == ICCL_ERR_IN_PROGRESS) break;  // relay ring full: the proxy issues the rest
+    if (r) return r;
+    x.next_issue++;
+  }
+  publish(c, x);
+  c->pending_xfers.fetch_add(1);
+  {
+    std::lock_guard<std::mutex> gl(c->qmu);
+    c->handoff.push_back(std::move(x));
+  }
+  c->qcv.notify_one();
   return ICCL_SUCCESS;
 }
 
@@ -1340,8 +1430,8 @@ static iccl_result_t enqueue_op(iccl_comm* c, int kind, const void* buf, size_t 
           bytes <= kLLMaxBytes && c->ll_region != nullptr;
   if (op.ll) {
     op.ll_seq = kind == 0 ? ++c->ll_sent[peer] : ++c->ll_recvd[peer];
-  } else if (kind == 1) {
-    r = do_post_cts(c, peer, (void*)buf, bytes, op.slot, op.gen);
+  } else {
+    r = rzv_post(c, op);
     if (r) return r;
   }
   c->ranks[c->rank].op_count.fetch_add(1, std::memory_order_relaxed);
@@ -1351,13 +1441,7 @@ static iccl_result_t enqueue_op(iccl_comm* c, int kind, const void* buf, size_t 
     return ICCL_SUCCESS;
   }
   if (op.ll) return launch_ll_ops(c, s, {op});
-  r = stream_markers(c, s, {op});
-  if (r) return r;
-  if (kind == 0) {
-    c->pending_xfers.fetch_add(1);
-    push_op(c, op);
-  }
-  return ICCL_SUCCESS;
+  return stream_markers(c, s, {op});
 }
 
 extern "C" {
@@ -1404,14 +1488,10 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
   c->cfg = conf;
   c->monitor_enabled.store(conf.monitor_enabled);
   c->shm_name = b.shm_name;
-  for (int i = 0; i < kMaxRanks; i++) {
-    c->path_req[i].store(-1);
-    c->active_path_pub[i].store(0);
-  }
-  {
-    std::lock_guard<std::mutex> g(g_rc_mu);
-    g_rc[c].posted.assign(nranks, 0);
-  }
+  for (int i = 0; i < 2 * kMaxRanks; i++) c->path_req[i].store(-1);
+  c->pair_sends.assign(nranks, 0);
+  c->pair_recvs.assign(nranks, 0);
+  c->peer_ipc.resize(nranks);
   ShmLayout L(nranks);
   int fd = shm_open(b.shm_name, O_CREAT | O_RDWR, 0600);
   if (fd < 0) {
@@ -1437,7 +1517,7 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
   c->hdr = (ShmHeader*)m;
   c->ranks = (RankInfo*)((char*)m + L.off_ranks);
   c->flags = (RankFlags*)((char*)m + L.off_flags);
-  c->rings = (CtsRing*)((char*)m + L.off_rings);
+  c->rings = (RzvRing*)((char*)m + L.off_rings);
   // device-visible control block: every rank's copy streams write flags here
   ICCL_CHECK_CUDA(cudaHostRegister(m, L.total, cudaHostRegisterMapped | cudaHostRegisterPortable));
   c->pinned_bytes = 64 * 1024 + sizeof(KernelStamp) * kStampSlots + kGateWords * 4;
@@ -1496,10 +1576,11 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
   if (r) return r;
   if (rank == 0) shm_unlink(b.shm_name);
 
-  // streams: per peer S copy-engine streams + 1 SM stream + 1 probe stream
+  // streams: per channel (peer x {push, pull}) S copy-engine streams + 1 SM
+  // stream + 1 probe stream (+ 1 relay stream for a push channel)
   int prio_lo, prio_hi;
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-  c->ch.resize(nranks);
+  c->ch.resize(2 * nranks);
   uint32_t* prog = c->pinned;  // first 32 KB of pinned: progress words
   int next_prog = 0;
   auto mk_stream = [&](int engine) -> int {
@@ -1511,9 +1592,28 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
     c->streams.push_back(sc);
     return (int)c->streams.size() - 1;
   };
+  std::vector<char*> peer_scratch(nranks, nullptr);
   for (int p = 0; p < nranks; p++) {
-    Channel& chn = c->ch[p];
+    if (p == rank) {
+      peer_scratch[p] = c->scratch + 2048;
+    } else {
+      void* ps = nullptr;
+      ICCL_CHECK_CUDA(cudaIpcOpenMemHandle(&ps, c->ranks[p].scratch_handle, cudaIpcMemLazyEnablePeerAccess));
+      c->peer_scratch_base.push_back((char*)ps);
+      peer_scratch[p] = (char*)ps + 16 * (1 + rank);
+      void* pl = nullptr;
+      ICCL_CHECK_CUDA(cudaIpcOpenMemHandle(&pl, c->ranks[p].ll_handle, cudaIpcMemLazyEnablePeerAccess));
+      c->peer_ll[p] = (char*)pl;
+    }
+  }
+  for (int ci = 0; ci < 2 * nranks; ci++) {
+    const int p = ci / 2;
+    Channel& chn = c->ch[ci];
     chn.peer = p;
+    chn.dir = ci % 2;
+    chn.src = chn.dir == 0 ? rank : p;
+    chn.dst = chn.dir == 0 ? p : rank;
+    chn.peer_scratch = peer_scratch[p];
     for (int s = 0; s < conf.streams_per_peer; s++) {
       int si = mk_stream(ENG_CE);
       chn.path_streams[0].push_back(si);
@@ -1522,7 +1622,7 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
     int sm = mk_stream(ENG_SM);
     chn.path_streams[0].push_back(sm);
     chn.path_streams[1].push_back(sm);
-    if (c->relay_buf && p != rank) {
+    if (c->relay_buf && p != rank && chn.dir == 0) {
       for (int q = 0; q < nranks; q++)
         if (q != rank && q != p) {
           chn.relay_rank = q;  // lowest-index GPU that is not an endpoint
@@ -1531,16 +1631,6 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
       chn.path_streams[1].push_back(mk_stream(ENG_RELAY));
     }
     chn.probe_stream = mk_stream(ENG_CE);
-    if (p == rank) {
-      chn.peer_scratch = c->scratch + 2048;
-    } else {
-      void* ps = nullptr;
-      ICCL_CHECK_CUDA(cudaIpcOpenMemHandle(&ps, c->ranks[p].scratch_handle, cudaIpcMemLazyEnablePeerAccess));
-      chn.peer_scratch = (char*)ps + 16 * (1 + rank);
-      void* pl = nullptr;
-      ICCL_CHECK_CUDA(cudaIpcOpenMemHandle(&pl, c->ranks[p].ll_handle, cudaIpcMemLazyEnablePeerAccess));
-      c->peer_ll[p] = (char*)pl;
-    }
   }
   if (c->relay_buf) {
     c->relay_serve.assign(nranks, -1);
@@ -1584,15 +1674,13 @@ static void teardown(iccl_comm* c) {
     if (sc.ev) cudaEventDestroy(sc.ev);
   }
   for (cudaEvent_t e : c->all_events) cudaEventDestroy(e);
-  for (auto& chn : c->ch) {
-    for (auto& kv : chn.ipc) cudaIpcCloseMemHandle(kv.second);
-    if (chn.peer != c->rank && chn.peer_scratch) cudaIpcCloseMemHandle(chn.peer_scratch - 16 * (1 + c->rank));
-  }
+  for (auto& cache : c->peer_ipc)
+    for (auto& kv : cache) cudaIpcCloseMemHandle(kv.second);
+  for (char* p : c->peer_scratch_base) cudaIpcCloseMemHandle(p);
   for (size_t p = 0; p < c->peer_ll.size(); p++)
     if (c->peer_ll[p] && (int)p != c->rank) cudaIpcCloseMemHandle(c->peer_ll[p]);
   for (char* p : c->peer_relay)
     if (p) cudaIpcCloseMemHandle(p);
-  for (auto& kv : c->relay_ipc) cudaIpcCloseMemHandle(kv.second);
   if (c->relay_buf) cudaFree(c->relay_buf);
   if (c->ll_region) cudaFree(c->ll_region);
   if (c->ll_counters) cudaFree(c->ll_counters);
@@ -1602,10 +1690,6 @@ static void teardown(iccl_comm* c) {
     munmap(c->shm, c->shm_bytes);
   }
   if (c->pinned) cudaFreeHost(c->pinned);
-  {
-    std::lock_guard<std::mutex> g(g_rc_mu);
-    g_rc.erase(c);
-  }
 }
 
 iccl_result_t iccl_comm_destroy(iccl_comm_t c) {
@@ -1743,15 +1827,6 @@ iccl_result_t iccl_group_end(iccl_comm_t c) {
     if (!r && !ce.empty()) r = stream_markers(c, s, ce, 2);  // done waits
     if (r) return r;
   }
-  {
-    std::lock_guard<std::mutex> g(c->qmu);
-    for (auto& p : ops)
-      if (p.first.kind == 0 && !p.first.ll) {
-        c->pending_xfers.fetch_add(1);
-        c->inbox.push_back(p.first);
-      }
-  }
-  c->qcv.notify_one();
   return ICCL_SUCCESS;
 }
 
@@ -1839,16 +1914,21 @@ iccl_result_t iccl_req_state(iccl_comm_t c, iccl_req_t req, iccl_xfer_state_t* s
   return ICCL_SUCCESS;
 }
 
+// The directed path rank -> peer is switched for whichever side issues its
+// next transfer (the pair's shared state); transfers this rank has in flight
+// on the pair move at the receiver's breakpoint (switch_qp).
 iccl_result_t iccl_path_switch(iccl_comm_t c, int peer, int to) {
   if (!c || peer < 0 || peer >= c->nranks || (to != 0 && to != 1)) return ICCL_ERR_INVALID_ARGUMENT;
-  c->path_req[peer].store(to);
+  pair_of(c, c->rank, peer).active_path.store(to);
+  c->path_req[2 * peer + 0].store(to);
+  if (peer == c->rank) c->path_req[2 * peer + 1].store(to);  // a self pair is also issued by its pull side
   c->qcv.notify_one();
   return ICCL_SUCCESS;
 }
 
 iccl_result_t iccl_path_active(iccl_comm_t c, int peer, int* path) {
   if (!c || !path || peer < 0 || peer >= c->nranks) return ICCL_ERR_INVALID_ARGUMENT;
-  *path = c->active_path_pub[peer].load();
+  *path = pair_of(c, c->rank, peer).active_path.load();
   return ICCL_SUCCESS;
 }
 
@@ -1862,7 +1942,7 @@ iccl_result_t iccl_fault_set(iccl_comm_t c, const iccl_fault_t* f, int n) {
     c->faults.push_back(Fault{f[i], false});
   }
   c->faults_t0 = now_ns();
-  for (auto& chn : c->ch) chn.sends_seen = 0;
+  for (auto& chn : c->ch) chn.fault_seq_base = chn.dir == 0 ? c->pair_sends[chn.peer] : c->pair_recvs[chn.peer];
   return ICCL_SUCCESS;
 }
 

@@ -207,6 +207,27 @@ int main(int argc, char** argv) {
       }
     }
   }
+  SECTION("5. 16 x 8 MiB peer copies on one stream: bare / untimed event / timed event between copies (us per copy)");
+  {
+    char *y0, *y1; CK(cudaSetDevice(0)); CK(cudaMalloc(&y0, 128 << 20)); CK(cudaSetDevice(1)); CK(cudaMalloc(&y1, 128 << 20)); CK(cudaSetDevice(0));
+    cudaEvent_t ut[16], tt[16];
+    for (int i = 0; i < 16; i++) { CK(cudaEventCreateWithFlags(&ut[i], cudaEventDisableTiming)); CK(cudaEventCreate(&tt[i])); }
+    for (int mode = 0; mode < 3; mode++) {
+      std::vector<double> v;
+      for (int rep = 0; rep < 10; rep++) {
+        CK(cudaEventRecord(a, s0));
+        for (int k = 0; k < 16; k++) {
+          CK(cudaMemcpyAsync(y1 + ((size_t)k << 23), y0 + ((size_t)k << 23), 8 << 20, cudaMemcpyDefault, s0));
+          if (mode == 1) CK(cudaEventRecord(ut[k], s0));
+          if (mode == 2) CK(cudaEventRecord(tt[k], s0));
+        }
+        CK(cudaEventRecord(b, s0)); CK(cudaEventSynchronize(b));
+        float ms; CK(cudaEventElapsedTime(&ms, a, b)); if (rep > 1) v.push_back(ms * 1e3 / 16);
+      }
+      std::sort(v.begin(), v.end());
+      printf("  mode %d: %.2f us per 8 MiB copy (%.1f GB/s)\n", mode, v[v.size() / 2], (8 << 20) / v[v.size() / 2] / 1e3); fflush(stdout);
+    }
+  }
   SECTION("done");
   return 0;
 }
