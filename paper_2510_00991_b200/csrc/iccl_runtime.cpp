@@ -79,6 +79,7 @@ constexpr int kMaxRanks = 64;
 constexpr int kGateWords = 1024;
 constexpr int kStampSlots = 4096;
 constexpr size_t kScratchBytes = 4096;
+constexpr int kProxyNapUs = 20;  // proxy back-off when a pass moved nothing
 
 // ---------------------------------------------------------------- shared control block
 struct alignas(64) ShmHeader {
@@ -133,10 +134,11 @@ struct RzvSide {
 };
 
 // Rendezvous of the k-th send and the k-th recv of an ordered pair: each side
-// writes its half, then bumps `arrivals`; the side that sees 2g+1 (g = k /
-// depth) arrived second and issues the transfer.
+// writes its half, then bumps `arrivals` (the side that sees 2g+1, g = k /
+// depth, arrived second); the transfer is issued by whoever wins `claimed`.
 struct alignas(64) RzvEntry {
   std::atomic<uint64_t> arrivals;
+  std::atomic<uint64_t> claimed;  // generations whose transfer has an issuer (CAS g -> g + 1)
   RzvSide side[2];  // 0 sender, 1 receiver
 };
 
@@ -312,6 +314,19 @@ struct Fault {
   bool fired = false;
 };
 
+// A rendezvous this rank's proxy must finish: kind 0 = my send arrived first,
+// push once the receiver's CTS is posted; kind 1 = my recv arrived second
+// after the sender's RTS — the sender's proxy pushes, and this is the rescue:
+// pull if nobody claimed the transfer by `deadline` (the sender's process may
+// be stuck in a synchronous CUDA call, see rzv_post).
+struct RzvWatch {
+  int kind = 0;
+  int peer = -1;
+  uint64_t k = 0;
+  uint64_t op_seq = 0;
+  uint64_t deadline = 0;
+};
+
 }  // namespace iccl
 
 using namespace iccl;
@@ -368,6 +383,8 @@ struct iccl_comm {
   std::mutex qmu;
   std::condition_variable qcv;
   std::vector<Xfer> handoff;  // issued by the API thread, tracked by the proxy
+  std::vector<RzvWatch> watch_in;  // new rendezvous watches from the API thread (under qmu)
+  std::vector<RzvWatch> watches;   // proxy-owned
   std::mutex mon_mu;
   std::deque<iccl_mon_rec_t> mon;
   std::deque<iccl_switch_event_t> sw_events;
@@ -1116,6 +1133,10 @@ static iccl_result_t monitor_failed_link(iccl_comm* c, Channel& chn) {
   return ICCL_SUCCESS;
 }
 
+}  // namespace iccl
+static iccl_result_t progress_watches(iccl_comm* c, bool* busy);  // defined with the rendezvous below
+namespace iccl {
+
 static void proxy_loop(iccl_comm* c) {
   cudaSetDevice(c->dev);
   if (c->cfg.proxy_cpu >= 0) {
@@ -1136,6 +1157,8 @@ static void proxy_loop(iccl_comm* c) {
         c->qcv.wait_for(lk, std::chrono::microseconds(c->relay_buf ? 50 : 500));
       }
       batch.swap(c->handoff);
+      c->watches.insert(c->watches.end(), c->watch_in.begin(), c->watch_in.end());
+      c->watch_in.clear();
     }
     for (Xfer& x : batch) {
       Channel& chn = c->ch[x.chan];
@@ -1148,6 +1171,13 @@ static void proxy_loop(iccl_comm* c) {
       continue;
     }
     fire_time_faults(c);
+    if (!c->watches.empty()) {
+      iccl_result_t r = progress_watches(c, &busy);
+      if (r) {
+        set_async(c, r, std::string("proxy: ") + last_error());
+        continue;
+      }
+    }
     for (int ci = 0; ci < 2 * c->nranks; ci++) {
       Channel& chn = c->ch[ci];
       int req = c->path_req[ci].exchange(-1);
@@ -1167,7 +1197,15 @@ static void proxy_loop(iccl_comm* c) {
     if (c->hdr->abort.load()) set_async(c, ICCL_ERR_ABORTED, "communicator aborted");
     if (c->ll_error && __atomic_load_n(c->ll_error, __ATOMIC_ACQUIRE))
       set_async(c, ICCL_ERR_TIMEOUT, "LL kernel wait exceeded 10 s (peer never posted the matching op)");
-    if (busy) idle_since = now_ns();
+    if (busy) {
+      idle_since = now_ns();
+    } else {
+      // Nothing moved: back off before the next pass.  Every cudaEventQuery
+      // takes the context lock the API thread needs to enqueue transfers, so
+      // a spinning proxy would slow the issuing thread down; completion is
+      // not latency-critical here (the device writes the done flags itself).
+      std::this_thread::sleep_for(std::chrono::microseconds(kProxyNapUs));
+    }
   }
 }
 
@@ -1220,22 +1258,124 @@ static iccl_result_t export_buffer(iccl_comm* c, const void* buf, RzvSide* side)
   return ICCL_SUCCESS;
 }
 
-// Rendezvous of the k-th op of an ordered pair (SPEC.md:194's RTS / CTS):
-// post my half, then arbitrate.  The side that arrives second has both
-// halves and issues every chunk of the transfer right here, from the API
-// thread — a push by the sender or a pull by the receiver — behind stream
-// waits on both user streams' ready flags; the first side's stream is
-// released by the done flag the issuer's copy stream writes.  The proxy then
-// only tracks the transfer.  Returns with nothing issued if I came first.
+static RzvEntry& rzv_entry(iccl_comm* c, int kind, int peer, uint64_t k) {
+  const int src = kind == 0 ? c->rank : peer, dst = kind == 0 ? peer : c->rank;
+  return ring_of(c, src, dst)->e[k % kRzvDepth];
+}
+
+static bool rzv_claim(RzvEntry& e, uint64_t k) {
+  uint64_t g = k / kRzvDepth;
+  return e.claimed.compare_exchange_strong(g, g + 1, std::memory_order_acq_rel);
+}
+
+// Issue the whole transfer of rendezvous entry k of the pair (as `kind`: 0 =
+// push by the sender, 1 = pull by the receiver) after winning its claim:
+// every chunk goes to the channel's copy stream behind waits on both user
+// streams' ready flags, the last one writes both done flags.  From the API
+// thread the transfer is handed to the proxy; from the proxy it is tracked
+// in place.
+static iccl_result_t rzv_issue(iccl_comm* c, int kind, int peer, uint64_t k, uint64_t op_seq, bool on_proxy) {
+  RzvEntry& e = rzv_entry(c, kind, peer, k);
+  const int src = kind == 0 ? c->rank : peer, dst = kind == 0 ? peer : c->rank;
+  const RzvSide& snd = e.side[0];
+  const RzvSide& rcv = e.side[1];
+  if (snd.bytes != rcv.bytes) {
+    // release both streams so nothing hangs, and report the mismatch
+    __atomic_store_n(&flags_of(c, src)->done[snd.slot], snd.gen, __ATOMIC_SEQ_CST);
+    __atomic_store_n(&flags_of(c, dst)->done[rcv.slot], rcv.gen, __ATOMIC_SEQ_CST);
+    std::string msg = "send of " + std::to_string(snd.bytes) + " B from rank " + std::to_string(src) +
+                      " matched a recv of " + std::to_string(rcv.bytes) + " B on rank " + std::to_string(dst);
+    set_async(c, ICCL_ERR_SIZE_MISMATCH, msg);
+    set_last_error(msg);
+    return ICCL_ERR_SIZE_MISMATCH;
+  }
+  const int ci = 2 * peer + kind;
+  Channel& chn = c->ch[ci];
+  Xfer x;
+  x.op_seq = op_seq;
+  x.pair_seq = k;
+  x.src_rank = src;
+  x.dst_rank = dst;
+  x.chan = ci;
+  char* other = nullptr;
+  iccl_result_t r = open_peer_buffer(c, chn, e.side[kind ^ 1], &other);
+  if (r) return r;
+  char* own = (char*)(uintptr_t)e.side[kind].direct_ptr;
+  x.src = kind == 0 ? own : other;
+  x.dst = kind == 0 ? other : own;
+  x.bytes = snd.bytes;
+  x.s_slot = snd.slot;
+  x.s_gen = snd.gen;
+  x.r_ready_slot = x.r_done_slot = rcv.slot;
+  x.r_ready_gen = x.r_done_gen = rcv.gen;
+  x.dst_buffer_id = rcv.buffer_id;
+  x.dst_base_offset = rcv.base_offset;
+  x.dst_handle = rcv.handle;
+  x.chunk = (size_t)c->cfg.chunk_bytes;
+  x.nchunks = (int)((x.bytes + x.chunk - 1) / x.chunk);
+  x.rec.resize(x.nchunks);
+  x.path = pair_of(c, src, dst).active_path.load();
+  x.last_progress = now_ns();
+  {
+    std::lock_guard<std::mutex> gl(c->fault_mu);
+    x.fault_ops_index = (int)(k - chn.fault_seq_base);
+  }
+  ICCL_TRACE("issue %s (%s) pair %d->%d #%llu, %zu B, %d chunk(s), path %d", kind == 0 ? "push" : "pull",
+             on_proxy ? "proxy" : "api", src, dst, (unsigned long long)k, x.bytes, x.nchunks, x.path);
+  while (x.next_issue < x.nchunks) {
+    r = issue_chunk(c, chn, x, x.next_issue);
+    if (r == ICCL_ERR_IN_PROGRESS) break;  // relay ring full: the proxy issues the rest
+    if (r) return r;
+    x.next_issue++;
+  }
+  publish(c, x);
+  c->pending_xfers.fetch_add(1);
+  if (on_proxy) {
+    chn.xfers.push_back(std::move(x));
+    return ICCL_SUCCESS;
+  }
+  {
+    std::lock_guard<std::mutex> gl(c->qmu);
+    c->handoff.push_back(std::move(x));
+  }
+  c->qcv.notify_one();
+  return ICCL_SUCCESS;
+}
+
+static void add_watch(iccl_comm* c, const RzvWatch& w) {
+  c->pending_xfers.fetch_add(1);  // destroy waits until the watch is resolved
+  {
+    std::lock_guard<std::mutex> g(c->qmu);
+    c->watch_in.push_back(w);
+  }
+  c->qcv.notify_one();
+}
+
+// Rendezvous of the k-th op of an ordered pair (SPEC.md:194's RTS / CTS): post
+// my half (IPC handle, offset, op slot), then decide who issues.
+//
+// The sender issues (a push by its copy engine): pushes in both directions
+// run at full NVLink rate, two opposite pulls do not (half rate measured,
+// scripts/diag_ring.py).  A sender that arrives second has both halves and
+// issues right here, from its API call.  A sender that arrives first leaves
+// a watch to its proxy, which pushes once the receiver's CTS is posted.
+//
+// The receiver's rescue: while any thread of a process sits in a
+// synchronous CUDA call on a stream parked behind one of our ops (a pageable
+// cudaMemcpy, .cpu()), every other CUDA call of that process blocks —
+// memcpy, kernel launch, stream memop, event record alike
+// (probes/p2p_probe6.cu) — so a sender's proxy can be stuck.  A receiver
+// that arrives second therefore also leaves a watch: if nobody claimed the
+// transfer after delta_us, its proxy claims it and pulls.  Exactly one side
+// wins `claimed`.  A self pair issues from the second API call.
 static iccl_result_t rzv_post(iccl_comm* c, const OpDesc& op) {
   const int peer = op.peer, kind = op.kind;
-  const int src = kind == 0 ? c->rank : peer, dst = kind == 0 ? peer : c->rank;
   const uint64_t k = kind == 0 ? c->pair_sends[peer]++ : c->pair_recvs[peer]++;
-  RzvEntry& e = ring_of(c, src, dst)->e[k % kRzvDepth];
+  RzvEntry& e = rzv_entry(c, kind, peer, k);
   const uint64_t g = k / kRzvDepth;
-  // the entry is reused once both sides arrived for its previous generation
+  // the entry is reused once both sides arrived and a side claimed its previous generation
   uint64_t t0 = now_ns();
-  while (e.arrivals.load(std::memory_order_acquire) < 2 * g) {
+  while (e.arrivals.load(std::memory_order_acquire) < 2 * g || e.claimed.load(std::memory_order_acquire) < g) {
     if (c->async_err.load() != ICCL_SUCCESS) return (iccl_result_t)c->async_err.load();
     if (c->hdr->abort.load()) return ICCL_ERR_ABORTED;
     if (now_ns() - t0 > 60ull * 1000000000ull) {
@@ -1255,65 +1395,47 @@ static iccl_result_t rzv_post(iccl_comm* c, const OpDesc& op) {
     iccl_result_t r = export_buffer(c, op.src, &mine);
     if (r) return r;
   }
-  const uint64_t prev = e.arrivals.fetch_add(1, std::memory_order_acq_rel);
-  if (prev != 2 * g + 1) return ICCL_SUCCESS;  // first: the peer issues when it arrives
-  const RzvSide& snd = e.side[0];
-  const RzvSide& rcv = e.side[1];
-  if (snd.bytes != rcv.bytes) {
-    // release both streams so nothing hangs, and report the mismatch
-    __atomic_store_n(&flags_of(c, src)->done[snd.slot], snd.gen, __ATOMIC_SEQ_CST);
-    __atomic_store_n(&flags_of(c, dst)->done[rcv.slot], rcv.gen, __ATOMIC_SEQ_CST);
-    std::string msg = "send of " + std::to_string(snd.bytes) + " B from rank " + std::to_string(src) +
-                      " matched a recv of " + std::to_string(rcv.bytes) + " B on rank " + std::to_string(dst);
-    set_async(c, ICCL_ERR_SIZE_MISMATCH, msg);
-    set_last_error(msg);
-    return ICCL_ERR_SIZE_MISMATCH;
+  const bool second = e.arrivals.fetch_add(1, std::memory_order_acq_rel) == 2 * g + 1;
+  if (second && (kind == 0 || peer == c->rank)) {
+    if (!rzv_claim(e, k)) return ICCL_SUCCESS;  // (cannot happen: the first side never claims)
+    return rzv_issue(c, kind, peer, k, op.op_seq, false);
   }
-  const int ci = 2 * peer + kind;
-  Channel& chn = c->ch[ci];
-  Xfer x;
-  x.op_seq = op.op_seq;
-  x.pair_seq = k;
-  x.src_rank = src;
-  x.dst_rank = dst;
-  x.chan = ci;
-  char* other = nullptr;
-  iccl_result_t r = open_peer_buffer(c, chn, e.side[kind ^ 1], &other);
-  if (r) return r;
-  x.src = kind == 0 ? op.src : other;
-  x.dst = kind == 0 ? other : (char*)op.src;
-  x.bytes = op.bytes;
-  x.s_slot = snd.slot;
-  x.s_gen = snd.gen;
-  x.r_ready_slot = x.r_done_slot = rcv.slot;
-  x.r_ready_gen = x.r_done_gen = rcv.gen;
-  x.dst_buffer_id = rcv.buffer_id;
-  x.dst_base_offset = rcv.base_offset;
-  x.dst_handle = rcv.handle;
-  x.chunk = (size_t)c->cfg.chunk_bytes;
-  x.nchunks = (int)((x.bytes + x.chunk - 1) / x.chunk);
-  x.rec.resize(x.nchunks);
-  x.path = pair_of(c, src, dst).active_path.load();
-  x.last_progress = now_ns();
-  {
-    std::lock_guard<std::mutex> gl(c->fault_mu);
-    x.fault_ops_index = (int)(k - chn.fault_seq_base);
+  if (kind == 0) {
+    add_watch(c, RzvWatch{0, peer, k, op.op_seq, 0});
+  } else if (second) {
+    add_watch(c, RzvWatch{1, peer, k, op.op_seq, now_ns() + c->cfg.delta_us * 1000ull});
   }
-  ICCL_TRACE("issue %s of op %llu: pair %d->%d #%llu, %zu B, %d chunk(s), path %d", kind == 0 ? "push" : "pull",
-             (unsigned long long)op.op_seq, src, dst, (unsigned long long)k, x.bytes, x.nchunks, x.path);
-  while (x.next_issue < x.nchunks) {
-    r = issue_chunk(c, chn, x, x.next_issue);
-    if (r == ICCL_ERR_IN_PROGRESS) break;  // relay ring full: the proxy issues the rest
-    if (r) return r;
-    x.next_issue++;
+  return ICCL_SUCCESS;
+}
+
+// Proxy side of the watches: push when the CTS arrived (and we win the
+// claim); rescue-pull after the deadline if the sender never claimed.
+static iccl_result_t progress_watches(iccl_comm* c, bool* busy) {
+  const uint64_t t = now_ns();
+  size_t keep = 0;
+  for (size_t i = 0; i < c->watches.size(); i++) {
+    RzvWatch w = c->watches[i];
+    RzvEntry& e = rzv_entry(c, w.kind, w.peer, w.k);
+    const uint64_t g = w.k / kRzvDepth;
+    bool resolved = false;
+    if (e.claimed.load(std::memory_order_acquire) > g) {
+      resolved = true;  // the other side issued it
+    } else if (w.kind == 0 ? e.arrivals.load(std::memory_order_acquire) >= 2 * g + 2 : t > w.deadline) {
+      resolved = true;
+      if (rzv_claim(e, w.k)) {
+        iccl_result_t r = rzv_issue(c, w.kind, w.peer, w.k, w.op_seq, true);
+        if (r) return r;
+        if (w.kind == 1) ICCL_TRACE("rescue pull of pair %d->%d #%llu", w.peer, c->rank, (unsigned long long)w.k);
+      }
+    }
+    if (resolved) {
+      c->pending_xfers.fetch_sub(1);
+      *busy = true;
+    } else {
+      c->watches[keep++] = w;
+    }
   }
-  publish(c, x);
-  c->pending_xfers.fetch_add(1);
-  {
-    std::lock_guard<std::mutex> gl(c->qmu);
-    c->handoff.push_back(std::move(x));
-  }
-  c->qcv.notify_one();
+  c->watches.resize(keep);
   return ICCL_SUCCESS;
 }
 
