@@ -80,6 +80,10 @@ constexpr int kGateWords = 1024;
 constexpr int kStampSlots = 4096;
 constexpr size_t kScratchBytes = 4096;
 constexpr int kProxyNapUs = 20;  // proxy back-off when a pass moved nothing
+// How long a send waits for its receiver's half before posting its own (so
+// that it arrives second and pushes, see rzv_post): single ops / a group.
+constexpr uint64_t kSendWaitUs = 50;
+constexpr uint64_t kGroupSendWaitUs = 2000;
 
 // ---------------------------------------------------------------- shared control block
 struct alignas(64) ShmHeader {
@@ -314,19 +318,6 @@ struct Fault {
   bool fired = false;
 };
 
-// A rendezvous this rank's proxy must finish: kind 0 = my send arrived first,
-// push once the receiver's CTS is posted; kind 1 = my recv arrived second
-// after the sender's RTS — the sender's proxy pushes, and this is the rescue:
-// pull if nobody claimed the transfer by `deadline` (the sender's process may
-// be stuck in a synchronous CUDA call, see rzv_post).
-struct RzvWatch {
-  int kind = 0;
-  int peer = -1;
-  uint64_t k = 0;
-  uint64_t op_seq = 0;
-  uint64_t deadline = 0;
-};
-
 }  // namespace iccl
 
 using namespace iccl;
@@ -383,8 +374,6 @@ struct iccl_comm {
   std::mutex qmu;
   std::condition_variable qcv;
   std::vector<Xfer> handoff;  // issued by the API thread, tracked by the proxy
-  std::vector<RzvWatch> watch_in;  // new rendezvous watches from the API thread (under qmu)
-  std::vector<RzvWatch> watches;   // proxy-owned
   std::mutex mon_mu;
   std::deque<iccl_mon_rec_t> mon;
   std::deque<iccl_switch_event_t> sw_events;
@@ -1133,10 +1122,6 @@ static iccl_result_t monitor_failed_link(iccl_comm* c, Channel& chn) {
   return ICCL_SUCCESS;
 }
 
-}  // namespace iccl
-static iccl_result_t progress_watches(iccl_comm* c, bool* busy);  // defined with the rendezvous below
-namespace iccl {
-
 static void proxy_loop(iccl_comm* c) {
   cudaSetDevice(c->dev);
   if (c->cfg.proxy_cpu >= 0) {
@@ -1157,8 +1142,6 @@ static void proxy_loop(iccl_comm* c) {
         c->qcv.wait_for(lk, std::chrono::microseconds(c->relay_buf ? 50 : 500));
       }
       batch.swap(c->handoff);
-      c->watches.insert(c->watches.end(), c->watch_in.begin(), c->watch_in.end());
-      c->watch_in.clear();
     }
     for (Xfer& x : batch) {
       Channel& chn = c->ch[x.chan];
@@ -1171,13 +1154,6 @@ static void proxy_loop(iccl_comm* c) {
       continue;
     }
     fire_time_faults(c);
-    if (!c->watches.empty()) {
-      iccl_result_t r = progress_watches(c, &busy);
-      if (r) {
-        set_async(c, r, std::string("proxy: ") + last_error());
-        continue;
-      }
-    }
     for (int ci = 0; ci < 2 * c->nranks; ci++) {
       Channel& chn = c->ch[ci];
       int req = c->path_req[ci].exchange(-1);
@@ -1342,38 +1318,30 @@ static iccl_result_t rzv_issue(iccl_comm* c, int kind, int peer, uint64_t k, uin
   return ICCL_SUCCESS;
 }
 
-static void add_watch(iccl_comm* c, const RzvWatch& w) {
-  c->pending_xfers.fetch_add(1);  // destroy waits until the watch is resolved
-  {
-    std::lock_guard<std::mutex> g(c->qmu);
-    c->watch_in.push_back(w);
-  }
-  c->qcv.notify_one();
-}
-
 // Rendezvous of the k-th op of an ordered pair (SPEC.md:194's RTS / CTS): post
-// my half (IPC handle, offset, op slot), then decide who issues.
+// my half (IPC handle, offset, op slot); the side that arrives second has
+// both halves and issues every chunk of the transfer right here, from its own
+// API call — a push by the sender or a pull by the receiver.
 //
-// The sender issues (a push by its copy engine): pushes in both directions
-// run at full NVLink rate, two opposite pulls do not (half rate measured,
-// scripts/diag_ring.py).  A sender that arrives second has both halves and
-// issues right here, from its API call.  A sender that arrives first leaves
-// a watch to its proxy, which pushes once the receiver's CTS is posted.
-//
-// The receiver's rescue: while any thread of a process sits in a
+// Why the API call and not the proxy: while any thread of a process sits in a
 // synchronous CUDA call on a stream parked behind one of our ops (a pageable
-// cudaMemcpy, .cpu()), every other CUDA call of that process blocks —
-// memcpy, kernel launch, stream memop, event record alike
-// (probes/p2p_probe6.cu) — so a sender's proxy can be stuck.  A receiver
-// that arrives second therefore also leaves a watch: if nobody claimed the
-// transfer after delta_us, its proxy claims it and pulls.  Exactly one side
-// wins `claimed`.  A self pair issues from the second API call.
-static iccl_result_t rzv_post(iccl_comm* c, const OpDesc& op) {
+// cudaMemcpy, .cpu()), every other CUDA call of that process blocks — memcpy,
+// kernel launch, stream memop, event record alike (probes/p2p_probe6.cu).  A
+// proxy that still had to enqueue the copy deadlocks with such a user; with
+// all device work enqueued before the API returns nothing can.
+//
+// Why senders try to come second: two opposite pushes between a pair run at
+// full rate each, two opposite pulls only at half rate (scripts/diag_ring.py).
+// A send therefore first waits up to `wait_us` for the receiver's half to be
+// posted (receivers usually post early; inside a group every recv is posted
+// before any send), and only then posts its own.
+static iccl_result_t rzv_post(iccl_comm* c, const OpDesc& op, uint64_t wait_us) {
   const int peer = op.peer, kind = op.kind;
   const uint64_t k = kind == 0 ? c->pair_sends[peer]++ : c->pair_recvs[peer]++;
   RzvEntry& e = rzv_entry(c, kind, peer, k);
   const uint64_t g = k / kRzvDepth;
-  // the entry is reused once both sides arrived and a side claimed its previous generation
+  // the entry is reused once both sides arrived for its previous generation
+  // and that transfer was claimed
   uint64_t t0 = now_ns();
   while (e.arrivals.load(std::memory_order_acquire) < 2 * g || e.claimed.load(std::memory_order_acquire) < g) {
     if (c->async_err.load() != ICCL_SUCCESS) return (iccl_result_t)c->async_err.load();
@@ -1383,6 +1351,10 @@ static iccl_result_t rzv_post(iccl_comm* c, const OpDesc& op) {
       return ICCL_ERR_TIMEOUT;
     }
     sched_yield();
+  }
+  if (kind == 0 && peer != c->rank && wait_us > 0) {
+    const uint64_t deadline = now_ns() + wait_us * 1000ull;
+    while (e.arrivals.load(std::memory_order_acquire) < 2 * g + 1 && now_ns() < deadline) sched_yield();
   }
   RzvSide& mine = e.side[kind];
   mine.bytes = op.bytes;
@@ -1395,48 +1367,9 @@ static iccl_result_t rzv_post(iccl_comm* c, const OpDesc& op) {
     iccl_result_t r = export_buffer(c, op.src, &mine);
     if (r) return r;
   }
-  const bool second = e.arrivals.fetch_add(1, std::memory_order_acq_rel) == 2 * g + 1;
-  if (second && (kind == 0 || peer == c->rank)) {
-    if (!rzv_claim(e, k)) return ICCL_SUCCESS;  // (cannot happen: the first side never claims)
-    return rzv_issue(c, kind, peer, k, op.op_seq, false);
-  }
-  if (kind == 0) {
-    add_watch(c, RzvWatch{0, peer, k, op.op_seq, 0});
-  } else if (second) {
-    add_watch(c, RzvWatch{1, peer, k, op.op_seq, now_ns() + c->cfg.delta_us * 1000ull});
-  }
-  return ICCL_SUCCESS;
-}
-
-// Proxy side of the watches: push when the CTS arrived (and we win the
-// claim); rescue-pull after the deadline if the sender never claimed.
-static iccl_result_t progress_watches(iccl_comm* c, bool* busy) {
-  const uint64_t t = now_ns();
-  size_t keep = 0;
-  for (size_t i = 0; i < c->watches.size(); i++) {
-    RzvWatch w = c->watches[i];
-    RzvEntry& e = rzv_entry(c, w.kind, w.peer, w.k);
-    const uint64_t g = w.k / kRzvDepth;
-    bool resolved = false;
-    if (e.claimed.load(std::memory_order_acquire) > g) {
-      resolved = true;  // the other side issued it
-    } else if (w.kind == 0 ? e.arrivals.load(std::memory_order_acquire) >= 2 * g + 2 : t > w.deadline) {
-      resolved = true;
-      if (rzv_claim(e, w.k)) {
-        iccl_result_t r = rzv_issue(c, w.kind, w.peer, w.k, w.op_seq, true);
-        if (r) return r;
-        if (w.kind == 1) ICCL_TRACE("rescue pull of pair %d->%d #%llu", w.peer, c->rank, (unsigned long long)w.k);
-      }
-    }
-    if (resolved) {
-      c->pending_xfers.fetch_sub(1);
-      *busy = true;
-    } else {
-      c->watches[keep++] = w;
-    }
-  }
-  c->watches.resize(keep);
-  return ICCL_SUCCESS;
+  if (e.arrivals.fetch_add(1, std::memory_order_acq_rel) != 2 * g + 1) return ICCL_SUCCESS;  // first
+  if (!rzv_claim(e, k)) return ICCL_SUCCESS;  // cannot happen: the first side never claims
+  return rzv_issue(c, kind, peer, k, op.op_seq, false);
 }
 
 // Stream markers of copy-engine ops: phase 0 = WriteValue(ready) for every
@@ -1552,10 +1485,10 @@ static iccl_result_t enqueue_op(iccl_comm* c, int kind, const void* buf, size_t 
           bytes <= kLLMaxBytes && c->ll_region != nullptr;
   if (op.ll) {
     op.ll_seq = kind == 0 ? ++c->ll_sent[peer] : ++c->ll_recvd[peer];
-  } else {
-    r = rzv_post(c, op);
+  } else if (kind == 1 || c->group_depth == 0) {
+    r = rzv_post(c, op, kind == 0 ? kSendWaitUs : 0);
     if (r) return r;
-  }
+  }  // a send inside a group posts at group_end, after every recv of the group
   c->ranks[c->rank].op_count.fetch_add(1, std::memory_order_relaxed);
   if (req) *req = ((uint64_t)op.slot << 32) | op.gen;
   if (c->group_depth > 0) {
@@ -1935,6 +1868,15 @@ iccl_result_t iccl_group_end(iccl_comm_t c) {
   if (--c->group_depth > 0) return ICCL_SUCCESS;
   std::vector<std::pair<OpDesc, cudaStream_t>> ops;
   ops.swap(c->group_ops);
+  // the group's sends, in call order: each waits (within one shared budget)
+  // for its receiver's half so that it arrives second and pushes
+  const uint64_t deadline = now_ns() + kGroupSendWaitUs * 1000ull;
+  for (auto& p : ops) {
+    if (p.first.kind != 0 || p.first.ll) continue;
+    const uint64_t t = now_ns();
+    iccl_result_t r = rzv_post(c, p.first, t < deadline ? (deadline - t) / 1000 : 0);
+    if (r) return r;
+  }
   // one batched marker set per distinct stream
   std::vector<cudaStream_t> order;
   for (auto& p : ops)
