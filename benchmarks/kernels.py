@@ -53,7 +53,7 @@ def timed(fn, reps, stream):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
-    ap.add_argument("--only", default="", help="comma list of k1_local,k1_peer,k2,k3")
+    ap.add_argument("--only", default="", help="comma list of k1_local,k1_peer,k1_pull,k2,k3")
     args = ap.parse_args()
     from paper_2510_00991_b200 import gather_rows, scatter_rows
     from paper_2510_00991_b200._lib import lib
@@ -93,6 +93,23 @@ def main():
                         "achieved_GBps": round(ach, 1), "peak": 770.0, "bound": "nvlink (measured peer copy)",
                         "frac": round(ach / 770.0, 4), "nominal_frac": round(ach / 900.0, 4), "bit_exact": ok})
         del dst
+    if (not only or "k1_pull" in only) and torch.cuda.device_count() > 1:
+        # pull: cuda:0 reads cuda:1's memory (the SM backup of a receiver-issued transfer)
+        rsrc = src.to("cuda:1")
+        dst = torch.empty_like(src)
+        torch.cuda.synchronize()
+        for name, fn, ctas_list in (("K1 iccl_copy_tma pull 1->0", lib.iccl_copy_sm, (16, 148)),
+                                    ("K1 iccl_copy_pull 1->0", lib.iccl_copy_sm_pull, (16, 64, 148))):
+            for ctas in ctas_list:
+                def run(fn=fn, ctas=ctas):
+                    assert fn(C.c_void_p(rsrc.data_ptr()), C.c_void_p(dst.data_ptr()), n, ctas, sh) == 0
+                t = timed(run, max(1, args.reps // 4), s)
+                ok = torch.equal(dst, src)
+                ach = n / t / 1e9
+                out.append({"kernel": name, "bytes": n, "ctas": ctas, "us": round(t * 1e6, 2),
+                            "achieved_GBps": round(ach, 1), "peak": 770.0, "bound": "nvlink (measured peer copy)",
+                            "frac": round(ach / 770.0, 4), "bit_exact": ok})
+        del dst, rsrc
     T, k, H = 4096, 8, 7168
     row = H * 2
     rows = T * k

@@ -6,19 +6,18 @@ without stealing SMs from it (SPEC.md:500-517
 ``enforce_order`` / ``run_1f1b``).  Every rank is one stage; each microbatch
 carries a bf16 [4, 4096, 8192] activation (256 MiB, config 3's hop).  Stage
 compute is a cuBLAS bf16 GEMM chain on the compute stream (forward: one
-[16384, 8192] x [8192, 8192] GEMM, backward: two), P2P runs on a separate
-communication stream and the compute stream waits only for the activation /
-gradient it consumes — so communication overlaps the neighbouring
-microbatches' compute.
+[16384, 8192] x [8192, 8192] GEMM, backward: two).
 
-Schedule (non-interleaved 1F1B): stage s runs min(S - s - 1, M) warm-up
-forwards, then alternates one forward / one backward, then drains the
-backwards.  Metric: iteration time for M microbatches (max over ranks,
-device-timed) and achieved TFLOP/s per GPU; ``--impl nccl`` runs the same
-schedule with torch.distributed isend/irecv on NCCL (its kernels take SMs
-from the GEMMs), ``--impl iccl`` the copy-engine path (0 SMs).
+Schedule: Megatron's non-interleaved 1F1B with its fused exchanges —
+``send_forward_recv_backward`` / ``send_backward_recv_forward`` are one
+batched isend/irecv each (the pattern that keeps NCCL deadlock-free) — on a
+communication stream; the compute stream waits only for the tensor it
+consumes.  Metric: iteration time for M microbatches (max over ranks,
+device-timed) and achieved TFLOP/s per GPU.  ``--impl nccl`` runs the
+identical schedule with ``torch.distributed.batch_isend_irecv`` on NCCL (its
+kernels take SMs from the GEMMs), ``--impl iccl`` the copy-engine path (0 SMs).
 
-    python -m torch.distributed.run --nproc-per-node 4 --master-addr 127.0.0.1 \
+    python -m torch.distributed.run --nproc-per-node 4 --master-addr 127.0.0.1 \\
         benchmarks/pp_1f1b.py --impl iccl
 """
 import argparse
@@ -46,83 +45,84 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     S, M = world, args.microbatches
     T, H = 4 * 4096, 8192
+    first, last = rank == 0, rank == S - 1
     comm = None
+    iccl = None
     if args.impl == "iccl":
         import paper_2510_00991_b200 as iccl
         comm = iccl.init(rank, world, local, iccl.IcclConfig.defaults())
     g = torch.Generator(device=dev).manual_seed(10 + rank)
     W = torch.randn(H, H, dtype=torch.bfloat16, device=dev, generator=g) * 0.01
     comp = torch.cuda.current_stream()
-    # one communication stream per (direction, peer): every stream carries one
-    # ordered pair's ops in FIFO order, so no op waits behind another pair's
-    streams = {}
-
-    def stream_for(kind, peer):
-        if (kind, peer) not in streams:
-            streams[(kind, peer)] = torch.cuda.Stream(device=dev)
-        return streams[(kind, peer)]
-    # per-microbatch buffers: activation in / out, gradient in / out
-    act_in = [torch.empty(T, H, dtype=torch.bfloat16, device=dev) for _ in range(M)]
-    act_out = [torch.empty(T, H, dtype=torch.bfloat16, device=dev) for _ in range(M)]
-    grad_in = [torch.empty(T, H, dtype=torch.bfloat16, device=dev) for _ in range(M)]
-    grad_out = [torch.empty(T, H, dtype=torch.bfloat16, device=dev) for _ in range(M)]
+    cstream = torch.cuda.Stream(device=dev)
+    pool = [torch.empty(T, H, dtype=torch.bfloat16, device=dev) for _ in range(8)]
     x0 = torch.randn(T, H, dtype=torch.bfloat16, device=dev, generator=g)
     tmp = torch.empty(T, H, dtype=torch.bfloat16, device=dev)
+    nxt = [0]
 
-    def p2p(kind, t, peer):
-        """Enqueue on the pair's comm stream after the compute that produced t; return an event."""
-        cstream = stream_for(kind, peer)
-        if kind == "send":
-            cstream.wait_stream(comp)  # the data is produced by the compute stream; a recv posts early
+    def buf():
+        b = pool[nxt[0] % len(pool)]
+        nxt[0] += 1
+        return b
+
+    def exchange(sends, recvs):
+        """One batched isend/irecv on the comm stream after the compute that
+        produced the sends; the compute stream then waits for the received
+        tensors, which are returned."""
+        cstream.wait_stream(comp)
+        outs = [buf() for _ in recvs]
         with torch.cuda.stream(cstream):
             if comm:
-                (comm.isend if kind == "send" else comm.irecv)(t, peer, stream=cstream)
+                ops = [iccl.P2POp("isend", t, p) for t, p in sends] + \
+                      [iccl.P2POp("irecv", o, p) for o, p in zip(outs, recvs)]
+                comm.batch_isend_irecv(ops, stream=cstream)
             else:
-                op = dist.P2POp(dist.isend if kind == "send" else dist.irecv, t, peer)
-                for w in dist.batch_isend_irecv([op]):
+                ops = [dist.P2POp(dist.isend, t, p) for t, p in sends] + \
+                      [dist.P2POp(dist.irecv, o, p) for o, p in zip(outs, recvs)]
+                for w in dist.batch_isend_irecv(ops):
                     w.wait()
-            t.record_stream(cstream)
-        ev = torch.cuda.Event()
-        ev.record(cstream)
-        return ev
+            for t, _ in sends:
+                t.record_stream(cstream)
+        if recvs:
+            comp.wait_stream(cstream)
+        return outs
 
-    def forward(i):
-        if rank > 0:
-            comp.wait_event(p2p("recv", act_in[i], rank - 1))
-            src = act_in[i]
-        else:
-            src = x0
-        torch.matmul(src, W, out=act_out[i])
-        if rank < S - 1:
-            p2p("send", act_out[i], rank + 1)
+    def forward(x):
+        y = buf()
+        torch.matmul(x0 if x is None else x, W, out=y)
+        return y
 
-    def backward(i):
-        if rank < S - 1:
-            comp.wait_event(p2p("recv", grad_in[i], rank + 1))
-            gsrc = grad_in[i]
-        else:
-            gsrc = act_out[i]
-        torch.matmul(gsrc, W.t(), out=grad_out[i])   # dX
-        torch.matmul(gsrc, W, out=tmp)               # stands in for dW (same flops)
-        if rank > 0:
-            p2p("send", grad_out[i], rank - 1)
+    def backward(dy):
+        dx = buf()
+        torch.matmul(dy, W.t(), out=dx)   # dX
+        torch.matmul(dy, W, out=tmp)      # stands in for dW (same flops)
+        return dx
 
     def iteration():
         warm = min(S - rank - 1, M)
-        f = b = 0
         for _ in range(warm):
-            forward(f)
-            f += 1
-        while f < M:
-            forward(f)
-            f += 1
-            backward(b)
-            b += 1
-        while b < M:
-            backward(b)
-            b += 1
-        for cs in streams.values():
-            comp.wait_stream(cs)
+            x = None if first else exchange([], [rank - 1])[0]              # recv_forward
+            y = forward(x)
+            exchange([(y, rank + 1)], [])                                     # send_forward
+        steady = M - warm
+        x = None if (first or steady == 0) else exchange([], [rank - 1])[0]
+        for i in range(steady):
+            y = forward(x)
+            dy = y if last else exchange([(y, rank + 1)], [rank + 1])[0]     # send_forward_recv_backward
+            dx = backward(dy)
+            if i == steady - 1:
+                if not first:
+                    exchange([(dx, rank - 1)], [])                            # send_backward
+            elif first:
+                x = None
+            else:
+                x = exchange([(dx, rank - 1)], [rank - 1])[0]                # send_backward_recv_forward
+        for _ in range(warm):
+            dy = exchange([], [rank + 1])[0]                                  # recv_backward
+            dx = backward(dy)
+            if not first:
+                exchange([(dx, rank - 1)], [])                                # send_backward
+        comp.wait_stream(cstream)
 
     for _ in range(args.warmup):
         iteration()

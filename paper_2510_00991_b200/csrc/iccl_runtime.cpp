@@ -83,6 +83,7 @@ constexpr int kProxyNapUs = 20;  // proxy back-off when a pass moved nothing
 // How long a send waits for its receiver's half before posting its own (so
 // that it arrives second and pushes, see rzv_post): single ops / a group.
 constexpr uint64_t kSendWaitUs = 50;
+constexpr int kPullCtas = 148;  // SM pulls need the whole GPU's loads in flight (probes: 16 CTAs 240 GB/s, 148: 755)
 constexpr uint64_t kGroupSendWaitUs = 2000;
 
 // ---------------------------------------------------------------- shared control block
@@ -797,7 +798,10 @@ static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
     iccl_result_t r = relay_push(c, chn, x, off, n, sc.s, rc);
     if (r) return r;
   } else {
-    ICCL_CHECK_CUDA(launch_copy(x.src + off, x.dst + off, n, c->cfg.sm_cap, st, sc.s));
+    if (chn.dir == 1 && chn.peer != c->rank)  // a pull: the source is the peer's memory
+      ICCL_CHECK_CUDA(launch_copy_pull(x.src + off, x.dst + off, n, kPullCtas, st, sc.s));
+    else
+      ICCL_CHECK_CUDA(launch_copy(x.src + off, x.dst + off, n, c->cfg.sm_cap, st, sc.s));
     c->copies_issued += 1;
   }
   c->kernels_launched += eng == ENG_SM ? 1 : 0;
@@ -2041,6 +2045,12 @@ iccl_result_t iccl_expand_rows(const void* src, void* dst, const int64_t* pos, i
   if ((n_src > 0 && k > 0 && (!src || !dst || !pos)) || n_src < 0 || k < 0 || row_bytes <= 0)
     return ICCL_ERR_INVALID_ARGUMENT;
   ICCL_CHECK_CUDA(launch_expand_rows(src, dst, pos, n_src, k, row_bytes, ctas > 0 ? ctas : 148 * 8, s));
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_copy_sm_pull(const void* src, void* dst, size_t bytes, int ctas, cudaStream_t s) {
+  if (bytes > 0 && (!src || !dst)) return ICCL_ERR_INVALID_ARGUMENT;
+  ICCL_CHECK_CUDA(launch_copy_pull(src, dst, bytes, ctas > 0 ? ctas : kPullCtas, nullptr, s));
   return ICCL_SUCCESS;
 }
 
