@@ -1334,8 +1334,8 @@ static iccl_result_t rzv_issue(iccl_comm* c, int kind, int peer, uint64_t k, uin
 // proxy that still had to enqueue the copy deadlocks with such a user; with
 // all device work enqueued before the API returns nothing can.
 //
-// Why senders try to come second: two opposite pushes between a pair run at
-// full rate each, two opposite pulls only at half rate (scripts/diag_ring.py).
+// Why senders try to come second: a copy-engine pull runs ~5% slower than a
+// push (probes/p2p_probe6.cu), and the paper's transfers are sender-driven.
 // A send therefore first waits up to `wait_us` for the receiver's half to be
 // posted (receivers usually post early; inside a group every recv is posted
 // before any send), and only then posts its own.
