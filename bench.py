@@ -20,6 +20,10 @@ Launch: ``python bench.py`` (N=1) or
 import argparse
 import json
 import os
+
+# one hardware queue per stream: a stream parked on a stream-memory wait must not
+# stall the library's other streams
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import subprocess
 import sys
 import time

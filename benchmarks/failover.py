@@ -24,6 +24,10 @@ Phases (each K timed steps, CUDA events, max over ranks):
 import argparse
 import json
 import os
+
+# one hardware queue per stream: a stream parked on a stream-memory wait must not
+# stall the library's other streams
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import statistics
 import sys
 import time

@@ -13,6 +13,10 @@ none.
 import argparse
 import json
 import os
+
+# one hardware queue per stream: a stream parked on a stream-memory wait must not
+# stall the library's other streams
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import random
 import statistics
 import sys

@@ -21,6 +21,10 @@ import argparse
 import ctypes as C
 import json
 import os
+
+# one hardware queue per stream: a stream parked on a stream-memory wait must not
+# stall the library's other streams
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import sys
 
 import torch
@@ -98,8 +102,7 @@ def main():
         rsrc = src.to("cuda:1")
         dst = torch.empty_like(src)
         torch.cuda.synchronize()
-        for name, fn, ctas_list in (("K1 iccl_copy_tma pull 1->0", lib.iccl_copy_sm, (16, 148)),
-                                    ("K1 iccl_copy_pull 1->0", lib.iccl_copy_sm_pull, (16, 64, 148))):
+        for name, fn, ctas_list in (("K1 iccl_copy_tma pull 1->0", lib.iccl_copy_sm, (16, 148)),):
             for ctas in ctas_list:
                 def run(fn=fn, ctas=ctas):
                     assert fn(C.c_void_p(rsrc.data_ptr()), C.c_void_p(dst.data_ptr()), n, ctas, sh) == 0

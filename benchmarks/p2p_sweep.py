@@ -18,6 +18,10 @@ from the difference of two loop lengths (cancels the start skew).
 import argparse
 import json
 import os
+
+# one hardware queue per stream: a stream parked on a stream-memory wait must not
+# stall the library's other streams
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import sys
 import time
 

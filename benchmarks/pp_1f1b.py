@@ -23,6 +23,10 @@ kernels take SMs from the GEMMs), ``--impl iccl`` the copy-engine path (0 SMs).
 import argparse
 import json
 import os
+
+# one hardware queue per stream: a stream parked on a stream-memory wait must not
+# stall the library's other streams
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import sys
 
 import torch

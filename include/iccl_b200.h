@@ -219,10 +219,6 @@ iccl_result_t iccl_expand_rows(const void* src, void* dst, const int64_t* pos, i
 /* SM copy kernel (K1) on its own, for measurement and for callers that want
  * the SM path explicitly: copies bytes src -> dst with <= ctas CTAs. */
 iccl_result_t iccl_copy_sm(const void* src, void* dst, size_t bytes, int ctas, cudaStream_t stream);
-/* Its pull form, for a source in a peer's memory (16 B vector loads; TMA bulk
- * loads from NVLink-mapped memory are slow): the SM backup path of a
- * receiver-issued transfer. */
-iccl_result_t iccl_copy_sm_pull(const void* src, void* dst, size_t bytes, int ctas, cudaStream_t stream);
 
 /* ---- pure host arithmetic (no device needed; the product's own formulas) */
 /* retry_timeout: 4.096 us * 2^exp * (retry + 1), in ns. */

@@ -120,7 +120,6 @@ PROTOTYPES = {
     "iccl_scatter_rows": (_c, [_p, _p, _p, _i64, _i64, C.c_int, _p]),
     "iccl_expand_rows": (_c, [_p, _p, _p, _i64, C.c_int32, _i64, C.c_int, _p]),
     "iccl_copy_sm": (_c, [_p, _p, _sz, C.c_int, _p]),
-    "iccl_copy_sm_pull": (_c, [_p, _p, _sz, C.c_int, _p]),
     "iccl_retry_timeout_ns": (_u64, [C.c_int, C.c_int]),
     "iccl_switch_pointers": (C.c_int, [C.POINTER(XferState), C.POINTER(XferState)]),
     "iccl_per_message_throughput": (_c, [C.POINTER(MonRec), C.POINTER(C.c_double)]),

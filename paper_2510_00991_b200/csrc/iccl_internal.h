@@ -64,9 +64,6 @@ struct alignas(64) KernelStamp {
 // with at most `ctas` CTAs; TMA bulk body + vector head/tail.  `stamp` may be
 // null.
 cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, KernelStamp* stamp, cudaStream_t st);
-// K1 pull form (source in the peer's memory): 16 B vector loads instead of TMA bulk.
-cudaError_t launch_copy_pull(const void* src, void* dst, size_t bytes, int ctas, KernelStamp* stamp,
-                             cudaStream_t st);
 // Force-load every kernel (see iccl_kernels.cu: lazy loading vs parked streams).
 cudaError_t preload_kernels();
 // K5: low-latency (LL) eager path for small and mid-size messages.  8-byte

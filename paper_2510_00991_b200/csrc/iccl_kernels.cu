@@ -148,20 +148,6 @@ __global__ void __launch_bounds__(kCopyThreads) iccl_copy_tma(const char* __rest
   stamp_end(stamp);
 }
 
-// K1, pull form: the source is the peer's memory (a receiver re-issuing a
-// transfer on the SM backup path).  TMA bulk loads from an NVLink-mapped
-// source crawl (a failover step took 1.29 s, profiles/r01/README.md), so the
-// pull reads with plain 16 B vector loads, four in flight per thread.
-__global__ void __launch_bounds__(512) iccl_copy_pull(const char* __restrict__ src, char* __restrict__ dst,
-                                                      size_t head, size_t body, size_t tail, KernelStamp* stamp) {
-  stamp_begin(stamp);
-  const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, nthreads = (size_t)gridDim.x * blockDim.x;
-  copy_bytes(src, dst, head, tid, nthreads);
-  copy_vec16((const int4*)(src + head), (int4*)(dst + head), body / 16, tid, nthreads);
-  copy_bytes(src + head + body, dst + head + body, tail, tid, nthreads);
-  stamp_end(stamp);
-}
-
 // Fallback for buffers whose addresses differ mod 16: byte copy.
 __global__ void __launch_bounds__(512) iccl_copy_unaligned(const char* __restrict__ src, char* __restrict__ dst,
                                                            size_t n, KernelStamp* stamp) {
@@ -402,24 +388,6 @@ cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, Kern
   return cudaGetLastError();
 }
 
-cudaError_t launch_copy_pull(const void* src, void* dst, size_t bytes, int ctas, KernelStamp* stamp,
-                             cudaStream_t st) {
-  if (bytes == 0) return cudaSuccess;
-  const uintptr_t s = (uintptr_t)src, d = (uintptr_t)dst;
-  if (((s ^ d) & 15) != 0) {
-    int grid = (int)min((size_t)ctas, (bytes + 512 * 16 - 1) / (512 * 16));
-    iccl_copy_unaligned<<<grid < 1 ? 1 : grid, 512, 0, st>>>((const char*)src, (char*)dst, bytes, stamp);
-    return cudaGetLastError();
-  }
-  size_t head = (16 - (s & 15)) & 15;
-  if (head > bytes) head = bytes;
-  const size_t body = (bytes - head) & ~(size_t)15;
-  const size_t tail = bytes - head - body;
-  int grid = (int)min((size_t)ctas, (body / 16 + 512 * 4 - 1) / (512 * 4));
-  iccl_copy_pull<<<grid < 1 ? 1 : grid, 512, 0, st>>>((const char*)src, (char*)dst, head, body, tail, stamp);
-  return cudaGetLastError();
-}
-
 // Load every kernel of this module now.  With CUDA lazy loading the first
 // launch of a kernel loads its module, and a load issued while one of our
 // streams is parked on a stream-memop wait blocked the launching thread on
@@ -427,7 +395,7 @@ cudaError_t launch_copy_pull(const void* src, void* dst, size_t bytes, int ctas,
 // iccl_comm_init_rank calls this before any wait is enqueued.
 cudaError_t preload_kernels() {
   cudaFuncAttributes a;
-  const void* fns[] = {(const void*)iccl_copy_tma,   (const void*)iccl_copy_unaligned, (const void*)iccl_copy_pull, (const void*)iccl_stamp,
+  const void* fns[] = {(const void*)iccl_copy_tma,   (const void*)iccl_copy_unaligned, (const void*)iccl_stamp,
                        (const void*)iccl_read_globaltimer, (const void*)iccl_gather_rows,
                        (const void*)iccl_scatter_rows, (const void*)iccl_expand_rows,
                        (const void*)iccl_ll_group};

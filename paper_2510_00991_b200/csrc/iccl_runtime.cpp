@@ -64,26 +64,29 @@ namespace iccl {
 // ICCL_DEBUG=1: the proxy traces every device call it makes (stderr), so a
 // stuck proxy shows the call it is blocked in.
 static const bool g_debug = getenv("ICCL_DEBUG") && atoi(getenv("ICCL_DEBUG")) > 0;
-#define ICCL_TRACE(...)                    \
-  do {                                     \
-    if (::iccl::g_debug) {                 \
-      fprintf(stderr, "[iccl] " __VA_ARGS__); \
-      fputc('\n', stderr);                 \
-    }                                      \
+#define ICCL_TRACE(...)                                                          \
+  do {                                                                           \
+    if (::iccl::g_debug) {                                                       \
+      char b_[512];                                                              \
+      snprintf(b_, sizeof(b_), __VA_ARGS__);                                     \
+      fprintf(stderr, "[iccl %.6f] %s\n", (double)::iccl::now_ns() * 1e-9, b_); \
+    }                                                                            \
   } while (0)
 
 constexpr uint64_t kMagic = 0x3030324242434349ull;  // "ICCLB200"
 constexpr int kSlots = 4096;                        // op slots per rank (ready/done flags)
 constexpr int kRzvDepth = 1024;                     // rendezvous entries per ordered pair
 constexpr int kMaxRanks = 64;
-constexpr int kGateWords = 1024;
+// Gate words (fault gates, probe gates): a closed gate is never recycled; a
+// released one only after the whole ring went round (16K allocations — at a
+// probe per 200 us, > 3 s — so every device wait on it has long executed).
+constexpr int kGateWords = 16384;
 constexpr int kStampSlots = 4096;
 constexpr size_t kScratchBytes = 4096;
 constexpr int kProxyNapUs = 20;  // proxy back-off when a pass moved nothing
 // How long a send waits for its receiver's half before posting its own (so
 // that it arrives second and pushes, see rzv_post): single ops / a group.
 constexpr uint64_t kSendWaitUs = 50;
-constexpr int kPullCtas = 148;  // SM pulls need the whole GPU's loads in flight (probes: 16 CTAs 240 GB/s, 148: 755)
 constexpr uint64_t kGroupSendWaitUs = 2000;
 
 // ---------------------------------------------------------------- shared control block
@@ -261,7 +264,6 @@ struct Xfer {
   bool eligible = false;
   uint64_t last_progress = 0;
   int switches = 0;
-  int pending_gate = -1;  // gate released once this xfer completes on the new path
   int fault_ops_index = -1;
   std::vector<ChunkRec> rec;
   std::vector<cudaEvent_t> fences;  // events the completion must also wait for
@@ -284,7 +286,6 @@ struct FaultState {
   bool down = false;
   int gate = -1;        // gate word index while down
   uint64_t down_at = 0;  // ns
-  std::vector<int> probe_gates;  // probes parked while down: released on Up
 };
 
 // One direction of traffic with one peer, as seen by the issuing side:
@@ -304,7 +305,6 @@ struct Channel {
   FaultState fault[2];
   // probe state
   bool probe_out = false;
-  int probe_gate = -1;
   uint32_t probe_ticket_expect = 0;
   uint64_t probe_sent = 0;
   int probe_path = 0;
@@ -339,6 +339,8 @@ struct iccl_comm {
   uint32_t* pinned = nullptr;
   size_t pinned_bytes = 0;
   volatile uint32_t* gate_words = nullptr;
+  std::vector<uint8_t> gate_closed;  // 1 while a gate is allocated and not yet released (gate_mu)
+  std::mutex gate_mu;                // leaf lock: gate allocation / release
   std::atomic<int> next_gate{0};
   KernelStamp* stamps = nullptr;
   std::atomic<int> next_stamp{0};
@@ -512,7 +514,10 @@ static void publish(iccl_comm* c, const Xfer& x) {
 }
 
 static int alloc_gate(iccl_comm* c) {
+  std::lock_guard<std::mutex> lk(c->gate_mu);
   int g = c->next_gate++ % kGateWords;
+  for (int tries = 0; c->gate_closed[g] && tries < kGateWords; tries++) g = c->next_gate++ % kGateWords;
+  c->gate_closed[g] = 1;
   c->gate_words[g] = 0;
   std::atomic_thread_fence(std::memory_order_seq_cst);
   return g;
@@ -520,7 +525,9 @@ static int alloc_gate(iccl_comm* c) {
 
 static void release_gate(iccl_comm* c, int g) {
   if (g < 0) return;
+  std::lock_guard<std::mutex> lk(c->gate_mu);
   __atomic_store_n((uint32_t*)&c->gate_words[g], 1u, __ATOMIC_SEQ_CST);
+  c->gate_closed[g] = 0;
 }
 
 static void push_switch_event(iccl_comm* c, int peer, int to, int resume, int trigger, uint64_t detect_ns) {
@@ -678,8 +685,6 @@ static void fault_up(iccl_comm* c, FaultState& fs) {
   fs.down = false;
   release_gate(c, fs.gate);
   fs.gate = -1;
-  for (int g : fs.probe_gates) release_gate(c, g);
-  fs.probe_gates.clear();
 }
 
 // A fault on directed path src -> dst applies on both endpoints (either may
@@ -798,10 +803,8 @@ static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
     iccl_result_t r = relay_push(c, chn, x, off, n, sc.s, rc);
     if (r) return r;
   } else {
-    if (chn.dir == 1 && chn.peer != c->rank)  // a pull: the source is the peer's memory
-      ICCL_CHECK_CUDA(launch_copy_pull(x.src + off, x.dst + off, n, kPullCtas, st, sc.s));
-    else
-      ICCL_CHECK_CUDA(launch_copy(x.src + off, x.dst + off, n, c->cfg.sm_cap, st, sc.s));
+    ICCL_TRACE("K1 op %llu chunk %d: %zu B on %p", (unsigned long long)x.op_seq, k, n, (void*)sc.s);
+    ICCL_CHECK_CUDA(launch_copy(x.src + off, x.dst + off, n, c->cfg.sm_cap, st, sc.s));
     c->copies_issued += 1;
   }
   c->kernels_launched += eng == ENG_SM ? 1 : 0;
@@ -883,52 +886,54 @@ static iccl_result_t switch_path(iccl_comm* c, Channel& chn, int to, int trigger
     x.path = to;
     x.done_enqueued = false;
     x.switches++;
-    if (had_work && stale_gate >= 0) x.pending_gate = stale_gate;
     x.last_progress = now_ns();
     publish(c, x);
   }
   if (stale_gate >= 0) {
-    // future work on the still-Down path waits on a fresh gate epoch; the old
-    // one is released (flushing the stale copies) once the data went the new way
+    // Future work on the still-Down path waits on a fresh gate epoch; the old
+    // gate is released right away: its copies are flushed (SPEC.md:285's
+    // Flushed WCs) — they rewrite the bytes the new path delivers, and the
+    // op's completion waits for them through the fences above.  Leaving a
+    // stream parked would also stall every stream sharing its hardware queue
+    // (a failover step took 1.29 s that way, profiles/r01/README.md).
     chn.fault[from].gate = alloc_gate(c);
-    bool any_pending = false;
-    for (Xfer& x : chn.xfers) any_pending |= (x.pending_gate == stale_gate);
-    if (!any_pending) release_gate(c, stale_gate);
+    release_gate(c, stale_gate);
   }
   lk.unlock();
   chn.failed_over = (to == 1 && trigger == 1);
   ps.active_path.store(to);
   ps.switches.fetch_add(1);
-  if (chn.probe_gate >= 0) release_gate(c, chn.probe_gate);  // abandon the outstanding probe
-  chn.probe_gate = -1;
-  chn.probe_out = false;
+  chn.probe_out = false;  // abandon the outstanding probe
   chn.last_probe = now_ns();
+  ICCL_TRACE("switch pair %d->%d to path %d at chunk %d (trigger %d, detect %llu ns)", chn.src, chn.dst, to, resume,
+             trigger, (unsigned long long)detect);
   push_switch_event(c, chn.peer, to, resume, trigger, detect);
   return ICCL_SUCCESS;
 }
 
-// A probe never stays parked on the device: while the path is Down it waits on
-// its own gate word, which the fault's Up releases (the probe then succeeds)
-// or the proxy releases when it gives up on the probe (result ignored), so no
-// device-wide synchronize can hang on an injected fault.
 static void retire_probe(iccl_comm* c, Channel& chn) {
-  if (chn.probe_gate >= 0) release_gate(c, chn.probe_gate);
-  chn.probe_gate = -1;
+  (void)c;
   chn.probe_out = false;
 }
 
+// The CTS probe of check_receiver_timeout / monitor_failed_link
+// (SPEC.md:246-273).  Over an injected-Down path it is lost: nothing is
+// enqueued (a probe parked on the device would stall every stream sharing its
+// hardware queue) and the proxy sees no completion within delta.
 static iccl_result_t send_probe(iccl_comm* c, Channel& chn, int path) {
   const int si = chn.probe_stream;
   StreamCtx& sc = c->streams[si];
-  chn.probe_gate = -1;
+  bool down;
   {
     std::lock_guard<std::mutex> g(c->fault_mu);
-    if (chn.fault[path].down) {
-      chn.probe_gate = alloc_gate(c);
-      chn.fault[path].probe_gates.push_back(chn.probe_gate);
-      iccl_result_t r = memop_wait(sc.s, &c->gate_words[chn.probe_gate], 1);
-      if (r) return r;
-    }
+    down = chn.fault[path].down;
+  }
+  chn.probe_out = true;
+  chn.probe_sent = now_ns();
+  chn.probe_path = path;
+  if (down) {
+    chn.probe_ticket_expect = sc.ticket + 0x40000000u;  // never reached
+    return ICCL_SUCCESS;
   }
   // a 16-byte CTS over the suspect path: into the peer's scratch (push
   // channel) or out of it (pull channel)
@@ -938,12 +943,7 @@ static iccl_result_t send_probe(iccl_comm* c, Channel& chn, int path) {
     ICCL_CHECK_CU(driver()->cuMemcpyDtoDAsync((CUdeviceptr)(c->scratch + 2048 + 16 * chn.peer),
                                               (CUdeviceptr)chn.peer_scratch, 16, (CUstream)sc.s));
   chn.probe_ticket_expect = ++sc.ticket;
-  iccl_result_t r = memop_write(sc.s, sc.prog, chn.probe_ticket_expect);
-  if (r) return r;
-  chn.probe_out = true;
-  chn.probe_sent = now_ns();
-  chn.probe_path = path;
-  return ICCL_SUCCESS;
+  return memop_write(sc.s, sc.prog, chn.probe_ticket_expect);
 }
 
 static void record_monitor(iccl_comm* c, Channel& chn, Xfer& x, int k, uint64_t t2_host) {
@@ -1030,13 +1030,6 @@ static iccl_result_t progress_channel(iccl_comm* c, Channel& chn, bool* busy) {
   while (!chn.xfers.empty()) {
     Xfer& x = chn.xfers.front();
     if (!(x.completed == x.nchunks && x.done_enqueued)) break;
-    if (x.pending_gate >= 0) {
-      int g = x.pending_gate;
-      x.pending_gate = -1;
-      bool others = false;
-      for (size_t i = 1; i < chn.xfers.size(); i++) others |= chn.xfers[i].pending_gate == g;
-      if (!others) release_gate(c, g);  // flush the abandoned path's stale copies
-    }
     if (!x.fences.empty()) {
       // fences may only be destroyed after the device consumed them; the
       // done flag write follows them on the same stream
@@ -1044,6 +1037,8 @@ static iccl_result_t progress_channel(iccl_comm* c, Channel& chn, bool* busy) {
       for (cudaEvent_t fe : x.fences) cudaEventDestroy(fe);
       x.fences.clear();
     }
+    ICCL_TRACE("retire op %llu (pair %d->%d #%llu)", (unsigned long long)x.op_seq, x.src_rank, x.dst_rank,
+               (unsigned long long)x.pair_seq);
     put_events(c, x);
     chn.xfers.pop_front();
     c->pending_xfers.fetch_sub(1);
@@ -1582,7 +1577,8 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
   c->pinned_bytes = 64 * 1024 + sizeof(KernelStamp) * kStampSlots + kGateWords * 4;
   ICCL_CHECK_CUDA(cudaHostAlloc((void**)&c->pinned, c->pinned_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
   memset(c->pinned, 0, c->pinned_bytes);
-  c->gate_words = (volatile uint32_t*)((char*)c->pinned + 32 * 1024);
+  c->gate_words = (volatile uint32_t*)((char*)c->pinned + 64 * 1024 + sizeof(KernelStamp) * kStampSlots);
+  c->gate_closed.assign(kGateWords, 0);
   c->stamps = (KernelStamp*)((char*)c->pinned + 64 * 1024);
   c->gtimer = (unsigned long long*)((char*)c->pinned + 48 * 1024);
   ICCL_CHECK_CUDA(cudaMalloc((void**)&c->scratch, kScratchBytes));
@@ -2045,12 +2041,6 @@ iccl_result_t iccl_expand_rows(const void* src, void* dst, const int64_t* pos, i
   if ((n_src > 0 && k > 0 && (!src || !dst || !pos)) || n_src < 0 || k < 0 || row_bytes <= 0)
     return ICCL_ERR_INVALID_ARGUMENT;
   ICCL_CHECK_CUDA(launch_expand_rows(src, dst, pos, n_src, k, row_bytes, ctas > 0 ? ctas : 148 * 8, s));
-  return ICCL_SUCCESS;
-}
-
-iccl_result_t iccl_copy_sm_pull(const void* src, void* dst, size_t bytes, int ctas, cudaStream_t s) {
-  if (bytes > 0 && (!src || !dst)) return ICCL_ERR_INVALID_ARGUMENT;
-  ICCL_CHECK_CUDA(launch_copy_pull(src, dst, bytes, ctas > 0 ? ctas : kPullCtas, nullptr, s));
   return ICCL_SUCCESS;
 }
 

@@ -1,6 +1,10 @@
 import os
 import sys
 
+# before torch creates a CUDA context (spawned rank processes inherit it): one
+# hardware queue per stream, see INTEGRATION.md
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

@@ -111,11 +111,12 @@ def failover_pair(comm, rank, world, nbytes, fault_chunk, restore_us=0):
     torch.cuda.synchronize()
     import time
     time.sleep(0.05)
-    if rank == 0:
-        ev = comm.switch_events()
-        out["switch_to"] = np.array([0 if e["to"] == "primary" else 1 for e in ev], np.int32)
-        out["resume"] = np.array([e["resume_chunk"] for e in ev], np.int32)
-        out["detect_ns"] = np.array([e["detect_ns"] for e in ev], np.int64)
+    # either endpoint may have issued the transfer (push by 0 or pull by 1),
+    # and the issuer's watchdog is the one that switches
+    ev = [e for e in comm.switch_events() if e["peer"] == 1 - rank]
+    out["switch_to"] = np.array([0 if e["to"] == "primary" else 1 for e in ev], np.int32)
+    out["resume"] = np.array([e["resume_chunk"] for e in ev], np.int32)
+    out["detect_ns"] = np.array([e["detect_ns"] for e in ev], np.int64)
     return out
 
 
