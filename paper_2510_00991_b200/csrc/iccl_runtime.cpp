@@ -229,9 +229,10 @@ struct OpDesc {
 
 struct ChunkRec {
   int stream = -1;  // index into Channel::stream table
-  cudaEvent_t ev = nullptr;  // recorded after the chunk: the WC the proxy polls
-  bool timed = false;        // ev is timing-enabled (monitor on, copy-engine path)
-  cudaEvent_t t1ev = nullptr;  // monitor: device event marking the chunk's start (not owned)
+  cudaEvent_t ev = nullptr;   // recorded after the chunk on its copy stream: the WC
+  cudaEvent_t tev = nullptr;  // monitor on, copy-engine path: timing event on the channel's
+                              // monitor stream right behind ev (the WC then; the chunk's t2)
+  cudaEvent_t t1ev = nullptr;  // monitor: timing event marking the chunk's start (not owned)
   uint64_t t1 = 0;
   int path = 0;
   int stamp = -1;
@@ -298,6 +299,8 @@ struct Channel {
   std::deque<Xfer> xfers;    // issued by this rank, in issue order
   std::vector<int> path_streams[2];
   int probe_stream = -1;
+  int mon_stream = -1;            // monitor timing events (kept off the copy streams)
+  cudaEvent_t bridge = nullptr;   // untimed event copy stream -> monitor stream (op anchors)
   // on the backup because the primary failed (watchdog + probe): only then
   // does monitor_failed_link probe the primary to switch back;
   // an API switch_qp is sticky until the next API switch
@@ -480,11 +483,11 @@ static cudaEvent_t get_tevent(iccl_comm* c) {
 
 static void put_events(iccl_comm* c, Xfer& x) {
   std::lock_guard<std::mutex> g(c->ev_mu);
-  for (ChunkRec& r : x.rec)
-    if (r.ev) {
-      (r.timed ? c->tevent_pool : c->event_pool).push_back(r.ev);
-      r.ev = nullptr;
-    }
+  for (ChunkRec& r : x.rec) {
+    if (r.ev) c->event_pool.push_back(r.ev);
+    if (r.tev) c->tevent_pool.push_back(r.tev);
+    r.ev = r.tev = nullptr;
+  }
   for (cudaEvent_t e : x.anchors) c->tevent_pool.push_back(e);
   x.anchors.clear();
   x.last_ev.clear();
@@ -750,11 +753,14 @@ static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
     if (r) return r;
     x.waited[path] |= bit;
     if (eng == ENG_CE && c->monitor_enabled.load(std::memory_order_relaxed)) {
-      // monitor anchor: the stream is released here, so an event at this point
-      // sits at a drain the copy pays anyway (no extra chunk boundary)
+      // monitor anchor (the op's start on this stream): an untimed event on
+      // the copy stream bridged to a timing event on the monitor stream
       cudaEvent_t a = get_tevent(c);
       x.anchors.push_back(a);
-      ICCL_CHECK_CUDA(cudaEventRecord(a, sc.s));
+      cudaStream_t ms = c->streams[chn.mon_stream].s;
+      ICCL_CHECK_CUDA(cudaEventRecord(chn.bridge, sc.s));
+      ICCL_CHECK_CUDA(cudaStreamWaitEvent(ms, chn.bridge, 0));
+      ICCL_CHECK_CUDA(cudaEventRecord(a, ms));
       x.last_ev.emplace_back(si, a);
     }
   }
@@ -775,11 +781,13 @@ static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
   rc.stamp = -1;
   // Monitor on, SM path: K1 itself stamps the chunk's WR/WC pair with
   // %globaltimer (K4 epilogue) and the t2 stamp doubles as the WC the proxy
-  // polls.  Copy-engine path: the WC is an event after the chunk — with the
-  // monitor on a timing event, whose device time (and the previous event on
-  // the stream, the chunk's start) give t1/t2 with no kernel at all, so the
-  // path stays at 0 SMs.  (A stream memop here would cost a full copy-engine
-  // drain per chunk: probes/p2p_probe3.)
+  // polls.  Copy-engine path: the WC is an untimed event after the chunk;
+  // with the monitor on, the channel's monitor stream waits for it and
+  // records a timing event, whose device time (and the previous one, the
+  // chunk's start) give t1/t2 with no kernel — the path stays at 0 SMs — and
+  // without a timing event between copies (2.7 us of copy-engine stall per
+  // chunk, profiles/r01/probe5b.txt).  A stream memop there would cost a full
+  // copy-engine drain per chunk (probes/p2p_probe3).
   const bool mon = c->monitor_enabled.load(std::memory_order_relaxed);
   KernelStamp* st = nullptr;
   if (mon && eng == ENG_SM) {
@@ -810,19 +818,21 @@ static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
   c->kernels_launched += eng == ENG_SM ? 1 : 0;
   c->bytes_issued += n;
   if (!st && eng != ENG_RELAY) {
-    const bool timed = mon && eng == ENG_CE;
-    if (rc.ev && rc.timed != timed) {
-      (rc.timed ? c->tevent_pool : c->event_pool).push_back(rc.ev);
-      rc.ev = nullptr;
-    }
-    if (!rc.ev) rc.ev = timed ? get_tevent(c) : get_event(c);
-    rc.timed = timed;
+    if (!rc.ev) rc.ev = get_event(c);
     ICCL_TRACE("event record");
     ICCL_CHECK_CUDA(cudaEventRecord(rc.ev, sc.s));
     ICCL_TRACE("event recorded");
-    if (timed) {
+    if (mon && eng == ENG_CE) {
+      if (!rc.tev) rc.tev = get_tevent(c);
+      cudaStream_t ms = c->streams[chn.mon_stream].s;
+      ICCL_CHECK_CUDA(cudaStreamWaitEvent(ms, rc.ev, 0));
+      ICCL_CHECK_CUDA(cudaEventRecord(rc.tev, ms));
       for (auto& le : x.last_ev)
-        if (le.first == si) le.second = rc.ev;
+        if (le.first == si) le.second = rc.tev;
+    } else if (rc.tev) {
+      std::lock_guard<std::mutex> g(c->ev_mu);
+      c->tevent_pool.push_back(rc.tev);
+      rc.tev = nullptr;
     }
   }
   iccl_result_t r = ICCL_SUCCESS;
@@ -951,9 +961,9 @@ static void record_monitor(iccl_comm* c, Channel& chn, Xfer& x, int k, uint64_t 
   iccl_mon_rec_t m{};
   m.t1_ns = rc.t1;
   m.t2_ns = t2_host;
-  if (rc.timed && rc.t1ev) {
+  if (rc.tev && rc.t1ev) {
     // copy-engine path: device times of the chunk's start / end events
-    uint64_t a = event_abs_ns(c, rc.t1ev), b = event_abs_ns(c, rc.ev);
+    uint64_t a = event_abs_ns(c, rc.t1ev), b = event_abs_ns(c, rc.tev);
     if (a && b && b >= a) {
       m.t1_ns = a;
       m.t2_ns = b;
@@ -961,10 +971,9 @@ static void record_monitor(iccl_comm* c, Channel& chn, Xfer& x, int k, uint64_t 
     // keep the float-ms elapsed time short: re-base once a second
     if (b > (uint64_t)c->base_abs_ns + 1000000000ull) {
       float ms = 0.f;
-      if (cudaEventElapsedTime(&ms, c->base_ev, rc.ev) == cudaSuccess) {
-        cudaEvent_t nb = rc.ev;  // ownership moves to the time base
-        rc.ev = nullptr;
-        rc.timed = false;
+      if (cudaEventElapsedTime(&ms, c->base_ev, rc.tev) == cudaSuccess) {
+        cudaEvent_t nb = rc.tev;  // ownership moves to the time base
+        rc.tev = nullptr;
         // a later chunk of this op may still name the old base as its start
         // event: recycle it only two re-bases (>= 2 s) later
         c->old_bases.push_back(c->base_ev);
@@ -1011,7 +1020,7 @@ static iccl_result_t progress_channel(iccl_comm* c, Channel& chn, bool* busy) {
       } else if (rc.stamp >= 0) {
         if (__atomic_load_n(&c->stamps[rc.stamp].t2, __ATOMIC_ACQUIRE) == 0) break;
       } else {
-        cudaError_t q = cudaEventQuery(rc.ev);
+        cudaError_t q = cudaEventQuery(rc.tev ? rc.tev : rc.ev);
         if (q == cudaErrorNotReady) break;
         if (q != cudaSuccess) {
           set_last_error(std::string("chunk completion: ") + cudaGetErrorString(q));
@@ -1686,6 +1695,9 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
       chn.path_streams[1].push_back(mk_stream(ENG_RELAY));
     }
     chn.probe_stream = mk_stream(ENG_CE);
+    chn.mon_stream = mk_stream(ENG_CE);
+    ICCL_CHECK_CUDA(cudaEventCreateWithFlags(&chn.bridge, cudaEventDisableTiming));
+    c->all_events.push_back(chn.bridge);
   }
   if (c->relay_buf) {
     c->relay_serve.assign(nranks, -1);

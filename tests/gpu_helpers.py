@@ -53,7 +53,20 @@ def _worker(rank, world, port, fn, outdir, kwargs):
 
 def run_ranks(world: int, fn, tmpdir, timeout: float = 120.0, **kwargs):
     """Run fn(comm, rank, world, **kwargs) -> dict of numpy arrays on `world`
-    GPUs, one process each; returns the per-rank dicts."""
+    GPUs, one process each; returns the per-rank dicts.  A rendezvous port
+    taken between free_port() and the bind is retried once."""
+    try:
+        return _run_ranks(world, fn, tmpdir, timeout, **kwargs)
+    except AssertionError as e:
+        if "EADDRINUSE" not in str(e):
+            raise
+        for f in os.listdir(str(tmpdir)):
+            if f.startswith("rank"):
+                os.remove(os.path.join(str(tmpdir), f))
+        return _run_ranks(world, fn, tmpdir, timeout, **kwargs)
+
+
+def _run_ranks(world: int, fn, tmpdir, timeout: float = 120.0, **kwargs):
     import torch.multiprocessing as mp
     port = free_port()
     ctx = mp.get_context("spawn")
