@@ -318,6 +318,10 @@ class Connection:
             x.last_progress = self.sim.now
         self.switches.append((self.sim.now, direction, resume, trigger))
         self.log("receiver", "switch_to_backup" if target == "Backup" else "switch_to_primary", resume)
+        if x:
+            # done == total: the retreat set acked := done, nothing to resend
+            # — the acks still in flight on the old QP are flushed
+            x.check_complete()
         if x and not x.complete:
             x.post_recvs()
             x.pump()

@@ -309,3 +309,19 @@ def test_AC3_fuzz_failover_exactly_once(size, fault_frac, chunk_pow, restore, se
     c = g.conns[(0, 1)]
     assert (out == src).all()
     assert c.delivered_sequence == list(range(tr.n_chunks(size, chunk)))
+
+
+def test_switch_back_after_last_chunk_completes():  # G15: done == total -> no retransmission
+    """Regression (found by the AC3 fuzz): the primary recovers and
+    monitor_failed_link switches back while the last chunks' acks are still in
+    flight on the backup; the retreat sets acked := done == total and the
+    transfer must complete instead of waiting for the flushed acks."""
+    size, chunk = 3_243_700, 1 << 17
+    wire = int(size / 900.0) + 2000
+    down = int(wire * 0.41201096553431754)
+    g = co.CommGroup(2, chunk_size=chunk, delta_ns=5_000, probe_period_ns=3_000,
+                     faults=FaultScript([(down, path_port(0, 1, 0), False), (down + wire, path_port(0, 1, 0), True)]))
+    src = np.random.default_rng(0).integers(0, 255, size, dtype=np.uint8)
+    out = co.send_recv(g, 0, 1, src)
+    assert (out == src).all()
+    assert g.conns[(0, 1)].delivered_sequence == list(range(tr.n_chunks(size, chunk)))
