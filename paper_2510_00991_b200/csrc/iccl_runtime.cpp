@@ -1361,8 +1361,10 @@ static iccl_result_t rzv_post(iccl_comm* c, const OpDesc& op, uint64_t wait_us) 
     sched_yield();
   }
   if (kind == 0 && peer != c->rank && wait_us > 0) {
-    const uint64_t deadline = now_ns() + wait_us * 1000ull;
+    const uint64_t t_wait = now_ns(), deadline = t_wait + wait_us * 1000ull;
     while (e.arrivals.load(std::memory_order_acquire) < 2 * g + 1 && now_ns() < deadline) sched_yield();
+    ICCL_TRACE("send %d->%d #%llu waited %.1f us for the CTS%s", c->rank, peer, (unsigned long long)k,
+               (now_ns() - t_wait) * 1e-3, e.arrivals.load() < 2 * g + 1 ? " (timed out)" : "");
   }
   RzvSide& mine = e.side[kind];
   mine.bytes = op.bytes;
@@ -1375,7 +1377,11 @@ static iccl_result_t rzv_post(iccl_comm* c, const OpDesc& op, uint64_t wait_us) 
     iccl_result_t r = export_buffer(c, op.src, &mine);
     if (r) return r;
   }
-  if (e.arrivals.fetch_add(1, std::memory_order_acq_rel) != 2 * g + 1) return ICCL_SUCCESS;  // first
+  if (e.arrivals.fetch_add(1, std::memory_order_acq_rel) != 2 * g + 1) {
+    ICCL_TRACE("%s %d->%d #%llu posted first", kind == 0 ? "send" : "recv", kind == 0 ? c->rank : peer,
+               kind == 0 ? peer : c->rank, (unsigned long long)k);
+    return ICCL_SUCCESS;  // first: the peer issues
+  }
   if (!rzv_claim(e, k)) return ICCL_SUCCESS;  // cannot happen: the first side never claims
   return rzv_issue(c, kind, peer, k, op.op_seq, false);
 }
