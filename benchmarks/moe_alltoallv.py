@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--impl", choices=["iccl", "nccl"], required=True)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--dump-records", action="store_true", help="monitor on; print rank 0's chunk records of one step")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -59,7 +60,7 @@ def main():
     comm = None
     if args.impl == "iccl":
         import paper_2510_00991_b200 as iccl
-        comm = iccl.init(rank, world, local, iccl.IcclConfig.defaults())
+        comm = iccl.init(rank, world, local, iccl.IcclConfig.defaults(monitor_enabled=args.dump_records))
 
     def step():
         if comm:
@@ -101,6 +102,21 @@ def main():
            "max_rank_egress_or_ingress_MiB": round(float(lim.item()) / 2**20, 1),
            "bit_exact_roundtrip": bool(okt.item() > 0), "send_rows_rank0": sc,
            "step": "dispatch alltoallv + combine alltoallv (same counts, reversed)"}
+    if comm and args.dump_records:
+        comm.monitor.drain()
+        torch.cuda.synchronize()
+        dist.barrier()
+        step()
+        torch.cuda.synchronize()
+        import time
+        time.sleep(0.01)
+        recs = comm.monitor.drain()
+        t0 = min(r.t1 for r in recs) if recs else 0
+        res[f"records_rank{rank}"] = [(r.peer, r.dir, r.op_seq, r.size >> 20, round((r.t1 - t0) / 1e3, 1),
+                                       round((r.t2 - t0) / 1e3, 1)) for r in recs]
+        for r_ in range(world):
+            if r_ == rank and rank != 0:
+                print(json.dumps({"rank": rank, "records": res[f"records_rank{rank}"]}), flush=True)
     if comm:
         s1 = comm.stats()
         res["kernels_launched"] = s1["kernels_launched"] - s0["kernels_launched"]

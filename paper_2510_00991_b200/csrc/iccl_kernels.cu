@@ -218,17 +218,23 @@ __global__ void __launch_bounds__(256) iccl_gather_rows(const int4* __restrict__
 // dst[pos[t*k + j]].  DRAM traffic = T rows read + T*k rows written, versus
 // T*k reads for the gather form (measured: the gather's re-reads miss L2,
 // profiles/r01/ncu/k2k3_full_summary.csv).
+// Each token row is split into `parts` column ranges, one warp each, so T
+// tokens give T * parts warps (a whole-row warp left ~1/3 of the warp slots
+// busy at T = 4096: ncu, profiles/r01/ncu/k2_expand_k3_summary.csv).
 __global__ void __launch_bounds__(256) iccl_expand_rows(const int4* __restrict__ src, int4* __restrict__ dst,
                                                        const int64_t* __restrict__ pos, int64_t n_src, int k,
-                                                       int64_t row16) {
+                                                       int64_t row16, int parts) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t t = warp; t < n_src; t += nwarps) {
+  const int64_t span = (row16 + parts - 1) / parts;
+  for (int64_t w = warp; w < n_src * parts; w += nwarps) {
+    const int64_t t = w / parts;
+    const int64_t c0 = (w % parts) * span, c1 = min(row16, c0 + span);
     const int4* s = src + t * row16;
     const int64_t* p = pos + t * k;
-    int64_t c = lane;
-    for (; c + 96 < row16; c += 128) {
+    int64_t c = c0 + lane;
+    for (; c + 96 < c1; c += 128) {
       const int4 v0 = ld_nc(s + c), v1 = ld_nc(s + c + 32), v2 = ld_nc(s + c + 64), v3 = ld_nc(s + c + 96);
       for (int j = 0; j < k; j++) {
         int4* d = dst + p[j] * row16;
@@ -238,7 +244,7 @@ __global__ void __launch_bounds__(256) iccl_expand_rows(const int4* __restrict__
         st_cs(d + c + 96, v3);
       }
     }
-    for (; c < row16; c += 32) {
+    for (; c < c1; c += 32) {
       const int4 v = ld_nc(s + c);
       for (int j = 0; j < k; j++) st_cs(dst + p[j] * row16 + c, v);
     }
@@ -441,8 +447,10 @@ cudaError_t launch_expand_rows(const void* src, void* dst, const int64_t* pos, i
                                int64_t row_bytes, int ctas, cudaStream_t st) {
   if (n_src == 0 || k == 0) return cudaSuccess;
   if ((row_bytes & 15) || ((uintptr_t)src & 15) || ((uintptr_t)dst & 15)) return cudaErrorInvalidValue;
-  iccl_expand_rows<<<rows_grid(n_src, ctas), 256, 0, st>>>((const int4*)src, (int4*)dst, pos, n_src, k,
-                                                           row_bytes / 16);
+  const int64_t row16 = row_bytes / 16;
+  const int parts = (int)max((int64_t)1, min((int64_t)8, row16 / 128));  // >= 4 int4 per lane per part
+  iccl_expand_rows<<<rows_grid(n_src * parts, ctas), 256, 0, st>>>((const int4*)src, (int4*)dst, pos, n_src, k,
+                                                                   row16, parts);
   return cudaGetLastError();
 }
 

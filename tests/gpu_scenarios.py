@@ -103,11 +103,12 @@ def failover_pair(comm, rank, world, nbytes, fault_chunk, restore_us=0):
     out = {}
     if rank == 0:
         comm.send(to_dev(src, dev), 1)
-    else:
+    elif rank == 1:
         r = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
         comm.recv(r, 0)
         torch.cuda.synchronize()
         out["recv"] = r.cpu().numpy()
+    # any other rank only takes part as a possible relay GPU
     torch.cuda.synchronize()
     import time
     time.sleep(0.05)
