@@ -120,7 +120,7 @@ typedef struct {
   int32_t peer;
   int32_t path;     /* ICCL_PATH_* */
   int32_t chunk;
-  int32_t dir;      /* 0 send */
+  int32_t dir;      /* 0: pushed by this rank to peer, 1: pulled by this rank from peer */
   uint64_t op_seq;
 } iccl_mon_rec_t;
 

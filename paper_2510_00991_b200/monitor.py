@@ -26,6 +26,7 @@ class MessageRecord:
     path: int = 0
     chunk: int = -1
     op_seq: int = 0
+    dir: int = 0  # 0: a transfer this rank pushed to `peer`, 1: one it pulled from `peer`
 
 
 @dataclass
@@ -127,7 +128,7 @@ class Monitor:
             for i in range(n.value):
                 r = buf[i]
                 got.append(MessageRecord(int(r.bytes), int(r.t1_ns), int(r.t2_ns), r.peer, r.path, r.chunk,
-                                         int(r.op_seq)))
+                                         int(r.op_seq), int(r.dir)))
             if n.value < 4096:
                 break
         self.records.extend(got)
