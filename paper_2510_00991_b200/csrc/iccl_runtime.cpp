@@ -214,7 +214,9 @@ struct UidBlob {
 static inline bool cyc_geq(uint32_t a, uint32_t b) { return (int32_t)(a - b) >= 0; }
 
 // ---------------------------------------------------------------- proxy-side structures
-enum Engine { ENG_CE = 0, ENG_SM = 1, ENG_RELAY = 2 };
+// ENG_CE_GROUP: the rank's one stream for the pushes of a group (alltoallv,
+// batch_isend_irecv) — see rzv_post.
+enum Engine { ENG_CE = 0, ENG_SM = 1, ENG_RELAY = 2, ENG_CE_GROUP = 3 };
 
 struct OpDesc {
   int kind;  // 0 send, 1 recv
@@ -260,7 +262,8 @@ struct Xfer {
   int next_issue = 0;  // sender posted == transmitted (chunks handed to an engine)
   int completed = 0;   // contiguous prefix observed delivered: acked == receiver done
   int path = 0;
-  uint32_t waited[2] = {0, 0};  // per path: stream bitmask that waited on the ready flags
+  std::vector<int> waited[2];  // per path: streams that already waited on the ready flags
+  bool group_stream = false;   // push of a group: the rank's shared group stream
   bool done_enqueued = false;
   bool eligible = false;
   uint64_t last_progress = 0;
@@ -675,8 +678,12 @@ static iccl_result_t serve_relays(iccl_comm* c, bool* busy) {
   return ICCL_SUCCESS;
 }
 
+static bool waited_on(const Xfer& x, int path, int si) {
+  return std::find(x.waited[path].begin(), x.waited[path].end(), si) != x.waited[path].end();
+}
+
 static int stream_for(iccl_comm* c, Channel& chn, int path, int engine, int k) {
-  // path_streams[path] holds [CE streams..., SM stream] — pick by engine
+  // path_streams[path] holds [CE streams..., SM stream (, relay) (, group)] — pick by engine
   std::vector<int>& v = chn.path_streams[path];
   std::vector<int> cand;
   for (int si : v)
@@ -740,18 +747,18 @@ static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
   const int eng = path_engine(c, chn, path, x.bytes);
   const size_t off = (size_t)k * x.chunk;
   const size_t n = std::min(x.chunk, x.bytes - off);
-  const int si = stream_for(c, chn, path, eng, k);
+  const int si = (eng == ENG_CE && x.group_stream) ? stream_for(c, chn, path, ENG_CE_GROUP, 0)
+                                                    : stream_for(c, chn, path, eng, k);
   StreamCtx& sc = c->streams[si];
-  const int bit = 1 << (si % 32);
   RankFlags* sender = flags_of(c, x.src_rank);
   RankFlags* receiver = flags_of(c, x.dst_rank);
-  if (!(x.waited[path] & bit)) {
+  if (!waited_on(x, path, si)) {
     // hostFunc#1 analog: the copy may start only once both user streams reached the op
     iccl_result_t r = memop_wait(sc.s, &sender->ready[x.s_slot], x.s_gen);
     if (r) return r;
     r = memop_wait(sc.s, &receiver->ready[x.r_ready_slot], x.r_ready_gen);
     if (r) return r;
-    x.waited[path] |= bit;
+    x.waited[path].push_back(si);
     if (eng == ENG_CE && c->monitor_enabled.load(std::memory_order_relaxed)) {
       // monitor anchor (the op's start on this stream): an untimed event on
       // the copy stream bridged to a timing event on the monitor stream
@@ -842,7 +849,7 @@ static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
     // both user streams.
     for (int p = 0; p < 2; p++) {
       for (int sj : chn.path_streams[p]) {
-        if (sj == si || !(x.waited[p] & (1 << (sj % 32)))) continue;
+        if (sj == si || !waited_on(x, p, sj)) continue;
         StreamCtx& o = c->streams[sj];
         ICCL_CHECK_CUDA(cudaEventRecord(o.ev, o.s));
         ICCL_CHECK_CUDA(cudaStreamWaitEvent(sc.s, o.ev, 0));
@@ -883,7 +890,7 @@ static iccl_result_t switch_path(iccl_comm* c, Channel& chn, int to, int trigger
     bool had_work = x.next_issue > x.completed || x.done_enqueued;
     if (had_work) {
       for (int sj : chn.path_streams[from]) {
-        if (!(x.waited[from] & (1 << (sj % 32)))) continue;
+        if (!waited_on(x, from, sj)) continue;
         cudaEvent_t fe;
         ICCL_CHECK_CUDA(cudaEventCreateWithFlags(&fe, cudaEventDisableTiming));
         ICCL_CHECK_CUDA(cudaEventRecord(fe, c->streams[sj].s));
@@ -1258,7 +1265,8 @@ static bool rzv_claim(RzvEntry& e, uint64_t k) {
 // streams' ready flags, the last one writes both done flags.  From the API
 // thread the transfer is handed to the proxy; from the proxy it is tracked
 // in place.
-static iccl_result_t rzv_issue(iccl_comm* c, int kind, int peer, uint64_t k, uint64_t op_seq, bool on_proxy) {
+static iccl_result_t rzv_issue(iccl_comm* c, int kind, int peer, uint64_t k, uint64_t op_seq, bool on_proxy,
+                               bool group = false) {
   RzvEntry& e = rzv_entry(c, kind, peer, k);
   const int src = kind == 0 ? c->rank : peer, dst = kind == 0 ? peer : c->rank;
   const RzvSide& snd = e.side[0];
@@ -1300,6 +1308,7 @@ static iccl_result_t rzv_issue(iccl_comm* c, int kind, int peer, uint64_t k, uin
   x.rec.resize(x.nchunks);
   x.path = pair_of(c, src, dst).active_path.load();
   x.last_progress = now_ns();
+  x.group_stream = group && kind == 0 && peer != c->rank;
   {
     std::lock_guard<std::mutex> gl(c->fault_mu);
     x.fault_ops_index = (int)(k - chn.fault_seq_base);
@@ -1343,7 +1352,15 @@ static iccl_result_t rzv_issue(iccl_comm* c, int kind, int peer, uint64_t k, uin
 // A send therefore first waits up to `wait_us` for the receiver's half to be
 // posted (receivers usually post early; inside a group every recv is posted
 // before any send), and only then posts its own.
-static iccl_result_t rzv_post(iccl_comm* c, const OpDesc& op, uint64_t wait_us) {
+//
+// The remote pushes of a group go to one stream, in call order: a GPU's copy
+// engine runs its peer copies one after another whatever stream they are on,
+// but in an order of its own — with one stream per peer, three senders of a
+// 4-rank alltoallv ended up pushing into the same receiver at once (incast,
+// each at half rate: MoE records, profiles/r01/README.md).  On one stream the
+// rotated order of iccl_alltoallv (step k: rank i -> i + k) holds, so at each
+// step every receiver has one sender.
+static iccl_result_t rzv_post(iccl_comm* c, const OpDesc& op, uint64_t wait_us, bool group = false) {
   const int peer = op.peer, kind = op.kind;
   const uint64_t k = kind == 0 ? c->pair_sends[peer]++ : c->pair_recvs[peer]++;
   RzvEntry& e = rzv_entry(c, kind, peer, k);
@@ -1383,7 +1400,7 @@ static iccl_result_t rzv_post(iccl_comm* c, const OpDesc& op, uint64_t wait_us) 
     return ICCL_SUCCESS;  // first: the peer issues
   }
   if (!rzv_claim(e, k)) return ICCL_SUCCESS;  // cannot happen: the first side never claims
-  return rzv_issue(c, kind, peer, k, op.op_seq, false);
+  return rzv_issue(c, kind, peer, k, op.op_seq, false, group);
 }
 
 // Stream markers of copy-engine ops: phase 0 = WriteValue(ready) for every
@@ -1662,6 +1679,8 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
     c->streams.push_back(sc);
     return (int)c->streams.size() - 1;
   };
+  // one stream for the remote pushes of a group, in call order (rzv_post)
+  const int group_si = mk_stream(ENG_CE_GROUP);
   std::vector<char*> peer_scratch(nranks, nullptr);
   for (int p = 0; p < nranks; p++) {
     if (p == rank) {
@@ -1699,6 +1718,10 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
           break;
         }
       chn.path_streams[1].push_back(mk_stream(ENG_RELAY));
+    }
+    if (chn.dir == 0 && p != rank) {
+      chn.path_streams[0].push_back(group_si);
+      chn.path_streams[1].push_back(group_si);
     }
     chn.probe_stream = mk_stream(ENG_CE);
     chn.mon_stream = mk_stream(ENG_CE);
@@ -1892,7 +1915,7 @@ iccl_result_t iccl_group_end(iccl_comm_t c) {
   for (auto& p : ops) {
     if (p.first.kind != 0 || p.first.ll) continue;
     const uint64_t t = now_ns();
-    iccl_result_t r = rzv_post(c, p.first, t < deadline ? (deadline - t) / 1000 : 0);
+    iccl_result_t r = rzv_post(c, p.first, t < deadline ? (deadline - t) / 1000 : 0, true);
     if (r) return r;
   }
   // one batched marker set per distinct stream
