@@ -86,7 +86,9 @@ typedef struct {
   uint64_t sm_small_bytes;    /* ICCL_SM_SMALL_BYTES  AUTO: messages <= this use the SM path    */
   int32_t proxy_cpu;          /* ICCL_PROXY_CPU       core to pin the proxy to, -1 = none        */
   int32_t relay_slot_mib;     /* ICCL_RELAY_SLOT_MIB  relay backup: staging slot per source (x2)  */
-  int32_t reserved[6];
+  int32_t direct_max_kib;     /* ICCL_DIRECT_MAX_KIB  AUTO: larger-than-LL messages up to this go
+                                                       the direct SM path (K6); 0 = off              */
+  int32_t reserved[5];
 } iccl_config_t;
 
 /* Six progress pointers of one transfer (Fig. 6). */

@@ -37,7 +37,8 @@ class Config(C.Structure):
         ("sm_small_bytes", C.c_uint64),
         ("proxy_cpu", C.c_int32),
         ("relay_slot_mib", C.c_int32),
-        ("reserved", C.c_int32 * 6),
+        ("direct_max_kib", C.c_int32),
+        ("reserved", C.c_int32 * 5),
     ]
 
 

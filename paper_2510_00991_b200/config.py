@@ -34,6 +34,7 @@ class IcclConfig:
     sm_small_bytes: int = 0
     proxy_cpu: int = -1
     relay_slot_mib: int = 0
+    direct_max_kib: int = 0
 
     @classmethod
     def defaults(cls, **overrides) -> "IcclConfig":
@@ -46,7 +47,7 @@ class IcclConfig:
                   backup_kind=inv_b.get(c.backup_kind, "sm"), transport=inv_t.get(c.transport, "auto"),
                   timeout_exponent=c.timeout_exponent, retry_count=c.retry_count, delta_us=c.delta_us,
                   probe_period_us=c.probe_period_us, sm_small_bytes=c.sm_small_bytes, proxy_cpu=c.proxy_cpu,
-                  relay_slot_mib=c.relay_slot_mib)
+                  relay_slot_mib=c.relay_slot_mib, direct_max_kib=c.direct_max_kib)
         names = {f.name for f in fields(cls)}
         for k, v in overrides.items():
             if k not in names:
@@ -72,6 +73,7 @@ class IcclConfig:
         c.sm_small_bytes = int(self.sm_small_bytes)
         c.proxy_cpu = int(self.proxy_cpu)
         c.relay_slot_mib = int(self.relay_slot_mib)
+        c.direct_max_kib = int(self.direct_max_kib)
         return c
 
     def validate(self) -> "IcclConfig":

@@ -108,6 +108,7 @@ iccl_result_t iccl_config_init(iccl_config_t* c) {
   c->sm_small_bytes = 256 * 1024;  // AUTO: <= 256 KiB between GPUs takes the LL kernel path (K5): 8-16 us vs ~21 us on the copy-engine chain
   c->proxy_cpu = -1;
   c->relay_slot_mib = 32;        // relay backup: 2 x 32 MiB staging per source on the relay GPU
+  c->direct_max_kib = 16 * 1024; // AUTO: 256 KiB < n <= 16 MiB take the direct SM path (K6)
   uint64_t u;
   int32_t i;
   if (env_u64("ICCL_CHUNK_BYTES", &u)) c->chunk_bytes = u;
@@ -125,6 +126,7 @@ iccl_result_t iccl_config_init(iccl_config_t* c) {
   if (env_u64("ICCL_SM_SMALL_BYTES", &u)) c->sm_small_bytes = u;
   if (env_i32("ICCL_PROXY_CPU", &i)) c->proxy_cpu = i;
   if (env_i32("ICCL_RELAY_SLOT_MIB", &i)) c->relay_slot_mib = i;
+  if (env_i32("ICCL_DIRECT_MAX_KIB", &i)) c->direct_max_kib = i;
   return ICCL_SUCCESS;
 }
 
@@ -146,6 +148,7 @@ iccl_result_t iccl_config_validate(const iccl_config_t* c) {
   ICCL_RETURN_IF(c->probe_period_us == 0, ICCL_ERR_INVALID_CONFIG, "probe period must be > 0");
   ICCL_RETURN_IF(c->relay_slot_mib < 1 || c->relay_slot_mib > 1024, ICCL_ERR_INVALID_CONFIG,
                  "relay_slot_mib must be in [1, 1024]");
+  ICCL_RETURN_IF(c->direct_max_kib < 0, ICCL_ERR_INVALID_CONFIG, "direct_max_kib must be >= 0");
   return ICCL_SUCCESS;
 }
 

@@ -64,6 +64,22 @@ struct alignas(64) KernelStamp {
 // with at most `ctas` CTAs; TMA bulk body + vector head/tail.  `stamp` may be
 // null.
 cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, KernelStamp* stamp, cudaStream_t st);
+// K6: direct zero-copy of a mid-size message by the side that arrived second
+// at the rendezvous, on its own user stream (see rzv_post).
+struct DirectOp {
+  const char* src;
+  char* dst;
+  size_t head, body, tail;          // filled by launch_direct
+  const uint32_t* peer_ready;       // the other side's ready flag (host-mapped control block)
+  uint32_t peer_ready_gen;
+  uint32_t* peer_done;              // the other side's done flag
+  uint32_t peer_done_gen;
+  uint32_t* my_done;                // this side's done flag (request bookkeeping)
+  uint32_t my_done_gen;
+  unsigned int* counter;            // CTA arrival counter (0 between uses)
+  unsigned int* error;              // host-mapped: set to 1 if the wait timed out
+};
+cudaError_t launch_direct(DirectOp op, size_t bytes, int ctas, cudaStream_t st);
 // Force-load every kernel (see iccl_kernels.cu: lazy loading vs parked streams).
 cudaError_t preload_kernels();
 // K5: low-latency (LL) eager path for small and mid-size messages.  8-byte

@@ -84,16 +84,13 @@ __device__ __forceinline__ void copy_vec16(const int4* __restrict__ src, int4* _
   for (; i < n16; i += nthreads) dst[i] = src[i];
 }
 
-// K1.  src/dst share the same alignment mod 16 (checked by the launcher);
-// [0, head) and [head + body, n) are copied with byte loads by warp 1..3,
-// the 16 B-aligned body by the TMA ring driven from thread 0.
-__global__ void __launch_bounds__(kCopyThreads) iccl_copy_tma(const char* __restrict__ src, char* __restrict__ dst,
-                                                              size_t head, size_t body, size_t tail,
-                                                              KernelStamp* stamp) {
-  extern __shared__ __align__(128) char smem[];
-  __shared__ __align__(8) uint64_t mbar[kStages];
-  stamp_begin(stamp);
-  // heads and tails (< 16 bytes each) by the non-elected threads of CTA 0
+// The TMA ring of one CTA: tiles blockIdx.x, blockIdx.x + gridDim.x, ... of
+// the 16 B-aligned body, global -> smem (cp.async.bulk + mbarrier
+// complete_tx) -> global (bulk_group), kStages stages in flight, driven by
+// thread 0; the < 16 B head and tail go with byte loads by warps 1..3 of
+// CTA 0.  All bulk stores are complete (visible) when it returns.
+__device__ __forceinline__ void tma_copy(const char* __restrict__ src, char* __restrict__ dst, size_t head,
+                                         size_t body, size_t tail, char* smem, uint64_t* mbar) {
   if (blockIdx.x == 0 && threadIdx.x >= 32) {
     copy_bytes(src, dst, head, threadIdx.x - 32, blockDim.x - 32);
     copy_bytes(src + head + body, dst + head + body, tail, threadIdx.x - 32, blockDim.x - 32);
@@ -142,10 +139,53 @@ __global__ void __launch_bounds__(kCopyThreads) iccl_copy_tma(const char* __rest
         issue_load(j + kStages);
       }
     }
-    // all bulk stores complete (visible) before the CTA retires
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
+}
+
+// K1.  src/dst share the same alignment mod 16 (checked by the launcher).
+__global__ void __launch_bounds__(kCopyThreads) iccl_copy_tma(const char* __restrict__ src, char* __restrict__ dst,
+                                                              size_t head, size_t body, size_t tail,
+                                                              KernelStamp* stamp) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(8) uint64_t mbar[kStages];
+  stamp_begin(stamp);
+  tma_copy(src, dst, head, body, tail, smem, mbar);
   stamp_end(stamp);
+}
+
+// K6: the direct path for mid-size messages.  Launched on the issuing
+// side's own user stream by the side that arrived second at the rendezvous
+// (no proxy, no side stream, no stream memop on this side): every CTA waits
+// for the other side's ready flag (its user stream reached the op), moves its
+// tiles straight between the two tensors (push or pull, zero-copy), and the
+// last CTA releases both done flags.  Waits give up after 10 s (error flag).
+__global__ void __launch_bounds__(kCopyThreads) iccl_direct_copy(DirectOp op) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(8) uint64_t mbar[kStages];
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = globaltimer();
+    uint32_t v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(op.peer_ready) : "memory");
+      if ((int32_t)(v - op.peer_ready_gen) < 0 && globaltimer() - t0 > 10000000000ull) {
+        *op.error = 1;
+        break;
+      }
+    } while ((int32_t)(v - op.peer_ready_gen) < 0);
+  }
+  __syncthreads();
+  tma_copy(op.src, op.dst, op.head, op.body, op.tail, smem, mbar);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    if (atomicAdd(op.counter, 1u) == gridDim.x - 1) {
+      atomicExch(op.counter, 0u);
+      __threadfence_system();
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(op.peer_done), "r"(op.peer_done_gen) : "memory");
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(op.my_done), "r"(op.my_done_gen) : "memory");
+    }
+  }
 }
 
 // Fallback for buffers whose addresses differ mod 16: byte copy.
@@ -369,6 +409,19 @@ cudaError_t launch_ll(const LLBatch& b, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+cudaError_t launch_direct(DirectOp op, size_t bytes, int ctas, cudaStream_t st) {
+  const uintptr_t s = (uintptr_t)op.src, d = (uintptr_t)op.dst;
+  if (((s ^ d) & 15) != 0) return cudaErrorInvalidValue;  // caller routes mutually misaligned pairs elsewhere
+  op.head = (16 - (s & 15)) & 15;
+  if (op.head > bytes) op.head = bytes;
+  op.body = (bytes - op.head) & ~(size_t)15;
+  op.tail = bytes - op.head - op.body;
+  const size_t ntiles = (op.body + kTile - 1) / kTile;
+  int grid = (int)min((size_t)ctas, ntiles > 0 ? ntiles : (size_t)1);
+  iccl_direct_copy<<<grid < 1 ? 1 : grid, kCopyThreads, kStages * kTile, st>>>(op);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, KernelStamp* stamp, cudaStream_t st) {
   if (bytes == 0) return cudaSuccess;
   const uintptr_t s = (uintptr_t)src, d = (uintptr_t)dst;
@@ -401,7 +454,7 @@ cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, Kern
 // iccl_comm_init_rank calls this before any wait is enqueued.
 cudaError_t preload_kernels() {
   cudaFuncAttributes a;
-  const void* fns[] = {(const void*)iccl_copy_tma,   (const void*)iccl_copy_unaligned, (const void*)iccl_stamp,
+  const void* fns[] = {(const void*)iccl_copy_tma, (const void*)iccl_direct_copy,   (const void*)iccl_copy_unaligned, (const void*)iccl_stamp,
                        (const void*)iccl_read_globaltimer, (const void*)iccl_gather_rows,
                        (const void*)iccl_scatter_rows, (const void*)iccl_expand_rows,
                        (const void*)iccl_ll_group};
@@ -411,6 +464,8 @@ cudaError_t preload_kernels() {
   }
   if (!smem_configured) {
     cudaError_t e = cudaFuncSetAttribute(iccl_copy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kStages * kTile);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(iccl_direct_copy, cudaFuncAttributeMaxDynamicSharedMemorySize, kStages * kTile);
     if (e != cudaSuccess) return e;
     smem_configured = true;
   }

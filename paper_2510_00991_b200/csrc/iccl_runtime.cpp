@@ -227,6 +227,9 @@ struct OpDesc {
   uint64_t op_seq;
   bool ll = false;   // small message on the LL kernel path (K5)
   uint32_t ll_seq = 0;
+  bool direct = false;   // mid-size message: the side arriving second runs K6 on its user stream
+  bool issued_direct = false;  // ... and that side is this one: K6 replaces this op's stream markers
+  DirectOp dop{};        // K6 parameters when issued_direct
 };
 
 struct ChunkRec {
@@ -374,6 +377,7 @@ struct iccl_comm {
   std::vector<char*> peer_scratch_base;                       // IPC-opened peer scratch blocks
   int group_depth = 0;
   std::vector<std::pair<OpDesc, cudaStream_t>> group_ops;
+  int direct_ctas = 32;  // K6 grid (>= 16 CTAs keep NVLink busy, kernels bench)
   std::unordered_map<uint64_t, cudaIpcMemHandle_t> export_cache;
   // proxy
   std::vector<Channel> ch;  // 2 per peer: [2 * peer + dir]
@@ -1187,7 +1191,7 @@ static void proxy_loop(iccl_comm* c) {
     }
     if (c->hdr->abort.load()) set_async(c, ICCL_ERR_ABORTED, "communicator aborted");
     if (c->ll_error && __atomic_load_n(c->ll_error, __ATOMIC_ACQUIRE))
-      set_async(c, ICCL_ERR_TIMEOUT, "LL kernel wait exceeded 10 s (peer never posted the matching op)");
+      set_async(c, ICCL_ERR_TIMEOUT, "LL / direct kernel wait exceeded 10 s (peer never posted the matching op)");
     if (busy) {
       idle_since = now_ns();
     } else {
@@ -1360,7 +1364,7 @@ static iccl_result_t rzv_issue(iccl_comm* c, int kind, int peer, uint64_t k, uin
 // each at half rate: MoE records, profiles/r01/README.md).  On one stream the
 // rotated order of iccl_alltoallv (step k: rank i -> i + k) holds, so at each
 // step every receiver has one sender.
-static iccl_result_t rzv_post(iccl_comm* c, const OpDesc& op, uint64_t wait_us, bool group = false) {
+static iccl_result_t rzv_post(iccl_comm* c, OpDesc& op, uint64_t wait_us, bool group = false) {
   const int peer = op.peer, kind = op.kind;
   const uint64_t k = kind == 0 ? c->pair_sends[peer]++ : c->pair_recvs[peer]++;
   RzvEntry& e = rzv_entry(c, kind, peer, k);
@@ -1400,7 +1404,46 @@ static iccl_result_t rzv_post(iccl_comm* c, const OpDesc& op, uint64_t wait_us, 
     return ICCL_SUCCESS;  // first: the peer issues
   }
   if (!rzv_claim(e, k)) return ICCL_SUCCESS;  // cannot happen: the first side never claims
+  if (op.direct) {
+    const RzvSide& other = e.side[kind ^ 1];
+    // K6's TMA ring needs both tensors at the same alignment mod 16 (an IPC
+    // mapping is page-aligned, so the peer's offset decides); else the copy
+    // engine path below takes it
+    if (((uintptr_t)op.src & 15) == (other.base_offset & 15) && e.side[0].bytes == e.side[1].bytes) {
+      char* mapped = nullptr;
+      Channel& chn = c->ch[2 * peer + kind];
+      iccl_result_t r = open_peer_buffer(c, chn, other, &mapped);
+      if (r) return r;
+      DirectOp& d = op.dop;
+      d.src = kind == 0 ? op.src : mapped;
+      d.dst = kind == 0 ? mapped : (char*)op.src;
+      d.peer_ready = &flags_of(c, peer)->ready[other.slot];
+      d.peer_ready_gen = other.gen;
+      d.peer_done = &flags_of(c, peer)->done[other.slot];
+      d.peer_done_gen = other.gen;
+      d.my_done = &flags_of(c, c->rank)->done[op.slot];
+      d.my_done_gen = op.gen;
+      d.counter = c->ll_counters + (c->ll_ctr_next++ % kLLCounters);
+      d.error = c->ll_error;
+      op.issued_direct = true;
+      ICCL_TRACE("direct %s pair %d->%d #%llu, %zu B", kind == 0 ? "push" : "pull", kind == 0 ? c->rank : peer,
+                 kind == 0 ? peer : c->rank, (unsigned long long)k, op.bytes);
+      return ICCL_SUCCESS;
+    }
+  }
   return rzv_issue(c, kind, peer, k, op.op_seq, false, group);
+}
+
+// K6 for every op of `ops` this side issues directly, on stream s.
+static iccl_result_t launch_direct_ops(iccl_comm* c, cudaStream_t s, const std::vector<OpDesc>& ops) {
+  for (const OpDesc& op : ops) {
+    if (!op.issued_direct) continue;
+    ICCL_CHECK_CUDA(launch_direct(op.dop, op.bytes, c->direct_ctas, s));
+    c->kernels_launched += 1;
+    c->copies_issued += 1;
+    c->bytes_issued += op.bytes;
+  }
+  return ICCL_SUCCESS;
 }
 
 // Stream markers of copy-engine ops: phase 0 = WriteValue(ready) for every
@@ -1514,6 +1557,8 @@ static iccl_result_t enqueue_op(iccl_comm* c, int kind, const void* buf, size_t 
   // count, so the k-th LL send of a pair always meets the k-th LL recv.
   op.ll = peer != c->rank && c->cfg.transport != ICCL_TRANSPORT_CE && bytes <= c->cfg.sm_small_bytes &&
           bytes <= kLLMaxBytes && c->ll_region != nullptr;
+  op.direct = !op.ll && peer != c->rank && c->cfg.transport == ICCL_TRANSPORT_AUTO &&
+              bytes <= (size_t)c->cfg.direct_max_kib * 1024;
   if (op.ll) {
     op.ll_seq = kind == 0 ? ++c->ll_sent[peer] : ++c->ll_recvd[peer];
   } else if (kind == 1 || c->group_depth == 0) {
@@ -1527,6 +1572,7 @@ static iccl_result_t enqueue_op(iccl_comm* c, int kind, const void* buf, size_t 
     return ICCL_SUCCESS;
   }
   if (op.ll) return launch_ll_ops(c, s, {op});
+  if (op.issued_direct) return launch_direct_ops(c, s, {op});
   return stream_markers(c, s, {op});
 }
 
@@ -1918,17 +1964,22 @@ iccl_result_t iccl_group_end(iccl_comm_t c) {
     iccl_result_t r = rzv_post(c, p.first, t < deadline ? (deadline - t) / 1000 : 0, true);
     if (r) return r;
   }
+  // per stream: ready markers of the ops waiting on a peer (copy engine, or
+  // K6 run by the peer), then the kernels (LL, K6 this side runs), then the
+  // done waits — no kernel of ours ever sits in front of a ready flag a peer
+  // needs
   // one batched marker set per distinct stream
   std::vector<cudaStream_t> order;
   for (auto& p : ops)
     if (std::find(order.begin(), order.end(), p.second) == order.end()) order.push_back(p.second);
   for (cudaStream_t s : order) {
-    std::vector<OpDesc> ce, ll;
+    std::vector<OpDesc> ce, ll, direct;
     for (auto& p : ops)
-      if (p.second == s) (p.first.ll ? ll : ce).push_back(p.first);
+      if (p.second == s) (p.first.ll ? ll : p.first.issued_direct ? direct : ce).push_back(p.first);
     iccl_result_t r = ICCL_SUCCESS;
     if (!ce.empty()) r = stream_markers(c, s, ce, 1);  // ready
     if (!r && !ll.empty()) r = launch_ll_ops(c, s, ll);
+    if (!r && !direct.empty()) r = launch_direct_ops(c, s, direct);
     if (!r && !ce.empty()) r = stream_markers(c, s, ce, 2);  // done waits
     if (r) return r;
   }

@@ -144,3 +144,37 @@ def relay_ring(comm, rank, world, nbytes, iters=2):
     torch.cuda.synchronize()
     out["recv_back"] = dst.cpu().numpy()
     return out
+
+
+def direct_mixed(comm, rank, world, sizes, rounds=2):
+    """Mid-size messages (the direct K6 path) both ways in one group per round,
+    mixed with an LL and a copy-engine message, then as single ordered ops."""
+    from paper_2510_00991_b200 import P2POp
+    dev = torch.device("cuda", rank)
+    peer = 1 - rank
+    out = {}
+    for rd in range(rounds):
+        ops, recvs = [], []
+        for i, n in enumerate(sizes):
+            s = to_dev(payload(n, seed=20_000 * rank + 100 * rd + i), dev)
+            r = torch.zeros(n + 16, dtype=torch.uint8, device=dev)[16:]
+            ops += [P2POp("irecv", r, peer), P2POp("isend", s, peer)] if rank else \
+                   [P2POp("isend", s, peer), P2POp("irecv", r, peer)]
+            recvs.append(r)
+        comm.batch_isend_irecv(ops)
+        torch.cuda.synchronize()
+        for i, r in enumerate(recvs):
+            out[f"r{rd}_{i}"] = r.cpu().numpy()
+    for i, n in enumerate(sizes):
+        s = to_dev(payload(n, seed=777 + i), dev)
+        r = torch.zeros(n, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            comm.send(s, 1)
+            comm.recv(r, 1)
+        else:
+            comm.recv(r, 0)
+            comm.send(s, 0)
+        torch.cuda.synchronize()
+        out[f"single_{i}"] = r.cpu().numpy()
+    out["kernels"] = np.array([comm.stats()["kernels_launched"]], np.int64)
+    return out

@@ -340,3 +340,21 @@ def test_relay_ring_api_switch(need_gpus, tmp_path):
             assert np.array_equal(res[r][f"recv{it}"], payload(n, seed=70 + 10 * it + frm))
         assert np.array_equal(res[r]["recv_back"], payload(n, seed=90 + frm))
         assert int(res[r]["path"][0]) == 1
+
+
+def test_pair_direct_mid_size(need_gpus, tmp_path):
+    """256 KiB < n <= 16 MiB: the side that arrives second runs K6 on its own
+    stream (push or pull, zero-copy), bit-exact in groups and single ops."""
+    need_gpus(2)
+    import gpu_scenarios as sc
+    MiB_ = 1 << 20
+    sizes = [300 * 1024 + 5, MiB_, 3 * MiB_ + 7, 16 * MiB_, 1000, 40 * MiB_]
+    res = run_ranks(2, sc.direct_mixed, tmp_path, sizes=sizes)
+    for r in range(2):
+        peer = 1 - r
+        for rd in range(2):
+            for i, n in enumerate(sizes):
+                assert np.array_equal(res[r][f"r{rd}_{i}"], payload(n, seed=20_000 * peer + 100 * rd + i)), (r, rd, n)
+        for i, n in enumerate(sizes):
+            assert np.array_equal(res[r][f"single_{i}"], payload(n, seed=777 + i))
+    assert int(res[0]["kernels"][0]) + int(res[1]["kernels"][0]) > 0  # K6 / LL ran
