@@ -349,7 +349,7 @@ def test_pair_direct_mid_size(need_gpus, tmp_path):
     import gpu_scenarios as sc
     MiB_ = 1 << 20
     sizes = [300 * 1024 + 5, MiB_, 3 * MiB_ + 7, 16 * MiB_, 1000, 40 * MiB_]
-    res = run_ranks(2, sc.direct_mixed, tmp_path, sizes=sizes)
+    res = run_ranks(2, sc.direct_mixed, tmp_path, sizes=sizes, config=dict(direct_max_kib=16 * 1024))
     for r in range(2):
         peer = 1 - r
         for rd in range(2):
