@@ -77,6 +77,7 @@ struct DirectOp {
   uint32_t* my_done;                // this side's done flag (request bookkeeping)
   uint32_t my_done_gen;
   unsigned int* counter;            // CTA arrival counter (0 between uses)
+  unsigned int* go;                 // CTA 0 -> other CTAs: the peer is ready (device memory, gen-tagged)
   unsigned int* error;              // host-mapped: set to 1 if the wait timed out
 };
 cudaError_t launch_direct(DirectOp op, size_t bytes, int ctas, cudaStream_t st);

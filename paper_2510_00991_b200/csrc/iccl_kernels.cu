@@ -163,16 +163,30 @@ __global__ void __launch_bounds__(kCopyThreads) iccl_copy_tma(const char* __rest
 __global__ void __launch_bounds__(kCopyThreads) iccl_direct_copy(DirectOp op) {
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) uint64_t mbar[kStages];
+  // one thread of CTA 0 polls the host-mapped ready flag; the other CTAs
+  // wait on a word in this GPU's memory that it releases (gen-tagged, never
+  // reset), so only one poller crosses PCIe
   if (threadIdx.x == 0) {
     const unsigned long long t0 = globaltimer();
     uint32_t v;
-    do {
-      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(op.peer_ready) : "memory");
-      if ((int32_t)(v - op.peer_ready_gen) < 0 && globaltimer() - t0 > 10000000000ull) {
-        *op.error = 1;
-        break;
-      }
-    } while ((int32_t)(v - op.peer_ready_gen) < 0);
+    if (blockIdx.x == 0) {
+      do {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(op.peer_ready) : "memory");
+        if ((int32_t)(v - op.peer_ready_gen) < 0 && globaltimer() - t0 > 10000000000ull) {
+          *op.error = 1;
+          break;
+        }
+      } while ((int32_t)(v - op.peer_ready_gen) < 0);
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(op.go), "r"(op.my_done_gen) : "memory");
+    } else {
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(op.go) : "memory");
+        if (v != op.my_done_gen && globaltimer() - t0 > 10000000000ull) {
+          *op.error = 1;
+          break;
+        }
+      } while (v != op.my_done_gen);
+    }
   }
   __syncthreads();
   tma_copy(op.src, op.dst, op.head, op.body, op.tail, smem, mbar);

@@ -1424,6 +1424,7 @@ static iccl_result_t rzv_post(iccl_comm* c, OpDesc& op, uint64_t wait_us, bool g
       d.my_done = &flags_of(c, c->rank)->done[op.slot];
       d.my_done_gen = op.gen;
       d.counter = c->ll_counters + (c->ll_ctr_next++ % kLLCounters);
+      d.go = c->ll_counters + kLLCounters + (op.slot % kLLCounters);
       d.error = c->ll_error;
       op.issued_direct = true;
       ICCL_TRACE("direct %s pair %d->%d #%llu, %zu B", kind == 0 ? "push" : "pull", kind == 0 ? c->rank : peer,
@@ -1673,8 +1674,9 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
     ICCL_CHECK_CUDA(cudaMemset(c->ll_region, 0, ll_bytes));
     ICCL_CHECK_CUDA(cudaIpcGetMemHandle(&me.ll_handle, c->ll_region));
     c->ll_error = (unsigned int*)((char*)c->pinned + 56 * 1024);
-    ICCL_CHECK_CUDA(cudaMalloc((void**)&c->ll_counters, kLLCounters * sizeof(unsigned int)));
-    ICCL_CHECK_CUDA(cudaMemset(c->ll_counters, 0, kLLCounters * sizeof(unsigned int)));
+    // kLLCounters arrival counters + kLLCounters K6 go words
+    ICCL_CHECK_CUDA(cudaMalloc((void**)&c->ll_counters, 2 * kLLCounters * sizeof(unsigned int)));
+    ICCL_CHECK_CUDA(cudaMemset(c->ll_counters, 0, 2 * kLLCounters * sizeof(unsigned int)));
     c->ll_sent.assign(nranks, 0);
     c->ll_recvd.assign(nranks, 0);
     c->peer_ll.assign(nranks, nullptr);
