@@ -108,7 +108,7 @@ iccl_result_t iccl_config_init(iccl_config_t* c) {
   c->sm_small_bytes = 256 * 1024;  // AUTO: <= 256 KiB between GPUs takes the LL kernel path (K5): 8-16 us vs ~21 us on the copy-engine chain
   c->proxy_cpu = -1;
   c->relay_slot_mib = 32;        // relay backup: 2 x 32 MiB staging per source on the relay GPU
-  c->direct_max_kib = 0;         // direct SM path (K6) off by default: 40 us at 1-8 MiB, slower than the copy-engine chain
+  c->direct_max_kib = 16 * 1024; // AUTO: 256 KiB < n <= 16 MiB take the direct SM path (K6): 18-40 us vs 22-48 us on the copy-engine chain
   uint64_t u;
   int32_t i;
   if (env_u64("ICCL_CHUNK_BYTES", &u)) c->chunk_bytes = u;
