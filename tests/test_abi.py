@@ -125,6 +125,24 @@ def test_config_defaults_and_env_override():
     assert out.stdout.split() == [str(8 << 20), "12", "3", "32", "sm"], out.stderr
 
 
+def test_path_selection_defaults_and_overrides():
+    """The size classes of the data path: LL (K5) <= 256 KiB < direct (K6)
+    <= 16 MiB < copy engines; relay staging 32 MiB; each an ICCL_* knob."""
+    import paper_2510_00991_b200 as p
+    d = p.IcclConfig.defaults()
+    assert (d.sm_small_bytes, d.direct_max_kib, d.relay_slot_mib, d.backup_kind) == (256 * 1024, 16 * 1024, 32, "sm")
+    code = ("import paper_2510_00991_b200 as p; c=p.IcclConfig.defaults(); "
+            "print(c.sm_small_bytes, c.direct_max_kib, c.relay_slot_mib, c.backup_kind)")
+    env = dict(os.environ, ICCL_SM_SMALL_BYTES="4096", ICCL_DIRECT_MAX_KIB="0", ICCL_RELAY_SLOT_MIB="8",
+               ICCL_BACKUP="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=ROOT, capture_output=True, text=True)
+    assert out.stdout.split() == ["4096", "0", "8", "relay"], out.stderr
+    with pytest.raises(p.InvalidConfig):
+        p.IcclConfig.defaults(direct_max_kib=-1).validate()
+    with pytest.raises(p.InvalidConfig):
+        p.IcclConfig.defaults(relay_slot_mib=0).validate()
+
+
 def test_config_validation():
     import paper_2510_00991_b200 as p
     with pytest.raises(p.InvalidConfig):
