@@ -116,6 +116,18 @@ def main():
             rec[f"{mode}_GBps"] = round(n / per_op / 1e3, 2)
             rec[f"{mode}_lat_us"] = round(lat, 3)
         torch.cuda.synchronize()
+        if comm:
+            # SMs used: CTAs the library launched per 0->1 transfer, both ranks summed
+            st0 = comm.stats()
+            for _ in range(4):
+                bw_loop(s, r)()
+            torch.cuda.synchronize()
+            st1 = comm.stats()
+            d = torch.tensor([st1["ctas_launched"] - st0["ctas_launched"],
+                              st1["kernels_launched"] - st0["kernels_launched"]], device=dev, dtype=torch.float64)
+            dist.all_reduce(d)
+            rec["ctas_per_op"] = float(d[0].item()) / 4
+            rec["kernels_per_op"] = float(d[1].item()) / 4
         if rank == 1:
             ok = torch.equal(rbuf[:n], buf[:n])
             okt = torch.tensor([1 if ok else 0], device=dev)

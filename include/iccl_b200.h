@@ -158,13 +158,15 @@ iccl_result_t iccl_comm_get_async_error(iccl_comm_t comm, iccl_result_t* err);
 /* opCount of every rank, read from the shared control block. */
 iccl_result_t iccl_comm_op_counts(iccl_comm_t comm, uint64_t* counts, int n);
 
-/* Counters of the work this rank's proxy issued (SURVEY.md §5 metrics): SM
- * kernels launched (K1 copies, K4 stamps), copy-engine copies, payload bytes. */
+/* Counters of the work this rank issued (SURVEY.md §5 metrics): SM kernels
+ * launched (K1 backup copies, K5 LL, K6 direct) and their CTAs, copy-engine
+ * copies, payload bytes. */
 typedef struct {
   uint64_t kernels_launched;
   uint64_t copies_issued;
   uint64_t bytes_issued;
-  uint64_t reserved[5];
+  uint64_t ctas_launched;  /* CTAs of those kernels (the "SMs used" of the SM paths) */
+  uint64_t reserved[4];
 } iccl_stats_t;
 iccl_result_t iccl_comm_stats(iccl_comm_t comm, iccl_stats_t* stats);
 

@@ -75,7 +75,7 @@ class SwitchEvent(C.Structure):
 
 class Stats(C.Structure):
     _fields_ = [("kernels_launched", C.c_uint64), ("copies_issued", C.c_uint64), ("bytes_issued", C.c_uint64),
-                ("reserved", C.c_uint64 * 5)]
+                ("ctas_launched", C.c_uint64), ("reserved", C.c_uint64 * 4)]
 
 
 _c = C.c_int  # iccl_result_t

@@ -63,7 +63,8 @@ struct alignas(64) KernelStamp {
 // K1: copy `bytes` from src to dst (dst may be an IPC-mapped peer pointer)
 // with at most `ctas` CTAs; TMA bulk body + vector head/tail.  `stamp` may be
 // null.
-cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, KernelStamp* stamp, cudaStream_t st);
+cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, KernelStamp* stamp, cudaStream_t st,
+                        int* grid_out = nullptr);
 // K6: direct zero-copy of a mid-size message by the side that arrived second
 // at the rendezvous, on its own user stream (see rzv_post).
 struct DirectOp {
@@ -80,7 +81,7 @@ struct DirectOp {
   unsigned int* go;                 // CTA 0 -> other CTAs: the peer is ready (device memory, gen-tagged)
   unsigned int* error;              // host-mapped: set to 1 if the wait timed out
 };
-cudaError_t launch_direct(DirectOp op, size_t bytes, int ctas, cudaStream_t st);
+cudaError_t launch_direct(DirectOp op, size_t bytes, int ctas, cudaStream_t st, int* grid_out = nullptr);
 // Force-load every kernel (see iccl_kernels.cu: lazy loading vs parked streams).
 cudaError_t preload_kernels();
 // K5: low-latency (LL) eager path for small and mid-size messages.  8-byte
@@ -121,8 +122,6 @@ struct LLBatch {
 };
 cudaError_t launch_ll(const LLBatch& b, cudaStream_t st);
 
-// K4 stamp: which = 0 writes stamp->t1, which = 1 writes stamp->t2 (release).
-cudaError_t launch_stamp(KernelStamp* stamp, int which, cudaStream_t st);
 // Calibration: write %globaltimer into *out (host-mapped).
 cudaError_t launch_read_globaltimer(unsigned long long* out, cudaStream_t st);
 // K2 / K3: row gather / scatter of `row_bytes`-byte rows (MoE dispatch pack /

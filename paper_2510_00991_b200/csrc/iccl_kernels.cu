@@ -210,19 +210,6 @@ __global__ void __launch_bounds__(512) iccl_copy_unaligned(const char* __restric
   stamp_end(stamp);
 }
 
-// K4 on the copy-engine path: one thread stamps %globaltimer into the chunk's
-// host-mapped record before (which = 0) and after (which = 1) the copy.  The
-// t2 store is the chunk's WC: the proxy polls it instead of an event.
-__global__ void iccl_stamp(KernelStamp* st, int which) {
-  unsigned long long t = globaltimer();
-  if (which == 0) {
-    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(&st->t1), "l"(t) : "memory");
-  } else {
-    __threadfence_system();
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&st->t2), "l"(t) : "memory");
-  }
-}
-
 __global__ void iccl_read_globaltimer(unsigned long long* out) {
   unsigned long long t = globaltimer();
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(out), "l"(t) : "memory");
@@ -423,7 +410,7 @@ cudaError_t launch_ll(const LLBatch& b, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_direct(DirectOp op, size_t bytes, int ctas, cudaStream_t st) {
+cudaError_t launch_direct(DirectOp op, size_t bytes, int ctas, cudaStream_t st, int* grid_out) {
   const uintptr_t s = (uintptr_t)op.src, d = (uintptr_t)op.dst;
   if (((s ^ d) & 15) != 0) return cudaErrorInvalidValue;  // caller routes mutually misaligned pairs elsewhere
   op.head = (16 - (s & 15)) & 15;
@@ -432,16 +419,21 @@ cudaError_t launch_direct(DirectOp op, size_t bytes, int ctas, cudaStream_t st) 
   op.tail = bytes - op.head - op.body;
   const size_t ntiles = (op.body + kTile - 1) / kTile;
   int grid = (int)min((size_t)ctas, ntiles > 0 ? ntiles : (size_t)1);
-  iccl_direct_copy<<<grid < 1 ? 1 : grid, kCopyThreads, kStages * kTile, st>>>(op);
+  if (grid < 1) grid = 1;
+  if (grid_out) *grid_out = grid;
+  iccl_direct_copy<<<grid, kCopyThreads, kStages * kTile, st>>>(op);
   return cudaGetLastError();
 }
 
-cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, KernelStamp* stamp, cudaStream_t st) {
+cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, KernelStamp* stamp, cudaStream_t st,
+                        int* grid_out) {
+  if (grid_out) *grid_out = 0;
   if (bytes == 0) return cudaSuccess;
   const uintptr_t s = (uintptr_t)src, d = (uintptr_t)dst;
   if (((s ^ d) & 15) != 0) {
     int grid = (int)min((size_t)ctas, (bytes + 512 * 16 - 1) / (512 * 16));
     if (grid < 1) grid = 1;
+    if (grid_out) *grid_out = grid;
     iccl_copy_unaligned<<<grid, 512, 0, st>>>((const char*)src, (char*)dst, bytes, stamp);
     return cudaGetLastError();
   }
@@ -457,6 +449,7 @@ cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, Kern
   size_t ntiles = (body + kTile - 1) / kTile;
   int grid = (int)min((size_t)ctas, ntiles > 0 ? ntiles : (size_t)1);
   if (grid < 1) grid = 1;
+  if (grid_out) *grid_out = grid;
   iccl_copy_tma<<<grid, kCopyThreads, kStages * kTile, st>>>((const char*)src, (char*)dst, head, body, tail, stamp);
   return cudaGetLastError();
 }
@@ -468,7 +461,7 @@ cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, Kern
 // iccl_comm_init_rank calls this before any wait is enqueued.
 cudaError_t preload_kernels() {
   cudaFuncAttributes a;
-  const void* fns[] = {(const void*)iccl_copy_tma, (const void*)iccl_direct_copy,   (const void*)iccl_copy_unaligned, (const void*)iccl_stamp,
+  const void* fns[] = {(const void*)iccl_copy_tma, (const void*)iccl_direct_copy,   (const void*)iccl_copy_unaligned,
                        (const void*)iccl_read_globaltimer, (const void*)iccl_gather_rows,
                        (const void*)iccl_scatter_rows, (const void*)iccl_expand_rows,
                        (const void*)iccl_ll_group};
@@ -491,10 +484,6 @@ cudaError_t launch_read_globaltimer(unsigned long long* out, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_stamp(KernelStamp* stamp, int which, cudaStream_t st) {
-  iccl_stamp<<<1, 1, 0, st>>>(stamp, which);
-  return cudaGetLastError();
-}
 
 static int rows_grid(int64_t n_rows, int ctas) {
   int64_t warps_needed = n_rows;

@@ -401,7 +401,7 @@ struct iccl_comm {
   uint64_t faults_t0 = 0;
   std::atomic<int> path_req[2 * kMaxRanks];  // API-requested switches per channel: -1 none, else target path
   std::atomic<uint64_t> pending_xfers{0};
-  std::atomic<uint64_t> kernels_launched{0}, copies_issued{0}, bytes_issued{0};
+  std::atomic<uint64_t> kernels_launched{0}, ctas_launched{0}, copies_issued{0}, bytes_issued{0};
   std::vector<cudaEvent_t> event_pool;  // proxy-owned: chunk WC events
   std::vector<cudaEvent_t> tevent_pool;  // proxy-owned: timing-enabled WC / anchor events (monitor)
   std::vector<cudaEvent_t> all_events;
@@ -823,7 +823,9 @@ static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
     if (r) return r;
   } else {
     ICCL_TRACE("K1 op %llu chunk %d: %zu B on %p", (unsigned long long)x.op_seq, k, n, (void*)sc.s);
-    ICCL_CHECK_CUDA(launch_copy(x.src + off, x.dst + off, n, c->cfg.sm_cap, st, sc.s));
+    int grid = 0;
+    ICCL_CHECK_CUDA(launch_copy(x.src + off, x.dst + off, n, c->cfg.sm_cap, st, sc.s, &grid));
+    c->ctas_launched += grid;
     c->copies_issued += 1;
   }
   c->kernels_launched += eng == ENG_SM ? 1 : 0;
@@ -1439,8 +1441,10 @@ static iccl_result_t rzv_post(iccl_comm* c, OpDesc& op, uint64_t wait_us, bool g
 static iccl_result_t launch_direct_ops(iccl_comm* c, cudaStream_t s, const std::vector<OpDesc>& ops) {
   for (const OpDesc& op : ops) {
     if (!op.issued_direct) continue;
-    ICCL_CHECK_CUDA(launch_direct(op.dop, op.bytes, c->direct_ctas, s));
+    int grid = 0;
+    ICCL_CHECK_CUDA(launch_direct(op.dop, op.bytes, c->direct_ctas, s, &grid));
     c->kernels_launched += 1;
+    c->ctas_launched += grid;
     c->copies_issued += 1;
     c->bytes_issued += op.bytes;
   }
@@ -1526,6 +1530,7 @@ static iccl_result_t launch_ll_ops(iccl_comm* c, cudaStream_t s, const std::vect
     }
     ICCL_CHECK_CUDA(launch_ll(b, s));
     c->kernels_launched += 1;
+    c->ctas_launched += blocks;
   }
   return ICCL_SUCCESS;
 }
@@ -1907,6 +1912,7 @@ iccl_result_t iccl_comm_stats(iccl_comm_t c, iccl_stats_t* s) {
   if (!c || !s) return ICCL_ERR_INVALID_ARGUMENT;
   memset(s, 0, sizeof(*s));
   s->kernels_launched = c->kernels_launched.load();
+  s->ctas_launched = c->ctas_launched.load();
   s->copies_issued = c->copies_issued.load();
   s->bytes_issued = c->bytes_issued.load();
   return ICCL_SUCCESS;
