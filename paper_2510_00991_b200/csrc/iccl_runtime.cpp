@@ -377,6 +377,11 @@ struct iccl_comm {
   std::vector<char*> peer_scratch_base;                       // IPC-opened peer scratch blocks
   int group_depth = 0;
   std::vector<std::pair<OpDesc, cudaStream_t>> group_ops;
+  struct GroupJob {
+    int kind, peer;
+    uint64_t k, op_seq;
+  };
+  std::vector<GroupJob> group_jobs;  // copy-engine pushes of the open group, in call order
   int direct_ctas = 32;  // K6 grid (>= 16 CTAs keep NVLink busy, kernels bench)
   std::unordered_map<uint64_t, cudaIpcMemHandle_t> export_cache;
   // proxy
@@ -746,13 +751,32 @@ static void fire_chunk_faults(iccl_comm* c, Channel& chn, int op_index, int chun
   }
 }
 
+static int chunk_stream(iccl_comm* c, Channel& chn, const Xfer& x, int path, int eng, int k) {
+  return (eng == ENG_CE && x.group_stream) ? stream_for(c, chn, path, ENG_CE_GROUP, 0) : stream_for(c, chn, path, eng, k);
+}
+
+// The ready waits of a transfer's first chunk, enqueued ahead of time (a
+// group's pushes, see iccl_group_end).
+static iccl_result_t ready_waits(iccl_comm* c, Channel& chn, Xfer& x) {
+  const int eng = path_engine(c, chn, x.path, x.bytes);
+  if (eng != ENG_CE) return ICCL_SUCCESS;
+  const int si = chunk_stream(c, chn, x, x.path, eng, 0);
+  if (waited_on(x, x.path, si)) return ICCL_SUCCESS;
+  cudaStream_t s = c->streams[si].s;
+  iccl_result_t r = memop_wait(s, &flags_of(c, x.src_rank)->ready[x.s_slot], x.s_gen);
+  if (r) return r;
+  r = memop_wait(s, &flags_of(c, x.dst_rank)->ready[x.r_ready_slot], x.r_ready_gen);
+  if (r) return r;
+  x.waited[x.path].push_back(si);
+  return ICCL_SUCCESS;
+}
+
 static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
   const int path = x.path;
   const int eng = path_engine(c, chn, path, x.bytes);
   const size_t off = (size_t)k * x.chunk;
   const size_t n = std::min(x.chunk, x.bytes - off);
-  const int si = (eng == ENG_CE && x.group_stream) ? stream_for(c, chn, path, ENG_CE_GROUP, 0)
-                                                    : stream_for(c, chn, path, eng, k);
+  const int si = chunk_stream(c, chn, x, path, eng, k);
   StreamCtx& sc = c->streams[si];
   RankFlags* sender = flags_of(c, x.src_rank);
   RankFlags* receiver = flags_of(c, x.dst_rank);
@@ -763,7 +787,11 @@ static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
     r = memop_wait(sc.s, &receiver->ready[x.r_ready_slot], x.r_ready_gen);
     if (r) return r;
     x.waited[path].push_back(si);
-    if (eng == ENG_CE && c->monitor_enabled.load(std::memory_order_relaxed)) {
+  }
+  {
+    bool anchored = false;
+    for (auto& le : x.last_ev) anchored |= le.first == si;
+    if (!anchored && eng == ENG_CE && c->monitor_enabled.load(std::memory_order_relaxed)) {
       // monitor anchor (the op's start on this stream): an untimed event on
       // the copy stream bridged to a timing event on the monitor stream
       cudaEvent_t a = get_tevent(c);
@@ -1271,8 +1299,10 @@ static bool rzv_claim(RzvEntry& e, uint64_t k) {
 // streams' ready flags, the last one writes both done flags.  From the API
 // thread the transfer is handed to the proxy; from the proxy it is tracked
 // in place.
-static iccl_result_t rzv_issue(iccl_comm* c, int kind, int peer, uint64_t k, uint64_t op_seq, bool on_proxy,
-                               bool group = false) {
+// Build the transfer of rendezvous entry k of the pair (as `kind`: 0 = push
+// by the sender, 1 = pull by the receiver) after winning its claim; no
+// device work yet.
+static iccl_result_t rzv_build(iccl_comm* c, int kind, int peer, uint64_t k, uint64_t op_seq, bool group, Xfer* out) {
   RzvEntry& e = rzv_entry(c, kind, peer, k);
   const int src = kind == 0 ? c->rank : peer, dst = kind == 0 ? peer : c->rank;
   const RzvSide& snd = e.side[0];
@@ -1289,7 +1319,7 @@ static iccl_result_t rzv_issue(iccl_comm* c, int kind, int peer, uint64_t k, uin
   }
   const int ci = 2 * peer + kind;
   Channel& chn = c->ch[ci];
-  Xfer x;
+  Xfer& x = *out;
   x.op_seq = op_seq;
   x.pair_seq = k;
   x.src_rank = src;
@@ -1319,10 +1349,18 @@ static iccl_result_t rzv_issue(iccl_comm* c, int kind, int peer, uint64_t k, uin
     std::lock_guard<std::mutex> gl(c->fault_mu);
     x.fault_ops_index = (int)(k - chn.fault_seq_base);
   }
-  ICCL_TRACE("issue %s (%s) pair %d->%d #%llu, %zu B, %d chunk(s), path %d", kind == 0 ? "push" : "pull",
-             on_proxy ? "proxy" : "api", src, dst, (unsigned long long)k, x.bytes, x.nchunks, x.path);
+  ICCL_TRACE("issue %s pair %d->%d #%llu, %zu B, %d chunk(s), path %d", kind == 0 ? "push" : "pull", src, dst,
+             (unsigned long long)k, x.bytes, x.nchunks, x.path);
+  return ICCL_SUCCESS;
+}
+
+// Enqueue every chunk of a built transfer (each behind waits on both user
+// streams' ready flags, the last one writing both done flags) and hand it to
+// the proxy — or, issued by the proxy itself, track it in place.
+static iccl_result_t rzv_launch(iccl_comm* c, Xfer&& x, bool on_proxy) {
+  Channel& chn = c->ch[x.chan];
   while (x.next_issue < x.nchunks) {
-    r = issue_chunk(c, chn, x, x.next_issue);
+    iccl_result_t r = issue_chunk(c, chn, x, x.next_issue);
     if (r == ICCL_ERR_IN_PROGRESS) break;  // relay ring full: the proxy issues the rest
     if (r) return r;
     x.next_issue++;
@@ -1339,6 +1377,14 @@ static iccl_result_t rzv_issue(iccl_comm* c, int kind, int peer, uint64_t k, uin
   }
   c->qcv.notify_one();
   return ICCL_SUCCESS;
+}
+
+static iccl_result_t rzv_issue(iccl_comm* c, int kind, int peer, uint64_t k, uint64_t op_seq, bool on_proxy,
+                               bool group = false) {
+  Xfer x;
+  iccl_result_t r = rzv_build(c, kind, peer, k, op_seq, group, &x);
+  if (r) return r;
+  return rzv_launch(c, std::move(x), on_proxy);
 }
 
 // Rendezvous of the k-th op of an ordered pair (SPEC.md:194's RTS / CTS): post
@@ -1434,7 +1480,13 @@ static iccl_result_t rzv_post(iccl_comm* c, OpDesc& op, uint64_t wait_us, bool g
       return ICCL_SUCCESS;
     }
   }
-  return rzv_issue(c, kind, peer, k, op.op_seq, false, group);
+  if (group) {
+    // a group's pushes are launched together once the whole group has met
+    // its peers (iccl_group_end): all ready waits first, then the copies
+    c->group_jobs.push_back({kind, peer, k, op.op_seq});
+    return ICCL_SUCCESS;
+  }
+  return rzv_issue(c, kind, peer, k, op.op_seq, false, false);
 }
 
 // K6 for every op of `ops` this side issues directly, on stream s.
@@ -1971,6 +2023,27 @@ iccl_result_t iccl_group_end(iccl_comm_t c) {
     const uint64_t t = now_ns();
     iccl_result_t r = rzv_post(c, p.first, t < deadline ? (deadline - t) / 1000 : 0, true);
     if (r) return r;
+  }
+  {
+    // The group's pushes share one stream (rzv_post): enqueue every ready
+    // wait first, then the copies back to back — a wait placed between two
+    // copies would cost each a copy-engine drain (~15 us per peer in the
+    // 4-rank alltoallv records).
+    std::vector<Xfer> xs(c->group_jobs.size());
+    for (size_t i = 0; i < xs.size(); i++) {
+      const auto& j = c->group_jobs[i];
+      iccl_result_t r = rzv_build(c, j.kind, j.peer, j.k, j.op_seq, true, &xs[i]);
+      if (r) return r;
+    }
+    c->group_jobs.clear();
+    for (Xfer& x : xs) {
+      iccl_result_t r = ready_waits(c, c->ch[x.chan], x);
+      if (r) return r;
+    }
+    for (Xfer& x : xs) {
+      iccl_result_t r = rzv_launch(c, std::move(x), false);
+      if (r) return r;
+    }
   }
   // per stream: ready markers of the ops waiting on a peer (copy engine, or
   // K6 run by the peer), then the kernels (LL, K6 this side runs), then the
