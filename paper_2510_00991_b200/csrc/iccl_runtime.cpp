@@ -86,8 +86,8 @@ constexpr size_t kScratchBytes = 4096;
 constexpr int kProxyNapUs = 20;  // proxy back-off when a pass moved nothing
 // How long a send waits for its receiver's half before posting its own (so
 // that it arrives second and pushes, see rzv_post): single ops / a group.
-constexpr uint64_t kSendWaitUs = 50;
-constexpr uint64_t kGroupSendWaitUs = 2000;
+constexpr uint64_t kSendWaitUs = 20;
+constexpr uint64_t kGroupSendWaitUs = 200;
 
 // ---------------------------------------------------------------- shared control block
 struct alignas(64) ShmHeader {
