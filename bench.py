@@ -405,7 +405,12 @@ def run_alltoallv(args):
     eb = torch.tensor([max(c_out, c_in) * row], device=dev, dtype=torch.float64)
     tot = torch.tensor([2.0 * sum(plan.send_counts) * row], device=dev, dtype=torch.float64)
     okt = torch.tensor([1.0 if ok else 0.0], device=dev, dtype=torch.float64)
+    # rendezvous outcomes in the timed region, summed over ranks: transfers
+    # the receiver issued (pulls) and sends that gave up waiting for the CTS
+    rzv = torch.tensor([s1["pulls_issued"] - s0["pulls_issued"], s1["cts_timeouts"] - s0["cts_timeouts"]],
+                       device=dev, dtype=torch.float64)
     if world > 1:
+        dist.all_reduce(rzv, op=dist.ReduceOp.SUM)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(eb, op=dist.ReduceOp.MAX)
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
@@ -430,6 +435,8 @@ def run_alltoallv(args):
             "roofline": {"bound": "nvlink+hbm" if world > 1 else "hbm", "t_star_ms": round(t_star * 1e3, 4),
                          "frac": round(t_star / (ms * 1e-3), 4),
                          "note": "t* = 2 x max_i max(egress_i, ingress_i)/770 GB/s + K2/K3 HBM time"},
+            "rendezvous": {"pulls": int(rzv[0].item()), "cts_timeouts": int(rzv[1].item()),
+                           "transfers": 2 * args.steps * world * (world - 1)},
             "bit_exact_roundtrip": bool(okt.item() > 0), "gpu_launches": int(s1["kernels_launched"] - s0[
                 "kernels_launched"]) + 2 * args.steps,
             "clocks": clk.summary()}))

@@ -120,6 +120,8 @@ def main():
     if comm:
         s1 = comm.stats()
         res["kernels_launched"] = s1["kernels_launched"] - s0["kernels_launched"]
+        res["rank0_pulls_issued"] = s1["pulls_issued"] - s0["pulls_issued"]
+        res["rank0_cts_timeouts"] = s1["cts_timeouts"] - s0["cts_timeouts"]
         comm.destroy()
     if rank == 0:
         print(json.dumps(res), flush=True)

@@ -160,13 +160,15 @@ iccl_result_t iccl_comm_op_counts(iccl_comm_t comm, uint64_t* counts, int n);
 
 /* Counters of the work this rank issued (SURVEY.md §5 metrics): SM kernels
  * launched (K1 backup copies, K5 LL, K6 direct) and their CTAs, copy-engine
- * copies, payload bytes. */
+ * copies, payload bytes, and how the rendezvous went (pulls, CTS timeouts). */
 typedef struct {
   uint64_t kernels_launched;
   uint64_t copies_issued;
   uint64_t bytes_issued;
   uint64_t ctas_launched;  /* CTAs of those kernels (the "SMs used" of the SM paths) */
-  uint64_t reserved[4];
+  uint64_t pulls_issued;   /* transfers this rank issued as the receiver (it reached the rendezvous second) */
+  uint64_t cts_timeouts;   /* sends that stopped waiting for the receiver's half and posted first */
+  uint64_t reserved[2];
 } iccl_stats_t;
 iccl_result_t iccl_comm_stats(iccl_comm_t comm, iccl_stats_t* stats);
 

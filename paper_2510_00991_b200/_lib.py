@@ -75,7 +75,8 @@ class SwitchEvent(C.Structure):
 
 class Stats(C.Structure):
     _fields_ = [("kernels_launched", C.c_uint64), ("copies_issued", C.c_uint64), ("bytes_issued", C.c_uint64),
-                ("ctas_launched", C.c_uint64), ("reserved", C.c_uint64 * 4)]
+                ("ctas_launched", C.c_uint64), ("pulls_issued", C.c_uint64), ("cts_timeouts", C.c_uint64),
+                ("reserved", C.c_uint64 * 2)]
 
 
 _c = C.c_int  # iccl_result_t

@@ -283,12 +283,13 @@ class Communicator:
     # -- observability -----------------------------------------------------------
     def stats(self) -> dict:
         """Work this rank issued: SM kernels launched (K1, K5, K6) and their
-        CTAs, copy-engine copies and payload bytes."""
+        CTAs, copy-engine copies and payload bytes; transfers issued as the
+        receiver (pulls) and sends whose wait for the receiver timed out."""
         from ._lib import Stats
         s = Stats()
         raise_for(lib.iccl_comm_stats(self._h, C.byref(s)), "iccl_comm_stats")
         return dict(kernels_launched=s.kernels_launched, ctas_launched=s.ctas_launched, copies_issued=s.copies_issued,
-                    bytes_issued=s.bytes_issued)
+                    bytes_issued=s.bytes_issued, pulls_issued=s.pulls_issued, cts_timeouts=s.cts_timeouts)
 
     def op_counts(self) -> dict:
         arr = (C.c_uint64 * self.world_size)()

@@ -55,7 +55,11 @@
 #include <string>
 #include <thread>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
+
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include "iccl_internal.h"
 
@@ -69,8 +73,45 @@ static const bool g_debug = getenv("ICCL_DEBUG") && atoi(getenv("ICCL_DEBUG")) >
     if (::iccl::g_debug) {                                                       \
       char b_[512];                                                              \
       snprintf(b_, sizeof(b_), __VA_ARGS__);                                     \
-      fprintf(stderr, "[iccl %.6f] %s\n", (double)::iccl::now_ns() * 1e-9, b_); \
+      fprintf(stderr, "[iccl %.6f %d] %s\n", (double)::iccl::now_ns() * 1e-9,     \
+              (int)syscall(SYS_gettid), b_);                                     \
     }                                                                            \
+  } while (0)
+
+// Under ICCL_DEBUG every device call is also timed: one that blocks for more
+// than 50 us (a full command queue, a lock another thread holds in the
+// driver) is traced with the call and the calling thread.
+#define ICCL_TIMED_(expr, R_)                                                                     \
+  [&]() {                                                                                         \
+    const uint64_t t0_ = ::iccl::g_debug ? ::iccl::now_ns() : 0;                                  \
+    R_ v_ = (expr);                                                                               \
+    if (::iccl::g_debug) {                                                                        \
+      const uint64_t d_ = ::iccl::now_ns() - t0_;                                                 \
+      if (d_ > 50000) ICCL_TRACE("slow device call %.1f us at line %d: %s", d_ * 1e-3, __LINE__, #expr); \
+    }                                                                                             \
+    return v_;                                                                                    \
+  }()
+#undef ICCL_CHECK_CUDA
+#define ICCL_CHECK_CUDA(expr)                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = ICCL_TIMED_(expr, cudaError_t);                                       \
+    if (e_ != cudaSuccess) {                                                               \
+      ::iccl::set_last_error(std::string(#expr) + ": " + cudaGetErrorString(e_) + " at " + \
+                             __FILE__ + ":" + std::to_string(__LINE__));                   \
+      return ICCL_ERR_CUDA;                                                                \
+    }                                                                                      \
+  } while (0)
+#undef ICCL_CHECK_CU
+#define ICCL_CHECK_CU(expr)                                                              \
+  do {                                                                                   \
+    CUresult r_ = ICCL_TIMED_(expr, CUresult);                                           \
+    if (r_ != CUDA_SUCCESS) {                                                            \
+      const char* s_ = "?";                                                              \
+      if (::iccl::driver()) ::iccl::driver()->cuGetErrorString(r_, &s_);                 \
+      ::iccl::set_last_error(std::string(#expr) + ": " + s_ + " at " + __FILE__ + ":" +  \
+                             std::to_string(__LINE__));                                  \
+      return ICCL_ERR_CUDA;                                                              \
+    }                                                                                    \
   } while (0)
 
 constexpr uint64_t kMagic = 0x3030324242434349ull;  // "ICCLB200"
@@ -86,8 +127,13 @@ constexpr size_t kScratchBytes = 4096;
 constexpr int kProxyNapUs = 20;  // proxy back-off when a pass moved nothing
 // How long a send waits for its receiver's half before posting its own (so
 // that it arrives second and pushes, see rzv_post): single ops / a group.
-constexpr uint64_t kSendWaitUs = 20;
-constexpr uint64_t kGroupSendWaitUs = 200;
+// ICCL_SEND_WAIT_US / ICCL_GROUP_SEND_WAIT_US override them.
+static uint64_t env_us(const char* name, uint64_t dflt) {
+  const char* v = getenv(name);
+  return v && *v ? strtoull(v, nullptr, 10) : dflt;
+}
+static const uint64_t kSendWaitUs = env_us("ICCL_SEND_WAIT_US", 20);
+static const uint64_t kGroupSendWaitUs = env_us("ICCL_GROUP_SEND_WAIT_US", 200);
 
 // ---------------------------------------------------------------- shared control block
 struct alignas(64) ShmHeader {
@@ -156,8 +202,21 @@ struct alignas(64) PairState {
   std::atomic<int32_t> active_path, switches;
 };
 
+// Buffers src exported to dst (a new CU_POINTER_ATTRIBUTE_BUFFER_ID in one of
+// its halves): dst's proxy opens them ahead of need (premap_peer_buffers).
+constexpr int kAnnDepth = 64;
+struct AnnEntry {
+  uint64_t buffer_id;
+  cudaIpcMemHandle_t handle;
+};
+struct alignas(64) Announce {
+  std::atomic<uint64_t> head, tail;  // head: src's API thread, tail: dst's proxy
+  AnnEntry e[kAnnDepth];
+};
+
 struct alignas(64) RzvRing {
   PairState st;
+  Announce ann;
   RzvEntry e[kRzvDepth];
 };
 
@@ -214,8 +273,8 @@ struct UidBlob {
 static inline bool cyc_geq(uint32_t a, uint32_t b) { return (int32_t)(a - b) >= 0; }
 
 // ---------------------------------------------------------------- proxy-side structures
-// ENG_CE_GROUP: the rank's one stream for the pushes of a group (alltoallv,
-// batch_isend_irecv) — see rzv_post.
+// ENG_CE_GROUP: the rank's two group streams — one for the pushes, one for
+// the pulls of a group (alltoallv, batch_isend_irecv) — see rzv_post.
 enum Engine { ENG_CE = 0, ENG_SM = 1, ENG_RELAY = 2, ENG_CE_GROUP = 3 };
 
 struct OpDesc {
@@ -266,7 +325,7 @@ struct Xfer {
   int completed = 0;   // contiguous prefix observed delivered: acked == receiver done
   int path = 0;
   std::vector<int> waited[2];  // per path: streams that already waited on the ready flags
-  bool group_stream = false;   // push of a group: the rank's shared group stream
+  bool group_stream = false;   // remote copy of a group: the rank's group stream of its direction
   bool done_enqueued = false;
   bool eligible = false;
   uint64_t last_progress = 0;
@@ -381,9 +440,10 @@ struct iccl_comm {
     int kind, peer;
     uint64_t k, op_seq;
   };
-  std::vector<GroupJob> group_jobs;  // copy-engine pushes of the open group, in call order
+  std::vector<GroupJob> group_jobs;  // copy-engine transfers this side issues for the open group
   int direct_ctas = 32;  // K6 grid (>= 16 CTAs keep NVLink busy, kernels bench)
   std::unordered_map<uint64_t, cudaIpcMemHandle_t> export_cache;
+  std::vector<std::unordered_set<uint64_t>> announced;  // per peer: buffer ids announced to it
   // proxy
   std::vector<Channel> ch;  // 2 per peer: [2 * peer + dir]
   std::vector<StreamCtx> streams;
@@ -401,12 +461,14 @@ struct iccl_comm {
   std::mutex fault_mu;  // fault script + per-channel fault / gate state (API thread and proxy)
   std::mutex ev_mu;     // event pools (API thread and proxy)
   std::mutex relay_mu;  // relay piece counters (API thread and proxy)
-  std::mutex ipc_mu;    // peer_ipc (API thread and the relay server)
+  std::mutex ipc_mu;    // peer_ipc (API thread, relay server, premapping proxy)
+  std::mutex open_mu;   // serialises cudaIpcOpenMemHandle (map_peer_allocation)
   std::vector<Fault> faults;
   uint64_t faults_t0 = 0;
   std::atomic<int> path_req[2 * kMaxRanks];  // API-requested switches per channel: -1 none, else target path
   std::atomic<uint64_t> pending_xfers{0};
   std::atomic<uint64_t> kernels_launched{0}, ctas_launched{0}, copies_issued{0}, bytes_issued{0};
+  std::atomic<uint64_t> pulls_issued{0}, cts_timeouts{0};  // rendezvous outcomes (rzv_post)
   std::vector<cudaEvent_t> event_pool;  // proxy-owned: chunk WC events
   std::vector<cudaEvent_t> tevent_pool;  // proxy-owned: timing-enabled WC / anchor events (monitor)
   std::vector<cudaEvent_t> all_events;
@@ -557,16 +619,74 @@ static void push_switch_event(iccl_comm* c, int peer, int to, int resume, int tr
 // PAPER.md:410-412).  Shared by the API thread and the relay server.
 static iccl_result_t map_peer_allocation(iccl_comm* c, int owner, uint64_t buffer_id, cudaIpcMemHandle_t handle,
                                          char** base) {
-  std::lock_guard<std::mutex> g(c->ipc_mu);
-  auto& cache = c->peer_ipc[owner];
-  auto it = cache.find(buffer_id);
-  if (it == cache.end()) {
-    void* p = nullptr;
-    ICCL_CHECK_CUDA(cudaIpcOpenMemHandle(&p, handle, cudaIpcMemLazyEnablePeerAccess));
-    it = cache.emplace(buffer_id, (char*)p).first;
+  {
+    std::lock_guard<std::mutex> g(c->ipc_mu);
+    auto& cache = c->peer_ipc[owner];
+    auto it = cache.find(buffer_id);
+    if (it != cache.end()) {
+      *base = it->second;
+      return ICCL_SUCCESS;
+    }
   }
-  *base = it->second;
+  // opened under open_mu only (it can take tens of ms): a thread looking up
+  // an already-open buffer never waits for it
+  std::lock_guard<std::mutex> og(c->open_mu);
+  {
+    std::lock_guard<std::mutex> g(c->ipc_mu);
+    auto& cache = c->peer_ipc[owner];
+    auto it = cache.find(buffer_id);
+    if (it != cache.end()) {  // another thread opened it meanwhile
+      *base = it->second;
+      return ICCL_SUCCESS;
+    }
+  }
+  void* p = nullptr;
+  ICCL_CHECK_CUDA(cudaIpcOpenMemHandle(&p, handle, cudaIpcMemLazyEnablePeerAccess));
+  std::lock_guard<std::mutex> g(c->ipc_mu);
+  c->peer_ipc[owner].emplace(buffer_id, (char*)p);
+  *base = (char*)p;
   return ICCL_SUCCESS;
+}
+
+// Opening a peer allocation costs 0.3-55 ms (cudaIpcOpenMemHandle of a
+// caching-allocator segment, 4-rank alltoallv trace), during which the
+// opening thread issues nothing.  Whichever side reaches a rendezvous second
+// maps the other side's tensor, so a pair that has only ever pushed meets
+// that cost again the first time it pulls — and a host stalled for 45 ms
+// makes every peer's send stop waiting for it and post first, i.e. more
+// pulls (a 10-step alltoallv ran at 3-6 ms/step instead of 1.5, profiles/r01).
+// So each new buffer is announced to the peer on first use, and the peer's
+// proxy opens it in the background.
+static void announce_buffer(iccl_comm* c, int peer, const RzvSide& s) {
+  if (!c->announced[peer].insert(s.buffer_id).second) return;
+  Announce& a = ring_of(c, c->rank, peer)->ann;
+  const uint64_t h = a.head.load(std::memory_order_relaxed);
+  if (h - a.tail.load(std::memory_order_acquire) >= (uint64_t)kAnnDepth) return;  // best effort
+  a.e[h % kAnnDepth] = AnnEntry{s.buffer_id, s.handle};
+  a.head.store(h + 1, std::memory_order_release);
+}
+
+// Proxy: open what peers announced (errors are ignored: the owner may have
+// freed the buffer since; the issuing side maps on demand anyway).
+static bool premap_peer_buffers(iccl_comm* c) {
+  bool any = false;
+  for (int q = 0; q < c->nranks; q++) {
+    if (q == c->rank) continue;
+    Announce& a = ring_of(c, q, c->rank)->ann;
+    uint64_t t = a.tail.load(std::memory_order_relaxed);
+    const uint64_t h = a.head.load(std::memory_order_acquire);
+    for (; t < h; t++) {
+      const AnnEntry en = a.e[t % kAnnDepth];
+      char* base = nullptr;
+      const uint64_t t0 = now_ns();
+      if (map_peer_allocation(c, q, en.buffer_id, en.handle, &base) != ICCL_SUCCESS) cudaGetLastError();
+      ICCL_TRACE("premapped buffer %llu of rank %d in %.1f us", (unsigned long long)en.buffer_id, q,
+                 (now_ns() - t0) * 1e-3);
+      a.tail.store(t + 1, std::memory_order_release);
+      any = true;
+    }
+  }
+  return any;
 }
 
 // The other side's tensor in my address space: its own pointer for a self
@@ -1203,6 +1323,7 @@ static void proxy_loop(iccl_comm* c) {
       continue;
     }
     fire_time_faults(c);
+    busy |= premap_peer_buffers(c);
     for (int ci = 0; ci < 2 * c->nranks; ci++) {
       Channel& chn = c->ch[ci];
       int req = c->path_req[ci].exchange(-1);
@@ -1344,7 +1465,7 @@ static iccl_result_t rzv_build(iccl_comm* c, int kind, int peer, uint64_t k, uin
   x.rec.resize(x.nchunks);
   x.path = pair_of(c, src, dst).active_path.load();
   x.last_progress = now_ns();
-  x.group_stream = group && kind == 0 && peer != c->rank;
+  x.group_stream = group && peer != c->rank;
   {
     std::lock_guard<std::mutex> gl(c->fault_mu);
     x.fault_ops_index = (int)(k - chn.fault_seq_base);
@@ -1411,7 +1532,10 @@ static iccl_result_t rzv_issue(iccl_comm* c, int kind, int peer, uint64_t k, uin
 // 4-rank alltoallv ended up pushing into the same receiver at once (incast,
 // each at half rate: MoE records, profiles/r01/README.md).  On one stream the
 // rotated order of iccl_alltoallv (step k: rank i -> i + k) holds, so at each
-// step every receiver has one sender.
+// step every receiver has one sender.  The pulls a group's recvs end up
+// issuing (their sender posted first) go the same way, on a second stream:
+// issued one by one on per-peer streams at enqueue they ran the 4-rank
+// alltoallv at less than half speed (profiles/r01/README.md).
 static iccl_result_t rzv_post(iccl_comm* c, OpDesc& op, uint64_t wait_us, bool group = false) {
   const int peer = op.peer, kind = op.kind;
   const uint64_t k = kind == 0 ? c->pair_sends[peer]++ : c->pair_recvs[peer]++;
@@ -1432,8 +1556,10 @@ static iccl_result_t rzv_post(iccl_comm* c, OpDesc& op, uint64_t wait_us, bool g
   if (kind == 0 && peer != c->rank && wait_us > 0) {
     const uint64_t t_wait = now_ns(), deadline = t_wait + wait_us * 1000ull;
     while (e.arrivals.load(std::memory_order_acquire) < 2 * g + 1 && now_ns() < deadline) sched_yield();
+    const bool timed_out = e.arrivals.load(std::memory_order_acquire) < 2 * g + 1;
+    if (timed_out) c->cts_timeouts += 1;
     ICCL_TRACE("send %d->%d #%llu waited %.1f us for the CTS%s", c->rank, peer, (unsigned long long)k,
-               (now_ns() - t_wait) * 1e-3, e.arrivals.load() < 2 * g + 1 ? " (timed out)" : "");
+               (now_ns() - t_wait) * 1e-3, timed_out ? " (timed out)" : "");
   }
   RzvSide& mine = e.side[kind];
   mine.bytes = op.bytes;
@@ -1445,6 +1571,7 @@ static iccl_result_t rzv_post(iccl_comm* c, OpDesc& op, uint64_t wait_us, bool g
   if (peer != c->rank) {
     iccl_result_t r = export_buffer(c, op.src, &mine);
     if (r) return r;
+    announce_buffer(c, peer, mine);
   }
   if (e.arrivals.fetch_add(1, std::memory_order_acq_rel) != 2 * g + 1) {
     ICCL_TRACE("%s %d->%d #%llu posted first", kind == 0 ? "send" : "recv", kind == 0 ? c->rank : peer,
@@ -1452,6 +1579,7 @@ static iccl_result_t rzv_post(iccl_comm* c, OpDesc& op, uint64_t wait_us, bool g
     return ICCL_SUCCESS;  // first: the peer issues
   }
   if (!rzv_claim(e, k)) return ICCL_SUCCESS;  // cannot happen: the first side never claims
+  if (kind == 1 && peer != c->rank) c->pulls_issued += 1;
   if (op.direct) {
     const RzvSide& other = e.side[kind ^ 1];
     // K6's TMA ring needs both tensors at the same alignment mod 16 (an IPC
@@ -1620,7 +1748,7 @@ static iccl_result_t enqueue_op(iccl_comm* c, int kind, const void* buf, size_t 
   if (op.ll) {
     op.ll_seq = kind == 0 ? ++c->ll_sent[peer] : ++c->ll_recvd[peer];
   } else if (kind == 1 || c->group_depth == 0) {
-    r = rzv_post(c, op, kind == 0 ? kSendWaitUs : 0);
+    r = rzv_post(c, op, kind == 0 ? kSendWaitUs : 0, c->group_depth > 0);
     if (r) return r;
   }  // a send inside a group posts at group_end, after every recv of the group
   c->ranks[c->rank].op_count.fetch_add(1, std::memory_order_relaxed);
@@ -1680,6 +1808,7 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
   c->shm_name = b.shm_name;
   for (int i = 0; i < 2 * kMaxRanks; i++) c->path_req[i].store(-1);
   c->pair_sends.assign(nranks, 0);
+  c->announced.assign(nranks, {});
   c->pair_recvs.assign(nranks, 0);
   c->peer_ipc.resize(nranks);
   ShmLayout L(nranks);
@@ -1784,8 +1913,8 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
     c->streams.push_back(sc);
     return (int)c->streams.size() - 1;
   };
-  // one stream for the remote pushes of a group, in call order (rzv_post)
-  const int group_si = mk_stream(ENG_CE_GROUP);
+  // the group streams: remote pushes / remote pulls of a group (rzv_post)
+  const int group_si[2] = {mk_stream(ENG_CE_GROUP), mk_stream(ENG_CE_GROUP)};
   std::vector<char*> peer_scratch(nranks, nullptr);
   for (int p = 0; p < nranks; p++) {
     if (p == rank) {
@@ -1824,9 +1953,9 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
         }
       chn.path_streams[1].push_back(mk_stream(ENG_RELAY));
     }
-    if (chn.dir == 0 && p != rank) {
-      chn.path_streams[0].push_back(group_si);
-      chn.path_streams[1].push_back(group_si);
+    if (p != rank) {
+      chn.path_streams[0].push_back(group_si[chn.dir]);
+      chn.path_streams[1].push_back(group_si[chn.dir]);
     }
     chn.probe_stream = mk_stream(ENG_CE);
     chn.mon_stream = mk_stream(ENG_CE);
@@ -1967,6 +2096,8 @@ iccl_result_t iccl_comm_stats(iccl_comm_t c, iccl_stats_t* s) {
   s->ctas_launched = c->ctas_launched.load();
   s->copies_issued = c->copies_issued.load();
   s->bytes_issued = c->bytes_issued.load();
+  s->pulls_issued = c->pulls_issued.load();
+  s->cts_timeouts = c->cts_timeouts.load();
   return ICCL_SUCCESS;
 }
 
