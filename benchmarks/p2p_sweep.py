@@ -149,7 +149,6 @@ def main():
                 fh.write(json.dumps(rec) + "\n")
     dist.barrier()
     dist.destroy_process_group()
-    del time
 
 
 if __name__ == "__main__":

@@ -82,6 +82,16 @@ struct DirectOp {
   unsigned int* error;              // host-mapped: set to 1 if the wait timed out
 };
 cudaError_t launch_direct(DirectOp op, size_t bytes, int ctas, cudaStream_t st, int* grid_out = nullptr);
+// K7: the other side of a direct (K6-class) op waits for its done flags in a
+// one-warp kernel (ld.acquire.sys polling) instead of a stream memop wait.
+constexpr int kWaitMax = 32;
+struct WaitList {
+  const uint32_t* addr[kWaitMax];
+  uint32_t gen[kWaitMax];
+  int n;
+  unsigned int* error;  // host-mapped: set to 1 if a wait timed out (10 s)
+};
+cudaError_t launch_wait(const WaitList& wl, cudaStream_t st);
 // Force-load every kernel (see iccl_kernels.cu: lazy loading vs parked streams).
 cudaError_t preload_kernels();
 // K5: low-latency (LL) eager path for small and mid-size messages.  8-byte

@@ -410,6 +410,29 @@ cudaError_t launch_ll(const LLBatch& b, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// K7.  One thread polls each done flag in turn (the flags live in the
+// host-mapped control block); the stream continues when the kernel exits.
+__global__ void __launch_bounds__(32) iccl_wait_flags(WaitList wl) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long t0 = globaltimer();
+  for (int i = 0; i < wl.n; i++) {
+    uint32_t v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(wl.addr[i]) : "memory");
+      if ((int32_t)(v - wl.gen[i]) < 0 && globaltimer() - t0 > 10000000000ull) {
+        *wl.error = 1;
+        return;
+      }
+    } while ((int32_t)(v - wl.gen[i]) < 0);
+  }
+}
+
+cudaError_t launch_wait(const WaitList& wl, cudaStream_t st) {
+  if (wl.n <= 0) return cudaSuccess;
+  iccl_wait_flags<<<1, 32, 0, st>>>(wl);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_direct(DirectOp op, size_t bytes, int ctas, cudaStream_t st, int* grid_out) {
   const uintptr_t s = (uintptr_t)op.src, d = (uintptr_t)op.dst;
   if (((s ^ d) & 15) != 0) return cudaErrorInvalidValue;  // caller routes mutually misaligned pairs elsewhere
@@ -464,7 +487,7 @@ cudaError_t preload_kernels() {
   const void* fns[] = {(const void*)iccl_copy_tma, (const void*)iccl_direct_copy,   (const void*)iccl_copy_unaligned,
                        (const void*)iccl_read_globaltimer, (const void*)iccl_gather_rows,
                        (const void*)iccl_scatter_rows, (const void*)iccl_expand_rows,
-                       (const void*)iccl_ll_group};
+                       (const void*)iccl_ll_group, (const void*)iccl_wait_flags};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;

@@ -441,7 +441,8 @@ struct iccl_comm {
     uint64_t k, op_seq;
   };
   std::vector<GroupJob> group_jobs;  // copy-engine transfers this side issues for the open group
-  int direct_ctas = 32;  // K6 grid (>= 16 CTAs keep NVLink busy, kernels bench)
+  int direct_ctas = 32;
+  bool kernel_waits = true;  // K7 for the done waits of direct-class ops (ICCL_KERNEL_WAITS=0: memop waits)  // K6 grid (>= 16 CTAs keep NVLink busy, kernels bench)
   std::unordered_map<uint64_t, cudaIpcMemHandle_t> export_cache;
   std::vector<std::unordered_set<uint64_t>> announced;  // per peer: buffer ids announced to it
   // proxy
@@ -1649,8 +1650,24 @@ static iccl_result_t stream_markers(iccl_comm* c, cudaStream_t s, const std::vec
     w.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
     p.push_back(w);
   }
+  // done waits: a stream memop wait per op — except for direct-class ops
+  // (K6 sizes), whose wait is K7: a memop wait on the host-mapped flag cost
+  // ~6 us more per op in the mid-size sweep than a kernel polling it
+  WaitList wl;
+  memset(&wl, 0, sizeof(wl));
+  wl.error = c->ll_error;
+  std::vector<WaitList> kwaits;
   for (const OpDesc& op : ops) {
     if (!(phases & 2)) break;
+    if (op.direct && c->kernel_waits) {
+      wl.addr[wl.n] = &mine->done[op.slot];
+      wl.gen[wl.n] = op.gen;
+      if (++wl.n == kWaitMax) {
+        kwaits.push_back(wl);
+        wl.n = 0;
+      }
+      continue;
+    }
     CUstreamBatchMemOpParams w;
     memset(&w, 0, sizeof(w));
     w.waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
@@ -1662,6 +1679,12 @@ static iccl_result_t stream_markers(iccl_comm* c, cudaStream_t s, const std::vec
   for (size_t i = 0; i < p.size(); i += 128) {
     unsigned n = (unsigned)std::min<size_t>(128, p.size() - i);
     ICCL_CHECK_CU(driver()->cuStreamBatchMemOp((CUstream)s, n, p.data() + i, 0));
+  }
+  if (wl.n > 0) kwaits.push_back(wl);
+  for (const WaitList& w : kwaits) {
+    ICCL_CHECK_CUDA(launch_wait(w, s));
+    c->kernels_launched += 1;
+    c->ctas_launched += 1;
   }
   return ICCL_SUCCESS;
 }
@@ -1860,6 +1883,7 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
     ICCL_CHECK_CUDA(cudaMemset(c->ll_region, 0, ll_bytes));
     ICCL_CHECK_CUDA(cudaIpcGetMemHandle(&me.ll_handle, c->ll_region));
     c->ll_error = (unsigned int*)((char*)c->pinned + 56 * 1024);
+    c->kernel_waits = env_us("ICCL_KERNEL_WAITS", 1) != 0;
     // kLLCounters arrival counters + kLLCounters K6 go words
     ICCL_CHECK_CUDA(cudaMalloc((void**)&c->ll_counters, 2 * kLLCounters * sizeof(unsigned int)));
     ICCL_CHECK_CUDA(cudaMemset(c->ll_counters, 0, 2 * kLLCounters * sizeof(unsigned int)));
