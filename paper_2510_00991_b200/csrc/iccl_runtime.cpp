@@ -326,6 +326,7 @@ struct Xfer {
   int path = 0;
   std::vector<int> waited[2];  // per path: streams that already waited on the ready flags
   bool group_stream = false;   // remote copy of a group: the rank's group stream of its direction
+  int group_lane = 0;          // which of the direction's group streams (ICCL_GROUP_LANES)
   bool done_enqueued = false;
   bool eligible = false;
   uint64_t last_progress = 0;
@@ -442,7 +443,8 @@ struct iccl_comm {
   };
   std::vector<GroupJob> group_jobs;  // copy-engine transfers this side issues for the open group
   int direct_ctas = 32;
-  bool kernel_waits = true;  // K7 for the done waits of direct-class ops (ICCL_KERNEL_WAITS=0: memop waits)  // K6 grid (>= 16 CTAs keep NVLink busy, kernels bench)
+  bool kernel_waits = true;
+  int group_lanes = 1;       // group streams per direction (ICCL_GROUP_LANES)  // K7 for the done waits of direct-class ops (ICCL_KERNEL_WAITS=0: memop waits)  // K6 grid (>= 16 CTAs keep NVLink busy, kernels bench)
   std::unordered_map<uint64_t, cudaIpcMemHandle_t> export_cache;
   std::vector<std::unordered_set<uint64_t>> announced;  // per peer: buffer ids announced to it
   // proxy
@@ -873,7 +875,8 @@ static void fire_chunk_faults(iccl_comm* c, Channel& chn, int op_index, int chun
 }
 
 static int chunk_stream(iccl_comm* c, Channel& chn, const Xfer& x, int path, int eng, int k) {
-  return (eng == ENG_CE && x.group_stream) ? stream_for(c, chn, path, ENG_CE_GROUP, 0) : stream_for(c, chn, path, eng, k);
+  return (eng == ENG_CE && x.group_stream) ? stream_for(c, chn, path, ENG_CE_GROUP, x.group_lane)
+                                            : stream_for(c, chn, path, eng, k);
 }
 
 // The ready waits of a transfer's first chunk, enqueued ahead of time (a
@@ -1938,7 +1941,13 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
     return (int)c->streams.size() - 1;
   };
   // the group streams: remote pushes / remote pulls of a group (rzv_post)
-  const int group_si[2] = {mk_stream(ENG_CE_GROUP), mk_stream(ENG_CE_GROUP)};
+  // ICCL_GROUP_LANES (1..4) streams per direction: consecutive transfers of a
+  // group alternate between them
+  const int lanes = (int)std::min<uint64_t>(4, std::max<uint64_t>(1, env_us("ICCL_GROUP_LANES", 1)));
+  std::vector<int> group_si[2];
+  for (int d = 0; d < 2; d++)
+    for (int l = 0; l < lanes; l++) group_si[d].push_back(mk_stream(ENG_CE_GROUP));
+  c->group_lanes = lanes;
   std::vector<char*> peer_scratch(nranks, nullptr);
   for (int p = 0; p < nranks; p++) {
     if (p == rank) {
@@ -1978,8 +1987,10 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
       chn.path_streams[1].push_back(mk_stream(ENG_RELAY));
     }
     if (p != rank) {
-      chn.path_streams[0].push_back(group_si[chn.dir]);
-      chn.path_streams[1].push_back(group_si[chn.dir]);
+      for (int gs : group_si[chn.dir]) {
+        chn.path_streams[0].push_back(gs);
+        chn.path_streams[1].push_back(gs);
+      }
     }
     chn.probe_stream = mk_stream(ENG_CE);
     chn.mon_stream = mk_stream(ENG_CE);
@@ -2191,6 +2202,9 @@ iccl_result_t iccl_group_end(iccl_comm_t c) {
       if (r) return r;
     }
     c->group_jobs.clear();
+    int nth[2] = {0, 0};
+    for (Xfer& x : xs)
+      if (x.group_stream) x.group_lane = nth[c->ch[x.chan].dir]++ % c->group_lanes;
     for (Xfer& x : xs) {
       iccl_result_t r = ready_waits(c, c->ch[x.chan], x);
       if (r) return r;
