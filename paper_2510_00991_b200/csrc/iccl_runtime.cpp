@@ -133,7 +133,7 @@ static uint64_t env_us(const char* name, uint64_t dflt) {
   return v && *v ? strtoull(v, nullptr, 10) : dflt;
 }
 static const uint64_t kSendWaitUs = env_us("ICCL_SEND_WAIT_US", 20);
-static const uint64_t kGroupSendWaitUs = env_us("ICCL_GROUP_SEND_WAIT_US", 200);
+static const uint64_t kGroupSendWaitUs = env_us("ICCL_GROUP_SEND_WAIT_US", 1000);
 
 // ---------------------------------------------------------------- shared control block
 struct alignas(64) ShmHeader {
