@@ -77,6 +77,7 @@ struct DirectOp {
   uint32_t peer_done_gen;
   uint32_t* my_done;                // this side's done flag (request bookkeeping)
   uint32_t my_done_gen;
+  uint32_t* peer_done_dev;          // the other side's done word in its GPU memory (device flags), or null
   unsigned int* counter;            // CTA arrival counter (0 between uses)
   unsigned int* go;                 // CTA 0 -> other CTAs: the peer is ready (device memory, gen-tagged)
   unsigned int* error;              // host-mapped: set to 1 if the wait timed out
@@ -87,6 +88,8 @@ cudaError_t launch_direct(DirectOp op, size_t bytes, int ctas, cudaStream_t st, 
 constexpr int kWaitMax = 32;
 struct WaitList {
   const uint32_t* addr[kWaitMax];
+  const uint32_t* alt[kWaitMax];  // device flags: addr is a word in this GPU's memory and alt the
+                                  // host-mapped flag, read every 64th poll (paths that only write it)
   uint32_t gen[kWaitMax];
   int n;
   unsigned int* error;  // host-mapped: set to 1 if a wait timed out (10 s)

@@ -163,9 +163,10 @@ __global__ void __launch_bounds__(kCopyThreads) iccl_copy_tma(const char* __rest
 __global__ void __launch_bounds__(kCopyThreads) iccl_direct_copy(DirectOp op) {
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) uint64_t mbar[kStages];
-  // one thread of CTA 0 polls the host-mapped ready flag; the other CTAs
+  // one thread of CTA 0 polls the ready flag (host-mapped, or with device
+  // flags a word in the peer GPU's memory read over NVLink); the other CTAs
   // wait on a word in this GPU's memory that it releases (gen-tagged, never
-  // reset), so only one poller crosses PCIe
+  // reset), so only one poller leaves the GPU
   if (threadIdx.x == 0) {
     const unsigned long long t0 = globaltimer();
     uint32_t v;
@@ -196,6 +197,8 @@ __global__ void __launch_bounds__(kCopyThreads) iccl_direct_copy(DirectOp op) {
     if (atomicAdd(op.counter, 1u) == gridDim.x - 1) {
       atomicExch(op.counter, 0u);
       __threadfence_system();
+      if (op.peer_done_dev)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(op.peer_done_dev), "r"(op.peer_done_gen) : "memory");
       asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(op.peer_done), "r"(op.peer_done_gen) : "memory");
       asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(op.my_done), "r"(op.my_done_gen) : "memory");
     }
@@ -417,8 +420,12 @@ __global__ void __launch_bounds__(32) iccl_wait_flags(WaitList wl) {
   const unsigned long long t0 = globaltimer();
   for (int i = 0; i < wl.n; i++) {
     uint32_t v;
+    unsigned polls = 0;
     do {
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(wl.addr[i]) : "memory");
+      if ((int32_t)(v - wl.gen[i]) >= 0) break;
+      if (wl.alt[i] && (++polls & 63) == 0)
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(wl.alt[i]) : "memory");
       if ((int32_t)(v - wl.gen[i]) < 0 && globaltimer() - t0 > 10000000000ull) {
         *wl.error = 1;
         return;

@@ -444,6 +444,7 @@ struct iccl_comm {
   std::vector<GroupJob> group_jobs;  // copy-engine transfers this side issues for the open group
   int direct_ctas = 32;
   bool kernel_waits = true;
+  bool device_flags = true;  // direct-class ready/done words also in GPU memory (ICCL_DEVICE_FLAGS=0: host only)
   int group_lanes = 1;       // group streams per direction (ICCL_GROUP_LANES)  // K7 for the done waits of direct-class ops (ICCL_KERNEL_WAITS=0: memop waits)  // K6 grid (>= 16 CTAs keep NVLink busy, kernels bench)
   std::unordered_map<uint64_t, cudaIpcMemHandle_t> export_cache;
   std::vector<std::unordered_set<uint64_t>> announced;  // per peer: buffer ids announced to it
@@ -1512,6 +1513,24 @@ static iccl_result_t rzv_issue(iccl_comm* c, int kind, int peer, uint64_t k, uin
   return rzv_launch(c, std::move(x), on_proxy);
 }
 
+static size_t ll_slot_offset(int src, uint32_t seq) {
+  return ((size_t)src * kLLSlots + (seq - 1) % kLLSlots) * kLLLines * 8;
+}
+static size_t ll_credit_offset(int nranks, int peer) {
+  return (size_t)nranks * kLLSlots * kLLLines * 8 + (size_t)peer * 64;
+}
+// Device flags of direct-class (K6) ops, after the credits in the LL region:
+// ready[kSlots] then done[kSlots], gen-tagged like the host-mapped flags.  The
+// owner's user stream writes its ready word locally and K6 on the peer polls
+// it over NVLink; K6 stores the done word into the waiting side's GPU memory
+// and K7 there polls local memory instead of the host-mapped flag.
+static size_t dflag_ready_offset(int nranks, uint32_t slot) {
+  return ll_credit_offset(nranks, nranks) + (size_t)slot * 4;
+}
+static size_t dflag_done_offset(int nranks, uint32_t slot) {
+  return ll_credit_offset(nranks, nranks) + ((size_t)kSlots + slot) * 4;
+}
+
 // Rendezvous of the k-th op of an ordered pair (SPEC.md:194's RTS / CTS): post
 // my half (IPC handle, offset, op slot); the side that arrives second has
 // both halves and issues every chunk of the transfer right here, from its own
@@ -1603,6 +1622,11 @@ static iccl_result_t rzv_post(iccl_comm* c, OpDesc& op, uint64_t wait_us, bool g
       d.peer_done_gen = other.gen;
       d.my_done = &flags_of(c, c->rank)->done[op.slot];
       d.my_done_gen = op.gen;
+      d.peer_done_dev = nullptr;
+      if (c->device_flags) {
+        d.peer_ready = (const uint32_t*)(c->peer_ll[peer] + dflag_ready_offset(c->nranks, other.slot));
+        d.peer_done_dev = (uint32_t*)(c->peer_ll[peer] + dflag_done_offset(c->nranks, other.slot));
+      }
       d.counter = c->ll_counters + (c->ll_ctr_next++ % kLLCounters);
       d.go = c->ll_counters + kLLCounters + (op.slot % kLLCounters);
       d.error = c->ll_error;
@@ -1652,6 +1676,10 @@ static iccl_result_t stream_markers(iccl_comm* c, cudaStream_t s, const std::vec
     w.writeValue.value = op.gen;
     w.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
     p.push_back(w);
+    if (op.direct && c->device_flags) {  // the word K6 on the peer polls
+      w.writeValue.address = (CUdeviceptr)(c->ll_region + dflag_ready_offset(c->nranks, op.slot));
+      p.push_back(w);
+    }
   }
   // done waits: a stream memop wait per op — except for direct-class ops
   // (K6 sizes), whose wait is K7: a memop wait on the host-mapped flag cost
@@ -1664,6 +1692,11 @@ static iccl_result_t stream_markers(iccl_comm* c, cudaStream_t s, const std::vec
     if (!(phases & 2)) break;
     if (op.direct && c->kernel_waits) {
       wl.addr[wl.n] = &mine->done[op.slot];
+      wl.alt[wl.n] = nullptr;
+      if (c->device_flags) {  // K6 stores the local word; CE fallbacks only the host flag
+        wl.addr[wl.n] = (const uint32_t*)(c->ll_region + dflag_done_offset(c->nranks, op.slot));
+        wl.alt[wl.n] = &mine->done[op.slot];
+      }
       wl.gen[wl.n] = op.gen;
       if (++wl.n == kWaitMax) {
         kwaits.push_back(wl);
@@ -1690,13 +1723,6 @@ static iccl_result_t stream_markers(iccl_comm* c, cudaStream_t s, const std::vec
     c->ctas_launched += 1;
   }
   return ICCL_SUCCESS;
-}
-
-static size_t ll_slot_offset(int src, uint32_t seq) {
-  return ((size_t)src * kLLSlots + (seq - 1) % kLLSlots) * kLLLines * 8;
-}
-static size_t ll_credit_offset(int nranks, int peer) {
-  return (size_t)nranks * kLLSlots * kLLLines * 8 + (size_t)peer * 64;
 }
 
 // One fused K5 launch per (stream, group): every LL op of the group gets its
@@ -1881,12 +1907,13 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
   cudaDeviceGetPCIBusId(me.bus_id, sizeof(me.bus_id), cuda_dev);
   ICCL_CHECK_CUDA(cudaIpcGetMemHandle(&me.scratch_handle, c->scratch));
   {
-    size_t ll_bytes = ll_credit_offset(nranks, nranks);
+    size_t ll_bytes = dflag_done_offset(nranks, kSlots);
     ICCL_CHECK_CUDA(cudaMalloc((void**)&c->ll_region, ll_bytes));
     ICCL_CHECK_CUDA(cudaMemset(c->ll_region, 0, ll_bytes));
     ICCL_CHECK_CUDA(cudaIpcGetMemHandle(&me.ll_handle, c->ll_region));
     c->ll_error = (unsigned int*)((char*)c->pinned + 56 * 1024);
     c->kernel_waits = env_us("ICCL_KERNEL_WAITS", 1) != 0;
+    c->device_flags = env_us("ICCL_DEVICE_FLAGS", 1) != 0;
     // kLLCounters arrival counters + kLLCounters K6 go words
     ICCL_CHECK_CUDA(cudaMalloc((void**)&c->ll_counters, 2 * kLLCounters * sizeof(unsigned int)));
     ICCL_CHECK_CUDA(cudaMemset(c->ll_counters, 0, 2 * kLLCounters * sizeof(unsigned int)));
