@@ -444,7 +444,7 @@ struct iccl_comm {
   std::vector<GroupJob> group_jobs;  // copy-engine transfers this side issues for the open group
   int direct_ctas = 32;
   bool kernel_waits = true;
-  bool device_flags = true;  // direct-class ready/done words also in GPU memory (ICCL_DEVICE_FLAGS=0: host only)
+  bool device_flags = false;  // direct-class ready/done words also in GPU memory (ICCL_DEVICE_FLAGS=1; slower, profiles/r01/README.md §2)
   int group_lanes = 1;       // group streams per direction (ICCL_GROUP_LANES)  // K7 for the done waits of direct-class ops (ICCL_KERNEL_WAITS=0: memop waits)  // K6 grid (>= 16 CTAs keep NVLink busy, kernels bench)
   std::unordered_map<uint64_t, cudaIpcMemHandle_t> export_cache;
   std::vector<std::unordered_set<uint64_t>> announced;  // per peer: buffer ids announced to it
@@ -1913,7 +1913,7 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
     ICCL_CHECK_CUDA(cudaIpcGetMemHandle(&me.ll_handle, c->ll_region));
     c->ll_error = (unsigned int*)((char*)c->pinned + 56 * 1024);
     c->kernel_waits = env_us("ICCL_KERNEL_WAITS", 1) != 0;
-    c->device_flags = env_us("ICCL_DEVICE_FLAGS", 1) != 0;
+    c->device_flags = env_us("ICCL_DEVICE_FLAGS", 0) != 0;
     // kLLCounters arrival counters + kLLCounters K6 go words
     ICCL_CHECK_CUDA(cudaMalloc((void**)&c->ll_counters, 2 * kLLCounters * sizeof(unsigned int)));
     ICCL_CHECK_CUDA(cudaMemset(c->ll_counters, 0, 2 * kLLCounters * sizeof(unsigned int)));

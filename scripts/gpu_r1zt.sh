@@ -1,0 +1,8 @@
+# round-1 close-out on a 2-GPU box: host-mapped flags back as the default
+export PYTHONUNBUFFERED=1
+R2="python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1"
+timeout 600 python -m pytest tests -x -q -m gpu -p no:cacheprovider > gpurun_out/zt_pytest_gpu2.log 2>&1; echo pytest_rc=$? >> gpurun_out/zt_pytest_gpu2.log
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/zt_smoke.log 2>&1; echo rc=$? >> gpurun_out/zt_smoke.log
+timeout 180 python bench.py > gpurun_out/zt_bench_n1.log 2>&1
+timeout 180 $R2 --master-port 29652 bench.py --gpus 2 > gpurun_out/zt_bench_n2.log 2>&1
+timeout 150 $R2 --master-port 29653 benchmarks/p2p_sweep.py --impl iccl-auto --min-pow 18 --max-pow 26 > gpurun_out/zt_sweep.log 2>&1
