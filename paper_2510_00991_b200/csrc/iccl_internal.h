@@ -78,6 +78,7 @@ struct DirectOp {
   uint32_t* my_done;                // this side's done flag (request bookkeeping)
   uint32_t my_done_gen;
   uint32_t* peer_done_dev;          // the other side's done word in its GPU memory (device flags), or null
+  int vec;                          // 1: register copy (16 B vectors, no smem stage) instead of the TMA ring
   unsigned int* counter;            // CTA arrival counter (0 between uses)
   unsigned int* go;                 // CTA 0 -> other CTAs: the peer is ready (device memory, gen-tagged)
   unsigned int* error;              // host-mapped: set to 1 if the wait timed out

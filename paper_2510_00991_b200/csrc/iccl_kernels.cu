@@ -190,7 +190,16 @@ __global__ void __launch_bounds__(kCopyThreads) iccl_direct_copy(DirectOp op) {
     }
   }
   __syncthreads();
-  tma_copy(op.src, op.dst, op.head, op.body, op.tail, smem, mbar);
+  if (op.vec) {
+    // small ops: every thread moves 16 B vectors straight between the two
+    // tensors, no shared-memory round trip before the first store
+    const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, nt = (size_t)gridDim.x * blockDim.x;
+    copy_bytes(op.src, op.dst, op.head, tid, nt);
+    copy_vec16((const int4*)(op.src + op.head), (int4*)(op.dst + op.head), op.body / 16, tid, nt);
+    copy_bytes(op.src + op.head + op.body, op.dst + op.head + op.body, op.tail, tid, nt);
+  } else {
+    tma_copy(op.src, op.dst, op.head, op.body, op.tail, smem, mbar);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();
@@ -447,11 +456,12 @@ cudaError_t launch_direct(DirectOp op, size_t bytes, int ctas, cudaStream_t st, 
   if (op.head > bytes) op.head = bytes;
   op.body = (bytes - op.head) & ~(size_t)15;
   op.tail = bytes - op.head - op.body;
-  const size_t ntiles = (op.body + kTile - 1) / kTile;
+  const size_t tile = op.vec ? (size_t)kCopyThreads * 16 * 4 : (size_t)kTile;  // vec: one unrolled pass per CTA
+  const size_t ntiles = (op.body + tile - 1) / tile;
   int grid = (int)min((size_t)ctas, ntiles > 0 ? ntiles : (size_t)1);
   if (grid < 1) grid = 1;
   if (grid_out) *grid_out = grid;
-  iccl_direct_copy<<<grid, kCopyThreads, kStages * kTile, st>>>(op);
+  iccl_direct_copy<<<grid, kCopyThreads, op.vec ? 0 : kStages * kTile, st>>>(op);
   return cudaGetLastError();
 }
 

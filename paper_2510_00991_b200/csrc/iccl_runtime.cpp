@@ -444,6 +444,7 @@ struct iccl_comm {
   std::vector<GroupJob> group_jobs;  // copy-engine transfers this side issues for the open group
   int direct_ctas = 32;
   bool kernel_waits = true;
+  size_t k6_vec_bytes = 0;     // K6 copies ops up to this size with registers (ICCL_K6_VEC_KIB)
   bool device_flags = false;  // direct-class ready/done words also in GPU memory (ICCL_DEVICE_FLAGS=1; slower, profiles/r01/README.md §2)
   int group_lanes = 1;       // group streams per direction (ICCL_GROUP_LANES)  // K7 for the done waits of direct-class ops (ICCL_KERNEL_WAITS=0: memop waits)  // K6 grid (>= 16 CTAs keep NVLink busy, kernels bench)
   std::unordered_map<uint64_t, cudaIpcMemHandle_t> export_cache;
@@ -1623,6 +1624,7 @@ static iccl_result_t rzv_post(iccl_comm* c, OpDesc& op, uint64_t wait_us, bool g
       d.my_done = &flags_of(c, c->rank)->done[op.slot];
       d.my_done_gen = op.gen;
       d.peer_done_dev = nullptr;
+      d.vec = op.bytes <= c->k6_vec_bytes;
       if (c->device_flags) {
         d.peer_ready = (const uint32_t*)(c->peer_ll[peer] + dflag_ready_offset(c->nranks, other.slot));
         d.peer_done_dev = (uint32_t*)(c->peer_ll[peer] + dflag_done_offset(c->nranks, other.slot));
@@ -1914,6 +1916,7 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
     c->ll_error = (unsigned int*)((char*)c->pinned + 56 * 1024);
     c->kernel_waits = env_us("ICCL_KERNEL_WAITS", 1) != 0;
     c->device_flags = env_us("ICCL_DEVICE_FLAGS", 0) != 0;
+    c->k6_vec_bytes = (size_t)env_us("ICCL_K6_VEC_KIB", 0) * 1024;
     // kLLCounters arrival counters + kLLCounters K6 go words
     ICCL_CHECK_CUDA(cudaMalloc((void**)&c->ll_counters, 2 * kLLCounters * sizeof(unsigned int)));
     ICCL_CHECK_CUDA(cudaMemset(c->ll_counters, 0, 2 * kLLCounters * sizeof(unsigned int)));
