@@ -339,6 +339,11 @@ struct Xfer {
   // ended, or at the op's anchor recorded right after the ready waits)
   std::vector<std::pair<int, cudaEvent_t>> last_ev;
   std::vector<cudaEvent_t> anchors;  // owned timing events (returned at retire)
+  // issued from this side's API call: the issuing user stream's position at
+  // the op, recorded right there; the copy streams wait on it instead of
+  // polling this side's host-mapped ready flag (same process, same GPU)
+  cudaEvent_t own_ready = nullptr;
+  int own_side = -1;  // 0: stands for the sender's ready flag, 1: the receiver's
 };
 
 struct StreamCtx {
@@ -445,7 +450,8 @@ struct iccl_comm {
   int direct_ctas = 32;
   bool kernel_waits = true;
   size_t k6_vec_bytes = 0;     // K6 copies ops up to this size with registers (ICCL_K6_VEC_KIB)
-  bool device_flags = false;  // direct-class ready/done words also in GPU memory (ICCL_DEVICE_FLAGS=1; slower, profiles/r01/README.md §2)
+  bool device_flags = false;
+  bool event_ready = true;  // same-process ready wait as a CUDA event (ICCL_EVENT_READY=0: memop on the host flag)  // direct-class ready/done words also in GPU memory (ICCL_DEVICE_FLAGS=1; slower, profiles/r01/README.md §2)
   int group_lanes = 1;       // group streams per direction (ICCL_GROUP_LANES)  // K7 for the done waits of direct-class ops (ICCL_KERNEL_WAITS=0: memop waits)  // K6 grid (>= 16 CTAs keep NVLink busy, kernels bench)
   std::unordered_map<uint64_t, cudaIpcMemHandle_t> export_cache;
   std::vector<std::unordered_set<uint64_t>> announced;  // per peer: buffer ids announced to it
@@ -569,6 +575,8 @@ static void put_events(iccl_comm* c, Xfer& x) {
   }
   for (cudaEvent_t e : x.anchors) c->tevent_pool.push_back(e);
   x.anchors.clear();
+  if (x.own_ready) c->event_pool.push_back(x.own_ready);
+  x.own_ready = nullptr;
   x.last_ev.clear();
 }
 
@@ -883,15 +891,28 @@ static int chunk_stream(iccl_comm* c, Channel& chn, const Xfer& x, int path, int
 
 // The ready waits of a transfer's first chunk, enqueued ahead of time (a
 // group's pushes, see iccl_group_end).
+// hostFunc#1 analog: a copy stream may start the op only once both user
+// streams reached it
+static iccl_result_t wait_both_ready(iccl_comm* c, cudaStream_t s, const Xfer& x) {
+  if (x.own_ready && x.own_side == 0) {
+    ICCL_CHECK_CUDA(cudaStreamWaitEvent(s, x.own_ready, 0));
+  } else {
+    iccl_result_t r = memop_wait(s, &flags_of(c, x.src_rank)->ready[x.s_slot], x.s_gen);
+    if (r) return r;
+  }
+  if (x.own_ready && x.own_side == 1) {
+    ICCL_CHECK_CUDA(cudaStreamWaitEvent(s, x.own_ready, 0));
+    return ICCL_SUCCESS;
+  }
+  return memop_wait(s, &flags_of(c, x.dst_rank)->ready[x.r_ready_slot], x.r_ready_gen);
+}
+
 static iccl_result_t ready_waits(iccl_comm* c, Channel& chn, Xfer& x) {
   const int eng = path_engine(c, chn, x.path, x.bytes);
   if (eng != ENG_CE) return ICCL_SUCCESS;
   const int si = chunk_stream(c, chn, x, x.path, eng, 0);
   if (waited_on(x, x.path, si)) return ICCL_SUCCESS;
-  cudaStream_t s = c->streams[si].s;
-  iccl_result_t r = memop_wait(s, &flags_of(c, x.src_rank)->ready[x.s_slot], x.s_gen);
-  if (r) return r;
-  r = memop_wait(s, &flags_of(c, x.dst_rank)->ready[x.r_ready_slot], x.r_ready_gen);
+  iccl_result_t r = wait_both_ready(c, c->streams[si].s, x);
   if (r) return r;
   x.waited[x.path].push_back(si);
   return ICCL_SUCCESS;
@@ -907,10 +928,7 @@ static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
   RankFlags* sender = flags_of(c, x.src_rank);
   RankFlags* receiver = flags_of(c, x.dst_rank);
   if (!waited_on(x, path, si)) {
-    // hostFunc#1 analog: the copy may start only once both user streams reached the op
-    iccl_result_t r = memop_wait(sc.s, &sender->ready[x.s_slot], x.s_gen);
-    if (r) return r;
-    r = memop_wait(sc.s, &receiver->ready[x.r_ready_slot], x.r_ready_gen);
+    iccl_result_t r = wait_both_ready(c, sc.s, x);
     if (r) return r;
     x.waited[path].push_back(si);
   }
@@ -1507,10 +1525,15 @@ static iccl_result_t rzv_launch(iccl_comm* c, Xfer&& x, bool on_proxy) {
 }
 
 static iccl_result_t rzv_issue(iccl_comm* c, int kind, int peer, uint64_t k, uint64_t op_seq, bool on_proxy,
-                               bool group = false) {
+                               bool group = false, cudaStream_t user_s = nullptr) {
   Xfer x;
   iccl_result_t r = rzv_build(c, kind, peer, k, op_seq, group, &x);
   if (r) return r;
+  if (user_s && c->event_ready && peer != c->rank) {
+    x.own_ready = get_event(c);
+    x.own_side = kind;
+    ICCL_CHECK_CUDA(cudaEventRecord(x.own_ready, user_s));
+  }
   return rzv_launch(c, std::move(x), on_proxy);
 }
 
@@ -1560,7 +1583,8 @@ static size_t dflag_done_offset(int nranks, uint32_t slot) {
 // issuing (their sender posted first) go the same way, on a second stream:
 // issued one by one on per-peer streams at enqueue they ran the 4-rank
 // alltoallv at less than half speed (profiles/r01/README.md).
-static iccl_result_t rzv_post(iccl_comm* c, OpDesc& op, uint64_t wait_us, bool group = false) {
+static iccl_result_t rzv_post(iccl_comm* c, OpDesc& op, uint64_t wait_us, bool group = false,
+                              cudaStream_t user_s = nullptr) {
   const int peer = op.peer, kind = op.kind;
   const uint64_t k = kind == 0 ? c->pair_sends[peer]++ : c->pair_recvs[peer]++;
   RzvEntry& e = rzv_entry(c, kind, peer, k);
@@ -1644,7 +1668,7 @@ static iccl_result_t rzv_post(iccl_comm* c, OpDesc& op, uint64_t wait_us, bool g
     c->group_jobs.push_back({kind, peer, k, op.op_seq});
     return ICCL_SUCCESS;
   }
-  return rzv_issue(c, kind, peer, k, op.op_seq, false, false);
+  return rzv_issue(c, kind, peer, k, op.op_seq, false, false, user_s);
 }
 
 // K6 for every op of `ops` this side issues directly, on stream s.
@@ -1802,7 +1826,7 @@ static iccl_result_t enqueue_op(iccl_comm* c, int kind, const void* buf, size_t 
   if (op.ll) {
     op.ll_seq = kind == 0 ? ++c->ll_sent[peer] : ++c->ll_recvd[peer];
   } else if (kind == 1 || c->group_depth == 0) {
-    r = rzv_post(c, op, kind == 0 ? kSendWaitUs : 0, c->group_depth > 0);
+    r = rzv_post(c, op, kind == 0 ? kSendWaitUs : 0, c->group_depth > 0, c->group_depth > 0 ? nullptr : s);
     if (r) return r;
   }  // a send inside a group posts at group_end, after every recv of the group
   c->ranks[c->rank].op_count.fetch_add(1, std::memory_order_relaxed);
@@ -1916,6 +1940,7 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
     c->ll_error = (unsigned int*)((char*)c->pinned + 56 * 1024);
     c->kernel_waits = env_us("ICCL_KERNEL_WAITS", 1) != 0;
     c->device_flags = env_us("ICCL_DEVICE_FLAGS", 0) != 0;
+    c->event_ready = env_us("ICCL_EVENT_READY", 1) != 0;
     c->k6_vec_bytes = (size_t)env_us("ICCL_K6_VEC_KIB", 0) * 1024;
     // kLLCounters arrival counters + kLLCounters K6 go words
     ICCL_CHECK_CUDA(cudaMalloc((void**)&c->ll_counters, 2 * kLLCounters * sizeof(unsigned int)));
