@@ -447,12 +447,12 @@ struct iccl_comm {
     uint64_t k, op_seq;
   };
   std::vector<GroupJob> group_jobs;  // copy-engine transfers this side issues for the open group
-  int direct_ctas = 32;
-  bool kernel_waits = true;
-  size_t k6_vec_bytes = 0;     // K6 copies ops up to this size with registers (ICCL_K6_VEC_KIB)
-  bool device_flags = false;
-  bool event_ready = true;  // same-process ready wait as a CUDA event (ICCL_EVENT_READY=0: memop on the host flag)  // direct-class ready/done words also in GPU memory (ICCL_DEVICE_FLAGS=1; slower, profiles/r01/README.md §2)
-  int group_lanes = 1;       // group streams per direction (ICCL_GROUP_LANES)  // K7 for the done waits of direct-class ops (ICCL_KERNEL_WAITS=0: memop waits)  // K6 grid (>= 16 CTAs keep NVLink busy, kernels bench)
+  int direct_ctas = 32;       // K6 grid (>= 16 CTAs keep NVLink busy, kernels bench)
+  bool kernel_waits = true;   // K7 for the done waits of direct-class ops (ICCL_KERNEL_WAITS=0: memop waits)
+  size_t k6_vec_bytes = 0;    // K6 copies ops up to this size with registers (ICCL_K6_VEC_KIB)
+  bool device_flags = false;  // direct-class ready/done words also in GPU memory (ICCL_DEVICE_FLAGS=1; slower)
+  bool event_ready = false;   // same-process ready wait as a CUDA event (ICCL_EVENT_READY=1; mixed result)
+  int group_lanes = 1;        // group streams per direction (ICCL_GROUP_LANES)
   std::unordered_map<uint64_t, cudaIpcMemHandle_t> export_cache;
   std::vector<std::unordered_set<uint64_t>> announced;  // per peer: buffer ids announced to it
   // proxy
@@ -1940,7 +1940,7 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
     c->ll_error = (unsigned int*)((char*)c->pinned + 56 * 1024);
     c->kernel_waits = env_us("ICCL_KERNEL_WAITS", 1) != 0;
     c->device_flags = env_us("ICCL_DEVICE_FLAGS", 0) != 0;
-    c->event_ready = env_us("ICCL_EVENT_READY", 1) != 0;
+    c->event_ready = env_us("ICCL_EVENT_READY", 0) != 0;
     c->k6_vec_bytes = (size_t)env_us("ICCL_K6_VEC_KIB", 0) * 1024;
     // kLLCounters arrival counters + kLLCounters K6 go words
     ICCL_CHECK_CUDA(cudaMalloc((void**)&c->ll_counters, 2 * kLLCounters * sizeof(unsigned int)));

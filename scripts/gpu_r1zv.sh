@@ -1,4 +1,4 @@
-# same-process ready wait as a CUDA event (ICCL_EVENT_READY=1, default) vs the host-flag memop (=0), 2 GPUs
+# same-process ready wait as a CUDA event (ICCL_EVENT_READY=1) vs the host-flag memop (=0, the default), 2 GPUs
 export PYTHONUNBUFFERED=1
 R2="python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1"
 timeout 600 python -m pytest tests -x -q -m gpu -p no:cacheprovider > gpurun_out/zv_pytest_gpu2.log 2>&1; echo pytest_rc=$? >> gpurun_out/zv_pytest_gpu2.log
