@@ -1,5 +1,9 @@
 """Helpers for the GPU parity tests: seeded payloads and a multi-process
-launcher (one process per GPU, as in production)."""
+launcher (one process per rank, as in production).  Ranks map to GPUs
+round-robin (rank % device_count), so every multi-rank test also runs on a
+one-GPU box: CUDA IPC, the copy engines, stream memops and the SM kernels
+all work between processes that share a device (a "peer" copy is then a
+local HBM copy)."""
 import os
 import socket
 import traceback
@@ -36,11 +40,12 @@ def _worker(rank, world, port, fn, outdir, kwargs):
     sys.stdout = sys.stderr = log
     faulthandler.dump_traceback_later(kwargs.pop("_hang_s", 100), exit=True, file=log)
     try:
-        torch.cuda.set_device(rank)
+        dev = rank % torch.cuda.device_count()  # ranks share GPUs when there are fewer GPUs than ranks
+        torch.cuda.set_device(dev)
         store = dist.TCPStore("127.0.0.1", port, world, rank == 0, wait_for_workers=True)
         from paper_2510_00991_b200 import Communicator, IcclConfig
         cfg = IcclConfig.defaults(**kwargs.pop("config", {}))
-        comm = Communicator(rank, world, rank, cfg, store=store)
+        comm = Communicator(rank, world, dev, cfg, store=store)
         res = fn(comm, rank, world, **kwargs)
         torch.cuda.synchronize()
         comm.destroy()
@@ -89,3 +94,9 @@ def _run_ranks(world: int, fn, tmpdir, timeout: float = 120.0, **kwargs):
     if errs:
         raise AssertionError("\n".join(errs))
     return [dict(np.load(os.path.join(str(tmpdir), f"rank{r}.npz"))) for r in range(world)]
+
+
+def dev_of(rank: int):
+    """The GPU rank `rank` runs on (round-robin over the visible GPUs)."""
+    import torch
+    return torch.device("cuda", rank % torch.cuda.device_count())

@@ -3,13 +3,13 @@ functions run by gpu_helpers.run_ranks, one process per GPU)."""
 import numpy as np
 import torch
 
-from gpu_helpers import payload, to_dev
+from gpu_helpers import dev_of, payload, to_dev
 
 
 def sendrecv_pair(comm, rank, world, sizes, offsets=(0,)):
     """0 -> 1 for each size (and every offset into a larger buffer)."""
     out = {}
-    dev = torch.device("cuda", rank)
+    dev = dev_of(rank)
     for i, n in enumerate(sizes):
         for off in offsets:
             src = payload(n + off, seed=1000 + i)
@@ -26,7 +26,7 @@ def sendrecv_pair(comm, rank, world, sizes, offsets=(0,)):
 
 
 def bidirectional(comm, rank, world, nbytes, iters=3):
-    dev = torch.device("cuda", rank)
+    dev = dev_of(rank)
     peer = 1 - rank
     src = to_dev(payload(nbytes, seed=rank), dev)
     dst = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
@@ -38,7 +38,7 @@ def bidirectional(comm, rank, world, nbytes, iters=3):
 
 
 def ring_shift(comm, rank, world, nbytes):
-    dev = torch.device("cuda", rank)
+    dev = dev_of(rank)
     from paper_2510_00991_b200 import P2POp
     src = to_dev(payload(nbytes, seed=50 + rank), dev)
     dst = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
@@ -48,7 +48,7 @@ def ring_shift(comm, rank, world, nbytes):
 
 
 def alltoallv_uneven(comm, rank, world, row_bytes, splits, seed=7):
-    dev = torch.device("cuda", rank)
+    dev = dev_of(rank)
     send_rows = splits[rank]
     recv_rows = [splits[i][rank] for i in range(world)]
     src = to_dev(payload(sum(send_rows) * row_bytes, seed=seed + rank), dev).view(-1, row_bytes)
@@ -62,7 +62,7 @@ def ll_mixed(comm, rank, world, sizes, rounds=3):
     """Small (LL kernel) and large (copy engine) messages interleaved in one
     group per round, both directions, more LL messages per pair than LL slots."""
     from paper_2510_00991_b200 import P2POp
-    dev = torch.device("cuda", rank)
+    dev = dev_of(rank)
     peer = 1 - rank
     out = {}
     for rd in range(rounds):
@@ -94,7 +94,7 @@ def failover_pair(comm, rank, world, nbytes, fault_chunk, restore_us=0):
     """0 -> 1 with the primary copy path 0->1 Down at `fault_chunk` of the
     first send; the transfer must resume on the SM path at the breakpoint."""
     from paper_2510_00991_b200 import FaultScript
-    dev = torch.device("cuda", rank)
+    dev = dev_of(rank)
     src = payload(nbytes, seed=99)
     fs = FaultScript().down(0, 1, chunk=fault_chunk, op_index=0)
     if restore_us:
@@ -125,7 +125,7 @@ def relay_ring(comm, rank, world, nbytes, iters=2):
     """Every pair of the ring shift forced onto the backup path (relay GPU)
     through the API switch (switch_qp ToBackup), then back to the primary."""
     from paper_2510_00991_b200 import P2POp
-    dev = torch.device("cuda", rank)
+    dev = dev_of(rank)
     to, frm = (rank + 1) % world, (rank - 1) % world
     comm.switch_qp(to, "ToBackup")
     out = {}
@@ -150,7 +150,7 @@ def direct_mixed(comm, rank, world, sizes, rounds=2):
     """Mid-size messages (the direct K6 path) both ways in one group per round,
     mixed with an LL and a copy-engine message, then as single ordered ops."""
     from paper_2510_00991_b200 import P2POp
-    dev = torch.device("cuda", rank)
+    dev = dev_of(rank)
     peer = 1 - rank
     out = {}
     for rd in range(rounds):

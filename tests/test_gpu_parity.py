@@ -3,7 +3,10 @@
 Every comparison is raw-byte (bit-exact).  Single-GPU tests drive the whole
 product path through the C ABI with a world-size-1 communicator (self send /
 recv through the proxy, copy engine, SM kernel, failover and monitor); the
-multi-GPU tests run one process per GPU and skip with fewer GPUs.
+multi-rank tests run one process per rank, mapped onto the visible GPUs
+round-robin, so they never skip: on a one-GPU box 2-8 ranks share cuda:0
+(CUDA IPC, stream memops, K5/K6/K7 and the copy engines all work between
+processes on one device).
 """
 import numpy as np
 import pytest
@@ -22,6 +25,12 @@ def torch_cuda():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch
+
+
+def _world(minimum: int) -> int:
+    """Ranks for a multi-rank test: every GPU, and at least `minimum`."""
+    import torch
+    return max(minimum, torch.cuda.device_count())
 
 
 def _comm1(**cfg):
@@ -232,8 +241,7 @@ def test_errors(torch_cuda):
 
 
 # ---------------------------------------------------------------- multi-GPU
-def test_pair_sendrecv_bytes(need_gpus, tmp_path):
-    need_gpus(2)
+def test_pair_sendrecv_bytes(torch_cuda, tmp_path):
     import gpu_scenarios as sc
     sizes = [8, 4096 + 1, 3 * MiB + 5, 64 * MiB]
     res = run_ranks(2, sc.sendrecv_pair, tmp_path, sizes=sizes, offsets=(0, 3))
@@ -244,29 +252,26 @@ def test_pair_sendrecv_bytes(need_gpus, tmp_path):
 
 
 @pytest.mark.parametrize("transport", ["ce", "sm"])
-def test_pair_bidirectional(need_gpus, tmp_path, transport):
-    need_gpus(2)
+def test_pair_bidirectional(torch_cuda, tmp_path, transport):
     import gpu_scenarios as sc
     res = run_ranks(2, sc.bidirectional, tmp_path, nbytes=64 * MiB + 48, config=dict(transport=transport))
     for r in range(2):
         assert np.array_equal(res[r]["recv"], payload(64 * MiB + 48, seed=1 - r))
 
 
-def test_ring_shift_all_gpus(need_gpus, tmp_path):
-    need_gpus(2)
+def test_ring_shift_all_gpus(torch_cuda, tmp_path):
     import torch
     import gpu_scenarios as sc
-    w = torch.cuda.device_count()
+    w = _world(4)
     res = run_ranks(w, sc.ring_shift, tmp_path, nbytes=32 * MiB)
     for r in range(w):
         assert np.array_equal(res[r]["recv"], payload(32 * MiB, seed=50 + (r - 1) % w))
 
 
-def test_alltoallv_uneven_vs_oracle(need_gpus, tmp_path):
-    need_gpus(2)
+def test_alltoallv_uneven_vs_oracle(torch_cuda, tmp_path):
     import torch
     import gpu_scenarios as sc
-    w = torch.cuda.device_count()
+    w = _world(4)
     rng = np.random.default_rng(0)
     splits = [[int(x) for x in rng.integers(0, 300, w)] for _ in range(w)]
     splits[0][w - 1] = 0  # a zero-count pair
@@ -281,10 +286,9 @@ def test_alltoallv_uneven_vs_oracle(need_gpus, tmp_path):
 
 
 @pytest.mark.parametrize("ll_max", [32 * 1024, 256 * 1024])
-def test_pair_ll_small_messages(need_gpus, tmp_path, ll_max):
+def test_pair_ll_small_messages(torch_cuda, tmp_path, ll_max):
     """LL path (K5) mixed with copy-engine ops in one group, more LL messages
     per pair than slots; at 256 KiB ops span up to 16 CTAs each."""
-    need_gpus(2)
     import gpu_scenarios as sc
     sizes = [1, 3, 4, 7, 64, 1000, 4096, 32 * 1024, 32 * 1024 + 1, 300 * 1024, 5, 6, 8, 9, 64 * 1024 + 5,
              200 * 1024 + 3, 256 * 1024]
@@ -298,8 +302,7 @@ def test_pair_ll_small_messages(need_gpus, tmp_path, ll_max):
             assert np.array_equal(res[r][f"single_{i}"], payload(n, seed=555 + i))
 
 
-def test_pair_failover_mid_message(need_gpus, tmp_path):
-    need_gpus(2)
+def test_pair_failover_mid_message(torch_cuda, tmp_path):
     import gpu_scenarios as sc
     n = 48 * MiB
     res = run_ranks(2, sc.failover_pair, tmp_path, nbytes=n, fault_chunk=5,
@@ -310,15 +313,14 @@ def test_pair_failover_mid_message(need_gpus, tmp_path):
     assert res[issuer]["resume"][0] == 5
 
 
-def test_relay_failover_mid_message(need_gpus, tmp_path):
+def test_relay_failover_mid_message(torch_cuda, tmp_path):
     """Backup = GPU relay (two copy-engine hops through the lowest-index
     non-endpoint GPU): primary 0->1 Down at chunk 3,
     resume through GPU 2 at the breakpoint, bit-exact."""
-    need_gpus(3)
     import torch
     import gpu_scenarios as sc
     n = 48 * MiB + 80
-    res = run_ranks(torch.cuda.device_count(), sc.failover_pair, tmp_path, nbytes=n, fault_chunk=3,
+    res = run_ranks(_world(3), sc.failover_pair, tmp_path, nbytes=n, fault_chunk=3,
                     config=dict(chunk_bytes=4 * MiB, delta_us=300, window=4, backup_kind="relay", relay_slot_mib=3))
     assert np.array_equal(res[1]["recv"], _oracle_sendrecv(payload(n, seed=99)))
     issuer = 0 if len(res[0]["switch_to"]) else 1
@@ -326,11 +328,10 @@ def test_relay_failover_mid_message(need_gpus, tmp_path):
     assert res[issuer]["resume"][0] == 3
 
 
-def test_relay_ring_api_switch(need_gpus, tmp_path):
-    need_gpus(3)
+def test_relay_ring_api_switch(torch_cuda, tmp_path):
     import torch
     import gpu_scenarios as sc
-    w = torch.cuda.device_count()
+    w = _world(3)
     n = 20 * MiB + 16
     res = run_ranks(w, sc.relay_ring, tmp_path, nbytes=n,
                     config=dict(chunk_bytes=8 * MiB, backup_kind="relay", relay_slot_mib=2))
@@ -342,10 +343,9 @@ def test_relay_ring_api_switch(need_gpus, tmp_path):
         assert int(res[r]["path"][0]) == 1
 
 
-def test_pair_direct_mid_size(need_gpus, tmp_path):
+def test_pair_direct_mid_size(torch_cuda, tmp_path):
     """256 KiB < n <= 16 MiB: the side that arrives second runs K6 on its own
     stream (push or pull, zero-copy), bit-exact in groups and single ops."""
-    need_gpus(2)
     import gpu_scenarios as sc
     MiB_ = 1 << 20
     sizes = [300 * 1024 + 5, MiB_, 3 * MiB_ + 7, 16 * MiB_, 1000, 40 * MiB_]
