@@ -371,15 +371,9 @@ def run_product(args):
 
 
 def moe_routing(rank, world, T=4096, k=8, E=64, device="cuda"):
-    """Config 4 routing: expert popularity p_e ~ (e+1)^-0.8,
-    permuted by seed 0; top-8 per token by multinomial with seed 1000+rank."""
-    import torch
-    g = torch.Generator().manual_seed(0)
-    p = torch.arange(1, E + 1, dtype=torch.float64) ** -0.8
-    p = p[torch.randperm(E, generator=g)]
-    g = torch.Generator().manual_seed(1000 + rank)
-    experts = torch.multinomial(p.expand(T, E), k, replacement=False, generator=g)
-    return experts.to(device)
+    """Config 4 routing, see paper_2510_00991_b200.moe.config4_routing."""
+    from paper_2510_00991_b200.moe import config4_routing
+    return config4_routing(rank, T, k, E, device)
 
 
 def run_alltoallv(args):
@@ -410,8 +404,8 @@ def run_alltoallv(args):
         return r.tolist()
 
     plan = plan_dispatch(experts, E, world, counts_exchange)
-    g = torch.Generator(device=dev).manual_seed(2000 + rank)
-    tokens = torch.randint(-32768, 32767, (T, H), dtype=torch.int16, device=dev, generator=g).view(torch.bfloat16)
+    from paper_2510_00991_b200.moe import config4_tokens
+    tokens = config4_tokens(rank, T, H, dev)
     packed = torch.empty(T * k, H, dtype=tokens.dtype, device=dev)
     recv = torch.empty(sum(plan.recv_counts), H, dtype=tokens.dtype, device=dev)
     back = torch.empty_like(packed)

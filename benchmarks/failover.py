@@ -146,8 +146,11 @@ def main():
     recs = comm.monitor.drain()
     ev = comm.switch_events()
     info = torch.zeros(8, device=dev, dtype=torch.float64)
-    if rank == src_r:
-        sw = [e for e in ev if e["peer"] == dst_r]
+    if rank in (src_r, dst_r):
+        # either endpoint may have issued the faulted transfer (a push by the
+        # sender, a pull by the receiver): its watchdog is the one that switched
+        other = dst_r if rank == src_r else src_r
+        sw = [e for e in ev if e["peer"] == other and e["to"] == "backup"]
         if sw:
             e0 = sw[0]
             t_inj = e0["t_ns"] - e0["detect_ns"]
@@ -157,7 +160,7 @@ def main():
             info[3] = 1 if e0["to"] == "backup" and e0["trigger"] == "watchdog" else 0
             # anomaly: first W=8 window sample on the faulted pair after the
             # injection whose throughput is below half the pre-fault median
-            pair = [r for r in pre_recs + recs if r.peer == dst_r]
+            pair = [r for r in pre_recs + recs if r.peer == other]
             samples = iccl.sample_series(pair, 8)
             pre = [s.value for s in samples if s.time < t_inj]
             med = statistics.median(pre) if pre else None
@@ -167,8 +170,8 @@ def main():
                 if bad:
                     info[4] = (bad[0].time - t_inj) / 1e3
                     info[5] = min(s.value for s in bad) / med
-            prim_recs = [r for r in pre_recs + recs if r.path == 0 and r.t2 > r.t1 and r.peer != src_r]
-            back_recs = [r for r in recs if r.path == 1 and r.t2 > r.t1 and r.peer == dst_r]
+            prim_recs = [r for r in pre_recs + recs if r.path == 0 and r.t2 > r.t1 and r.peer != rank]
+            back_recs = [r for r in recs if r.path == 1 and r.t2 > r.t1 and r.peer == other]
             if prim_recs and back_recs:
                 bp = sum(r.size for r in prim_recs) / (sum(r.t2 - r.t1 for r in prim_recs) * 1e-9) / 1e9
                 bb = sum(r.size for r in back_recs) / (sum(r.t2 - r.t1 for r in back_recs) * 1e-9) / 1e9
@@ -190,6 +193,9 @@ def main():
     timed(2)
     ev = comm.switch_events()
     back_ok = torch.tensor([1.0 if (rank != src_r or comm.active_path(dst_r) == "primary") else 0.0], device=dev)
+    sb = torch.tensor([1.0 if any(e["to"] == "primary" for e in ev) else 0.0], device=dev)
+    dist.all_reduce(sb, op=dist.ReduceOp.MAX)
+    res["switch_back_event"] = bool(sb.item() > 0)
     dist.all_reduce(back_ok, op=dist.ReduceOp.MIN)
     res["switched_back_to_primary"] = bool(back_ok.item() > 0)
     res["t_restored_ms"] = round(timed(args.steps), 4)

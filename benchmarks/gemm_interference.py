@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--impl", choices=["iccl-ce", "iccl-sm", "nccl", "none"], required=True)
     ap.add_argument("--reps", type=int, default=30)
     ap.add_argument("--gemms", type=int, default=4)
+    ap.add_argument("--msg-mib", type=float, default=256.0,
+                    help="P2P message per hop (256 = config 3's activation; 1-16 = the K6 mid-size band)")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -45,7 +47,8 @@ def main():
     a = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
     b = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
     c = torch.empty(8192, 8192, device=dev, dtype=torch.bfloat16)
-    act = torch.randint(-32768, 32767, (4, 4096, 8192), dtype=torch.int16, device=dev).view(torch.bfloat16)
+    nel = int(args.msg_mib * (1 << 20)) // 2
+    act = torch.randint(-32768, 32767, (nel,), dtype=torch.int16, device=dev).view(torch.bfloat16)
     rcv = torch.empty_like(act)
     comp = torch.cuda.Stream(device=dev)
     cs = torch.cuda.Stream(device=dev)
@@ -76,16 +79,49 @@ def main():
         if args.impl != "none":
             comm_burst(2)
     torch.cuda.synchronize()
+    # bursts long enough to cover the GEMM window (~3.2 ms): ~4 ms of transfers
+    burst = max(12, int(12 * 256 / max(args.msg_mib, 0.001) * 0.25)) if args.msg_mib < 256 else 12
+    burst = min(burst, 4000)
+    # attribution: SM clock and board power sampled (NVML, every ~2 ms) in
+    # each phase, so a slowdown can be told apart as a clock/power effect
+    # (the power cap pulls the SM clock down when the copy engines and HBM
+    # draw more) or as contention at the same clock
+    samp = {"A": [], "B": []}
+    phase = ["-"]
+    stop = [False]
+    import threading
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(local)
+
+        def sampler():
+            import time as _t
+            while not stop[0]:
+                p = phase[0]
+                if p in samp:
+                    samp[p].append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                                    pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0))
+                _t.sleep(0.002)
+        th = threading.Thread(target=sampler, daemon=True)
+        th.start()
+    except Exception:
+        th = None
     alone, withc = [], []
     order = ["A", "B"] * args.reps
     for ph in order:
         torch.cuda.synchronize()
         dist.barrier()
+        phase[0] = ph
         if ph == "B" and args.impl != "none":
-            comm_burst(12)  # ~4 ms of transfers: covers the GEMM window
+            comm_burst(burst)
         e0, e1 = timed_gemms()
         torch.cuda.synchronize()
+        phase[0] = "-"
         (alone if ph == "A" else withc).append(e0.elapsed_time(e1) / args.gemms)
+    stop[0] = True
+    if th is not None:
+        th.join()
     ratios = [b_ / a_ - 1 for a_, b_ in zip(alone, withc)]
     med = statistics.median(ratios)
     rnd = random.Random(0)
@@ -94,7 +130,13 @@ def main():
     rec = {"impl": args.impl, "rank": rank, "world": world, "gemm_ms_alone": round(statistics.median(alone), 4),
            "gemm_ms_with_comm": round(statistics.median(withc), 4), "slowdown_median": round(med, 5),
            "ci95": [round(boots[50], 5), round(boots[1949], 5)],
-           "tflops_alone": round(flop / (statistics.median(alone) * 1e-3) / 1e12, 1)}
+           "tflops_alone": round(flop / (statistics.median(alone) * 1e-3) / 1e12, 1), "msg_mib": args.msg_mib,
+           "burst_ops": burst}
+    for ph, lab in (("A", "alone"), ("B", "with_comm")):
+        if samp[ph]:
+            rec[f"sm_mhz_{lab}"] = statistics.median(x[0] for x in samp[ph])
+            rec[f"power_w_{lab}"] = round(statistics.median(x[1] for x in samp[ph]), 1)
+            rec[f"samples_{lab}"] = len(samp[ph])
     if comm is not None:
         rec["iccl_stats"] = comm.stats()
         comm.destroy()

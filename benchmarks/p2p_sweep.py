@@ -4,6 +4,12 @@
 same-box NCCL (torch.distributed, NCCL 2.28.9) — the comparison the paper
 makes (PAPER.md:640-666).
 
+NCCL runs in the three modes the paper's comparison must cover:
+``nccl`` (default, SM kernels), ``nccl-ce`` (NCCL_P2P_USE_CUDA_MEMCPY=1, its
+own copy-engine P2P) and ``nccl-zero`` (NCCL_CTA_POLICY=2, the zero-CTA
+policy of nccl.h:66).  ``--bidir`` times both directions at once (each rank
+sends and receives in one batched group).
+
 Two regimes per size, both nccl-tests style (device time, max over ranks):
 * ``gpu``: the whole loop is enqueued behind a ~30 ms device sleep, so the
   GPU runs the ops back to back — per-op device time, host API cost hidden;
@@ -33,7 +39,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--impl", choices=["iccl-ce", "iccl-sm", "iccl-auto", "nccl"], required=True)
+    ap.add_argument("--impl", choices=["iccl-ce", "iccl-sm", "iccl-auto", "nccl", "nccl-ce", "nccl-zero"],
+                    required=True)
+    ap.add_argument("--bidir", action="store_true", help="both directions at once (batched isend + irecv)")
     ap.add_argument("--min-pow", type=int, default=3)
     ap.add_argument("--max-pow", type=int, default=30)
     ap.add_argument("--step", type=int, default=1)
@@ -41,6 +49,10 @@ def main():
     ap.add_argument("--chunk-bytes", type=int, default=0)
     ap.add_argument("--ll-bytes", type=int, default=-1)
     args = ap.parse_args()
+    if args.impl == "nccl-ce":
+        os.environ["NCCL_P2P_USE_CUDA_MEMCPY"] = "1"
+    elif args.impl == "nccl-zero":
+        os.environ["NCCL_CTA_POLICY"] = "2"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -83,7 +95,16 @@ def main():
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) * 1e3  # us
 
+    def both(s, r):
+        if comm:
+            comm.batch_isend_irecv([iccl.P2POp("isend", s, peer), iccl.P2POp("irecv", r, peer)])
+        else:
+            for w in dist.batch_isend_irecv([dist.P2POp(dist.isend, s, peer), dist.P2POp(dist.irecv, r, peer)]):
+                w.wait()
+
     def bw_loop(s, r):
+        if args.bidir:
+            return lambda: both(s, r)
         return lambda: send(s) if rank == 0 else recv(r)
 
     def pp_loop(s, r):
@@ -103,7 +124,7 @@ def main():
         iters = 100 if n <= (4 << 20) else (30 if n <= (64 << 20) else 10)
         for _ in range(3):
             pp_loop(s, r)()
-        rec = {"impl": args.impl, "bytes": n}
+        rec = {"impl": args.impl, "bytes": n, "bidir": bool(args.bidir)}
         for mode, pre in (("gpu", True), ("api", False)):
             t = torch.tensor([timed(bw_loop(s, r), iters, pre) / iters], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -128,7 +149,7 @@ def main():
             dist.all_reduce(d)
             rec["ctas_per_op"] = float(d[0].item()) / 4
             rec["kernels_per_op"] = float(d[1].item()) / 4
-        if rank == 1:
+        if rank == 1 or args.bidir:
             ok = torch.equal(rbuf[:n], buf[:n])
             okt = torch.tensor([1 if ok else 0], device=dev)
         else:

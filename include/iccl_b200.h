@@ -241,6 +241,24 @@ iccl_result_t iccl_sample_series(const iccl_mon_rec_t* recs, int n, int window, 
 /* detect_lagging_rank: *rank = -1 for None. */
 iccl_result_t iccl_detect_lagging_rank(const uint64_t* op_counts, int n, uint64_t threshold, int* rank);
 
+/* ---- self-test hooks (no device needed) ----------------------------------
+ * The two shared-memory protocols of the control block, run on caller-owned
+ * host memory so CPU tests can drive them from several processes:
+ * - small-op routing (LL vs rendezvous) of one ordered pair: both sides must
+ *   route the pair's q-th small op alike while the pair is armed / disarmed
+ *   concurrently (fault scripts, switch_qp) — pair memory of
+ *   iccl_selftest_pair_bytes(), zero-initialised;
+ * - the rendezvous entry of one ordered pair (SPEC.md:194's RTS / CTS): the
+ *   side arriving second claims op k and sees both halves, entries reused
+ *   every 1024 ops — entry memory of iccl_selftest_rzv_bytes(), zeroed.
+ * iccl_selftest_rzv_post returns 0 (posted first), 1 (second: claimed, the
+ * other half's byte count in *other_bytes) or -1 (halves of different ops). */
+size_t iccl_selftest_pair_bytes(void);
+size_t iccl_selftest_rzv_bytes(void);
+int iccl_selftest_route_small(void* pair, int side);
+void iccl_selftest_route_arm(void* pair, int faults_delta, int active_path);
+int iccl_selftest_rzv_post(void* entry, int kind, uint64_t k, uint64_t bytes, uint64_t* other_bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,7 +21,7 @@ from .errors import (Aborted, ConfigError, ConnectionFailed, GroupTooSmall, Iccl
 from .faults import FaultEntry, FaultScript  # noqa: F401
 from .monitor import (MessageRecord, Monitor, ThroughputSample, detect_lagging_rank,  # noqa: F401
                       per_message_throughput, resample, sample_series, window_throughput)
-from .moe import (DispatchPlan, expand_rows, gather_rows, moe_combine, moe_dispatch, plan_dispatch,  # noqa: F401
-                  scatter_rows)
+from .moe import (DispatchPlan, config4_routing, config4_tokens, expand_rows, gather_rows, moe_combine,  # noqa: F401
+                  moe_dispatch, plan_dispatch, scatter_rows)
 
 __version__ = "0.1.0"

@@ -129,6 +129,11 @@ PROTOTYPES = {
     "iccl_sample_series": (_c, [C.POINTER(MonRec), C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(_u64),
                                 C.POINTER(C.c_int)]),
     "iccl_detect_lagging_rank": (_c, [C.POINTER(_u64), C.c_int, _u64, C.POINTER(C.c_int)]),
+    "iccl_selftest_pair_bytes": (_sz, []),
+    "iccl_selftest_rzv_bytes": (_sz, []),
+    "iccl_selftest_route_small": (C.c_int, [_p, C.c_int]),
+    "iccl_selftest_route_arm": (None, [_p, C.c_int, C.c_int]),
+    "iccl_selftest_rzv_post": (C.c_int, [_p, C.c_int, _u64, _u64, C.POINTER(_u64)]),
 }
 
 

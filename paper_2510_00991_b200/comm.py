@@ -59,13 +59,24 @@ class Work:
         return bool(done.value)
 
     def wait(self, timeout_s: Optional[float] = None) -> bool:
-        """Make the current stream wait for the op (device-side), like NCCL Work.wait."""
+        """Make the current stream wait for the op (device-side), like NCCL
+        Work.wait.  With ``timeout_s`` the host also waits for completion and
+        raises IcclTimeout past the deadline (iccl_req_wait)."""
         cur = torch.cuda.current_stream()
         if cur != self.stream:
             ev = torch.cuda.Event()
             ev.record(self.stream)
             cur.wait_event(ev)
+        if timeout_s is not None:
+            self.synchronize(timeout_s)
         return True
+
+    def state(self) -> dict:
+        """TransferState: the six progress pointers of this
+        op, its chunk count, active path and switch count (iccl_req_state)."""
+        st = XferState()
+        raise_for(lib.iccl_req_state(self.comm._h, C.c_uint64(self.req), C.byref(st)), "iccl_req_state")
+        return {f: getattr(st, f) for f, _ in XferState._fields_}
 
     def synchronize(self, timeout_s: float = 60.0) -> None:
         """Host-side wait for completion (iccl_req_wait)."""
@@ -149,6 +160,23 @@ class Communicator:
         err = C.c_int()
         lib.iccl_comm_get_async_error(self._h, C.byref(err))
         raise_for(err.value, "async")
+
+    # -- memory registration (MemoryRegion) -----------------------
+    def register(self, tensor: torch.Tensor) -> int:
+        """Register ``tensor``'s allocation for zero-copy transfers (User Buffer
+        Registration): exported over CUDA IPC once and cached.
+        Unexportable memory raises UnregisteredRegion.  Returns
+        the registration handle (the allocation's buffer id)."""
+        _check_tensor(tensor, "registered tensor")
+        h = C.c_uint64()
+        raise_for(lib.iccl_register(self._h, C.c_void_p(tensor.data_ptr()), tensor.numel() * tensor.element_size(),
+                                    C.byref(h)), "iccl_register")
+        return h.value
+
+    def deregister(self, handle: int) -> None:
+        """Drop a registration; peers that mapped the allocation close their
+        mappings.  No op in flight may still use the buffer."""
+        raise_for(lib.iccl_deregister(self._h, C.c_uint64(int(handle))), "iccl_deregister")
 
     # -- point to point (send_message / send_recv) ---------------------------------
     def isend(self, tensor: torch.Tensor, peer: int, stream: Optional[torch.cuda.Stream] = None) -> Work:

@@ -63,8 +63,11 @@ struct alignas(64) KernelStamp {
 // K1: copy `bytes` from src to dst (dst may be an IPC-mapped peer pointer)
 // with at most `ctas` CTAs; TMA bulk body + vector head/tail.  `stamp` may be
 // null.
+// `resume` (host-mapped, may be null) makes the launch conditional: it copies
+// only if chunk >= *resume when the kernel starts (the pre-enqueued backup
+// attempt of an armed transfer skips the chunks the primary delivered).
 cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, KernelStamp* stamp, cudaStream_t st,
-                        int* grid_out = nullptr);
+                        int* grid_out = nullptr, const uint32_t* resume = nullptr, uint32_t chunk = 0);
 // K6: direct zero-copy of a mid-size message by the side that arrived second
 // at the rendezvous, on its own user stream (see rzv_post).
 struct DirectOp {
@@ -82,6 +85,7 @@ struct DirectOp {
   unsigned int* counter;            // CTA arrival counter (0 between uses)
   unsigned int* go;                 // CTA 0 -> other CTAs: the peer is ready (device memory, gen-tagged)
   unsigned int* error;              // host-mapped: set to 1 if the wait timed out
+  KernelStamp* stamp;               // monitor on: %globaltimer t1 (peer ready seen) / t2 (last CTA done), or null
 };
 cudaError_t launch_direct(DirectOp op, size_t bytes, int ctas, cudaStream_t st, int* grid_out = nullptr);
 // K7: the other side of a direct (K6-class) op waits for its done flags in a
@@ -128,6 +132,7 @@ struct LLDesc {
   uint32_t first_blk;     // first CTA of this op in the launch
   uint32_t nblk;          // CTAs of this op
   unsigned int* counter;  // arrival counter of this op (local HBM, 0 between uses)
+  KernelStamp* stamp;     // send, monitor on: %globaltimer t1 (first CTA starts) / t2 (last CTA done), or null
 };
 struct LLBatch {
   int n;

@@ -10,7 +10,9 @@
 //                     primary-backup pair and as the SM transport.
 // K4  stamps          %globaltimer t1 at the first CTA's start and t2 at the
 //                     last CTA's end, written to a host-mapped KernelStamp
-//                     the proxy turns into a monitor record.
+//                     the proxy turns into a monitor record;
+//                     K1, K5 (sends) and K6 carry it, so every op the SM paths
+//                     move yields a WR/WC record.
 // K2  gather rows     MoE dispatch pack: dst[i] = src[idx[i]] (16 B vectors).
 // K3  scatter rows    MoE combine unpack: dst[idx[i]] = src[i].
 #include <cuda_runtime.h>
@@ -146,9 +148,15 @@ __device__ __forceinline__ void tma_copy(const char* __restrict__ src, char* __r
 // K1.  src/dst share the same alignment mod 16 (checked by the launcher).
 __global__ void __launch_bounds__(kCopyThreads) iccl_copy_tma(const char* __restrict__ src, char* __restrict__ dst,
                                                               size_t head, size_t body, size_t tail,
-                                                              KernelStamp* stamp) {
+                                                              KernelStamp* stamp, const uint32_t* resume,
+                                                              uint32_t chunk) {
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) uint64_t mbar[kStages];
+  if (resume) {  // conditional chunk of a backup attempt: skip what the primary delivered
+    uint32_t r;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(r) : "l"(resume) : "memory");
+    if (chunk < r) return;
+  }
   stamp_begin(stamp);
   tma_copy(src, dst, head, body, tail, smem, mbar);
   stamp_end(stamp);
@@ -179,6 +187,10 @@ __global__ void __launch_bounds__(kCopyThreads) iccl_direct_copy(DirectOp op) {
         }
       } while ((int32_t)(v - op.peer_ready_gen) < 0);
       asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(op.go), "r"(op.my_done_gen) : "memory");
+      if (op.stamp) {  // K4: the WR is posted once the other side is ready
+        const unsigned long long t = globaltimer();
+        asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(&op.stamp->t1), "l"(t) : "memory");
+      }
     } else {
       do {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(op.go) : "memory");
@@ -206,6 +218,10 @@ __global__ void __launch_bounds__(kCopyThreads) iccl_direct_copy(DirectOp op) {
     if (atomicAdd(op.counter, 1u) == gridDim.x - 1) {
       atomicExch(op.counter, 0u);
       __threadfence_system();
+      if (op.stamp) {  // K4: the WC (every CTA's bulk stores are complete)
+        const unsigned long long t = globaltimer();
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&op.stamp->t2), "l"(t) : "memory");
+      }
       if (op.peer_done_dev)
         asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(op.peer_done_dev), "r"(op.peer_done_gen) : "memory");
       asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(op.peer_done), "r"(op.peer_done_gen) : "memory");
@@ -216,7 +232,13 @@ __global__ void __launch_bounds__(kCopyThreads) iccl_direct_copy(DirectOp op) {
 
 // Fallback for buffers whose addresses differ mod 16: byte copy.
 __global__ void __launch_bounds__(512) iccl_copy_unaligned(const char* __restrict__ src, char* __restrict__ dst,
-                                                           size_t n, KernelStamp* stamp) {
+                                                           size_t n, KernelStamp* stamp, const uint32_t* resume,
+                                                           uint32_t chunk) {
+  if (resume) {
+    uint32_t r;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(r) : "l"(resume) : "memory");
+    if (chunk < r) return;
+  }
   stamp_begin(stamp);
   copy_bytes(src, dst, n, blockIdx.x * (size_t)blockDim.x + threadIdx.x, (size_t)gridDim.x * blockDim.x);
   stamp_end(stamp);
@@ -358,6 +380,10 @@ __global__ void __launch_bounds__(256) iccl_ll_group(LLBatch b) {
       }
       __syncthreads();
     }
+    if (d.stamp && part == 0 && threadIdx.x == 0) {  // K4: WR posted (the slot is free)
+      const unsigned long long t = globaltimer();
+      asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(&d.stamp->t1), "l"(t) : "memory");
+    }
     for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
       uint32_t w = 0;
       const size_t off = i * 4;
@@ -373,6 +399,11 @@ __global__ void __launch_bounds__(256) iccl_ll_group(LLBatch b) {
       // last CTA of the op: every CTA read its part of the source
       s_last = d.nblk == 1 || atomicAdd(d.counter, 1u) == d.nblk - 1;
       if (s_last && d.nblk > 1) atomicExch(d.counter, 0u);
+      if (s_last && d.stamp) {  // K4: every line of the op is out
+        __threadfence_system();
+        const unsigned long long t = globaltimer();
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&d.stamp->t2), "l"(t) : "memory");
+      }
       if (s_last && d.done_flag)
         asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(d.done_flag), "r"(d.done_gen) : "memory");
     }
@@ -466,7 +497,7 @@ cudaError_t launch_direct(DirectOp op, size_t bytes, int ctas, cudaStream_t st, 
 }
 
 cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, KernelStamp* stamp, cudaStream_t st,
-                        int* grid_out) {
+                        int* grid_out, const uint32_t* resume, uint32_t chunk) {
   if (grid_out) *grid_out = 0;
   if (bytes == 0) return cudaSuccess;
   const uintptr_t s = (uintptr_t)src, d = (uintptr_t)dst;
@@ -474,7 +505,7 @@ cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, Kern
     int grid = (int)min((size_t)ctas, (bytes + 512 * 16 - 1) / (512 * 16));
     if (grid < 1) grid = 1;
     if (grid_out) *grid_out = grid;
-    iccl_copy_unaligned<<<grid, 512, 0, st>>>((const char*)src, (char*)dst, bytes, stamp);
+    iccl_copy_unaligned<<<grid, 512, 0, st>>>((const char*)src, (char*)dst, bytes, stamp, resume, chunk);
     return cudaGetLastError();
   }
   size_t head = (16 - (s & 15)) & 15;
@@ -490,7 +521,8 @@ cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, Kern
   int grid = (int)min((size_t)ctas, ntiles > 0 ? ntiles : (size_t)1);
   if (grid < 1) grid = 1;
   if (grid_out) *grid_out = grid;
-  iccl_copy_tma<<<grid, kCopyThreads, kStages * kTile, st>>>((const char*)src, (char*)dst, head, body, tail, stamp);
+  iccl_copy_tma<<<grid, kCopyThreads, kStages * kTile, st>>>((const char*)src, (char*)dst, head, body, tail, stamp,
+                                                             resume, chunk);
   return cudaGetLastError();
 }
 

@@ -123,6 +123,7 @@ constexpr int kMaxRanks = 64;
 // probe per 200 us, > 3 s — so every device wait on it has long executed).
 constexpr int kGateWords = 16384;
 constexpr int kStampSlots = 4096;
+constexpr int kArmedSlots = 1024;  // armed transfers in flight per rank
 constexpr size_t kScratchBytes = 4096;
 constexpr int kProxyNapUs = 20;  // proxy back-off when a pass moved nothing
 // How long a send waits for its receiver's half before posting its own (so
@@ -184,6 +185,7 @@ struct RzvSide {
   uint64_t base_offset;  // offset of the tensor inside that allocation
   uint64_t direct_ptr;   // the tensor's pointer in its owner's address space
   uint32_t slot, gen;    // the owner's op slot: ready / done flags and six-pointer record
+  uint64_t stream;       // the owner's user stream (a self pair compares it: same stream => ordered)
   cudaIpcMemHandle_t handle;
 };
 
@@ -197,9 +199,31 @@ struct alignas(64) RzvEntry {
 };
 
 // Per ordered pair src->dst: the active path (shared by whichever side
-// issues) and the rendezvous ring.
+// issues), how many fault-script entries name the pair, and the routing of
+// its small (LL-size) ops.
+//
+// Small ops have no rendezvous: the k-th LL send of a pair meets the k-th LL
+// recv because both sides classify by size.  A pair that is armed for
+// failover (a fault script names it) or runs on its backup path must take
+// the rendezvous / chunked path instead, where gates, the watchdog,
+// switch_qp and the monitor apply — and both sides
+// must agree op by op.  So the route is a history of segments over the
+// pair's small-op index: a change appended under `route_lock` starts at
+// max(ops the sender classified, ops the receiver classified), i.e. after
+// every op either side has already routed, and each side routes its q-th
+// small op by the segment containing q.
+constexpr int kRouteSegs = 512;  // route changes remembered per pair (a side may lag the other by all of them)
 struct alignas(64) PairState {
   std::atomic<int32_t> active_path, switches;
+  std::atomic<int32_t> faults_armed;  // fault-script entries naming the pair (both endpoints' scripts)
+  std::atomic<uint32_t> route_lock;
+  uint64_t small_ops[2];              // small ops routed so far: [0] sender side, [1] receiver side
+  int32_t route_rdv;                  // current route of new small ops: 1 = rendezvous, 0 = LL
+  int32_t route_base;                 // route of ops older than every retained segment
+  uint32_t nseg;                      // segments appended so far (ring of kRouteSegs)
+  uint32_t pad;
+  uint64_t seg_start[kRouteSegs];
+  int32_t seg_rdv[kRouteSegs];
 };
 
 // Buffers src exported to dst (a new CU_POINTER_ATTRIBUTE_BUFFER_ID in one of
@@ -207,6 +231,7 @@ struct alignas(64) PairState {
 constexpr int kAnnDepth = 64;
 struct AnnEntry {
   uint64_t buffer_id;
+  uint64_t retire;  // 1: the owner deregistered the buffer — close its mapping
   cudaIpcMemHandle_t handle;
 };
 struct alignas(64) Announce {
@@ -272,6 +297,21 @@ struct UidBlob {
 
 static inline bool cyc_geq(uint32_t a, uint32_t b) { return (int32_t)(a - b) >= 0; }
 
+// Host-mapped words of one armed transfer (see armed_launch).  Device writes
+// come from stream memops; the watchdog thread only loads and stores them.
+struct alignas(64) ArmedWords {
+  uint32_t prog;        // primary chunks landed (a memop after each primary chunk)
+  uint32_t go;          // the backup attempt may run: the primary finished, or the watchdog switched
+  uint32_t resume;      // backup chunks below this are skipped (nchunks unless switched)
+  uint32_t probe_go;    // the CTS probe may run: the primary finished, or the watchdog suspects a stall
+  uint32_t probe_done;  // the probe crossed the primary path
+  uint32_t ns;          // no switch (1): the primary writes the done flags itself
+  uint32_t p_fin;       // the primary attempt's copies (stale ones included) all landed
+  uint32_t b_fin;       // the backup attempt drained
+  uint32_t fin;         // the primary passed its done writes (the slot may be reused)
+  uint32_t pad[7];
+};
+
 // ---------------------------------------------------------------- proxy-side structures
 // ENG_CE_GROUP: the rank's two group streams — one for the pushes, one for
 // the pulls of a group (alltoallv, batch_isend_irecv) — see rzv_post.
@@ -288,7 +328,10 @@ struct OpDesc {
   uint32_t ll_seq = 0;
   bool direct = false;   // mid-size message: the side arriving second runs K6 on its user stream
   bool issued_direct = false;  // ... and that side is this one: K6 replaces this op's stream markers
+  bool issued_instream = false;  // this side issued the copy on its own user stream (no markers)
+  bool markers_elided = false;   // self pair, both halves on one stream in one group: no markers at all
   DirectOp dop{};        // K6 parameters when issued_direct
+  int kstamp = -1;       // monitor on: K5 send / K6 stamp slot (K4), turned into a record by the proxy
 };
 
 struct ChunkRec {
@@ -344,6 +387,26 @@ struct Xfer {
   // polling this side's host-mapped ready flag (same process, same GPU)
   cudaEvent_t own_ready = nullptr;
   int own_side = -1;  // 0: stands for the sender's ready flag, 1: the receiver's
+  // In-stream issue (a healthy, unarmed pair): the issuing side enqueued every
+  // chunk on its own user stream behind a wait on the other side's ready
+  // flag, and the done writes behind the last chunk.  Such a transfer is not
+  // migrated by switch_qp; it completes where it was posted.
+  cudaStream_t ustream = nullptr;
+  bool instream = false;
+  bool gated = false;          // this attempt placed a chunk behind a closed fault gate
+  bool done_deferred = false;  // ... so its last chunk carries no done writes: the attempt that
+                               // completes the op releases both sides (device writes after the
+                               // fences, or the proxy's host writes once every chunk landed)
+  // Armed transfer (armed_launch): both attempts are on the device from the
+  // start; the watchdog thread drives the failover with host stores only.
+  bool armed = false;
+  int aw = -1;                   // ArmedWords slot
+  std::vector<int> bstamp;       // K4 stamp slot of each backup chunk (its WC)
+  cudaEvent_t p_end = nullptr;   // the primary attempt's end (the backup's fence)
+  bool switched = false;         // the backup attempt carries chunks [resume, N)
+  bool probing = false, probe_ok = false;
+  uint64_t probe_t = 0;
+  uint64_t t_obs = 0;            // host time of the last primary-progress observation (monitor t1)
 };
 
 struct StreamCtx {
@@ -386,6 +449,11 @@ struct Channel {
   uint64_t fault_seq_base = 0;  // pair op count at iccl_fault_set (chunk-triggered faults count from here)
   char* peer_scratch = nullptr;  // 16 B probe target on the peer
   int relay_rank = -1;  // relay GPU of the backup path: lowest rank not an endpoint (topology.py:140-151 tie-break)
+  // armed transfers (owned by the watchdog thread)
+  int b_si = -1;                   // the channel's backup-attempt stream, created on first use
+  std::deque<Xfer> armed;
+  bool armed_failed_over = false;  // the watchdog moved the pair to its backup path
+  uint64_t armed_last_probe = 0;
 };
 
 struct Fault {
@@ -445,6 +513,8 @@ struct iccl_comm {
   struct GroupJob {
     int kind, peer;
     uint64_t k, op_seq;
+    RzvSide side[2];      // both halves, copied before the claim (the entry may be reused after it)
+    cudaStream_t stream;  // this side's user stream
   };
   std::vector<GroupJob> group_jobs;  // copy-engine transfers this side issues for the open group
   int direct_ctas = 32;       // K6 grid (>= 16 CTAs keep NVLink busy, kernels bench)
@@ -458,11 +528,34 @@ struct iccl_comm {
   // proxy
   std::vector<Channel> ch;  // 2 per peer: [2 * peer + dir]
   std::vector<StreamCtx> streams;
+  // per-rank side streams shared by every channel (so N = 8 needs ~22 streams,
+  // under CUDA_DEVICE_MAX_CONNECTIONS = 32): the backup SM-kernel stream, the
+  // CTS probe stream, one monitor stream per direction (push / pull) and the
+  // relay hop-1 stream
+  int sm_si = -1, probe_si = -1, mon_si[2] = {-1, -1}, relay_si = -1;
+  bool instream_ce = true;  // healthy pairs: the issuer enqueues the copy on its own user stream (ICCL_INSTREAM=0: off)
+  // monitor records of ops the proxy does not track (K5 sends, K6): their
+  // %globaltimer stamps (K4), turned into records once t2 lands
+  struct KRec {
+    int stamp;
+    uint64_t bytes, op_seq;
+    int peer, dir;
+  };
+  std::deque<KRec> krecs;  // mon_mu
   std::thread proxy;
   std::atomic<bool> stop{false};
   std::mutex qmu;
   std::condition_variable qcv;
   std::vector<Xfer> handoff;  // issued by the API thread, tracked by the proxy
+  // the watchdog thread (armed transfers): no CUDA calls, so a user thread
+  // blocked in a synchronous CUDA call behind a failing op can never stall
+  // the failover that would release it
+  std::thread watchdog;
+  std::mutex amu;
+  std::vector<Xfer> ahandoff;  // armed transfers issued by the API thread
+  ArmedWords* armed_words = nullptr;
+  std::vector<uint8_t> armed_used;  // API thread sets, watchdog clears (atomic byte ops)
+  uint32_t armed_next = 0;
   std::mutex mon_mu;
   std::deque<iccl_mon_rec_t> mon;
   std::deque<iccl_switch_event_t> sw_events;
@@ -496,6 +589,48 @@ namespace iccl {
 static RankFlags* flags_of(iccl_comm* c, int r) { return &c->flags[r]; }
 static RzvRing* ring_of(iccl_comm* c, int src, int dst) { return &c->rings[src * c->nranks + dst]; }
 static PairState& pair_of(iccl_comm* c, int src, int dst) { return ring_of(c, src, dst)->st; }
+
+// A pair needs the failover-capable (rendezvous, chunked) path when a fault
+// script names it or it runs on its backup path.
+static bool pair_armed(PairState& ps) {
+  return ps.faults_armed.load(std::memory_order_acquire) > 0 || ps.active_path.load(std::memory_order_acquire) != 0;
+}
+
+struct RouteLock {
+  PairState& ps;
+  explicit RouteLock(PairState& p) : ps(p) {
+    uint32_t z = 0;
+    while (!ps.route_lock.compare_exchange_weak(z, 1u, std::memory_order_acquire)) {
+      z = 0;
+      sched_yield();
+    }
+  }
+  ~RouteLock() { ps.route_lock.store(0, std::memory_order_release); }
+};
+
+// Re-evaluate the pair's small-op route after its fault count or active path
+// changed: a new segment starts after every op either side already routed.
+static void route_update(PairState& ps) {
+  RouteLock lk(ps);
+  const int32_t want = pair_armed(ps) ? 1 : 0;
+  if (want == ps.route_rdv) return;
+  const uint32_t n = ps.nseg;
+  if (n >= (uint32_t)kRouteSegs) ps.route_base = ps.seg_rdv[n % kRouteSegs];  // evicted segment
+  ps.seg_start[n % kRouteSegs] = std::max(ps.small_ops[0], ps.small_ops[1]);
+  ps.seg_rdv[n % kRouteSegs] = want;
+  ps.nseg = n + 1;
+  ps.route_rdv = want;
+}
+
+// Route this side's next small op of the pair: true = rendezvous.
+static bool route_small(PairState& ps, int side) {
+  RouteLock lk(ps);
+  const uint64_t q = ps.small_ops[side]++;
+  const uint32_t n = ps.nseg, lo = n > (uint32_t)kRouteSegs ? n - kRouteSegs : 0;
+  for (uint32_t i = n; i-- > lo;)
+    if (ps.seg_start[i % kRouteSegs] <= q) return ps.seg_rdv[i % kRouteSegs] != 0;
+  return ps.route_base != 0;
+}
 
 static void set_async(iccl_comm* c, iccl_result_t e, const std::string& msg) {
   int expected = ICCL_SUCCESS;
@@ -670,13 +805,35 @@ static iccl_result_t map_peer_allocation(iccl_comm* c, int owner, uint64_t buffe
 // pulls (a 10-step alltoallv ran at 3-6 ms/step instead of 1.5, profiles/r01).
 // So each new buffer is announced to the peer on first use, and the peer's
 // proxy opens it in the background.
-static void announce_buffer(iccl_comm* c, int peer, const RzvSide& s) {
-  if (!c->announced[peer].insert(s.buffer_id).second) return;
+static bool announce_entry(iccl_comm* c, int peer, const AnnEntry& en) {
   Announce& a = ring_of(c, c->rank, peer)->ann;
   const uint64_t h = a.head.load(std::memory_order_relaxed);
-  if (h - a.tail.load(std::memory_order_acquire) >= (uint64_t)kAnnDepth) return;  // best effort
-  a.e[h % kAnnDepth] = AnnEntry{s.buffer_id, s.handle};
+  if (h - a.tail.load(std::memory_order_acquire) >= (uint64_t)kAnnDepth) return false;  // best effort
+  a.e[h % kAnnDepth] = en;
   a.head.store(h + 1, std::memory_order_release);
+  return true;
+}
+
+static void announce_buffer(iccl_comm* c, int peer, const RzvSide& s) {
+  if (!c->announced[peer].insert(s.buffer_id).second) return;
+  announce_entry(c, peer, AnnEntry{s.buffer_id, 0, s.handle});
+}
+
+// Peer side of iccl_deregister: drop (and close) the mapping of a buffer its
+// owner retired.  Buffer ids are never reused, so a stale entry could only
+// leak the mapping; closing it lets the owner's memory go.
+static void unmap_peer_allocation(iccl_comm* c, int owner, uint64_t buffer_id) {
+  std::lock_guard<std::mutex> og(c->open_mu);
+  char* base = nullptr;
+  {
+    std::lock_guard<std::mutex> g(c->ipc_mu);
+    auto& cache = c->peer_ipc[owner];
+    auto it = cache.find(buffer_id);
+    if (it == cache.end()) return;
+    base = it->second;
+    cache.erase(it);
+  }
+  cudaIpcCloseMemHandle(base);
 }
 
 // Proxy: open what peers announced (errors are ignored: the owner may have
@@ -690,6 +847,12 @@ static bool premap_peer_buffers(iccl_comm* c) {
     const uint64_t h = a.head.load(std::memory_order_acquire);
     for (; t < h; t++) {
       const AnnEntry en = a.e[t % kAnnDepth];
+      if (en.retire) {
+        unmap_peer_allocation(c, q, en.buffer_id);
+        a.tail.store(t + 1, std::memory_order_release);
+        any = true;
+        continue;
+      }
       char* base = nullptr;
       const uint64_t t0 = now_ns();
       if (map_peer_allocation(c, q, en.buffer_id, en.handle, &base) != ICCL_SUCCESS) cudaGetLastError();
@@ -824,12 +987,16 @@ static bool waited_on(const Xfer& x, int path, int si) {
   return std::find(x.waited[path].begin(), x.waited[path].end(), si) != x.waited[path].end();
 }
 
+// The stream a chunk of `engine` goes to on path `path`.  The channel owns its
+// copy-engine streams (which also carry a small-message pair's K1 primary);
+// the backup K1 stream and the relay hop-1 stream are per rank, shared by all
+// channels; ENG_CE_GROUP picks one of the rank's group streams (lane k).
 static int stream_for(iccl_comm* c, Channel& chn, int path, int engine, int k) {
-  // path_streams[path] holds [CE streams..., SM stream (, relay) (, group)] — pick by engine
-  std::vector<int>& v = chn.path_streams[path];
+  if (engine == ENG_SM && path == 1) return c->sm_si;
+  if (engine == ENG_RELAY) return c->relay_si;
   std::vector<int> cand;
-  for (int si : v)
-    if (c->streams[si].engine == engine) cand.push_back(si);
+  for (int si : chn.path_streams[path])
+    if (c->streams[si].engine == (engine == ENG_CE_GROUP ? ENG_CE_GROUP : ENG_CE)) cand.push_back(si);
   return cand[k % cand.size()];
 }
 
@@ -953,6 +1120,7 @@ static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
     if (chn.fault[path].down) {
       iccl_result_t r = memop_wait(sc.s, &c->gate_words[chn.fault[path].gate], 1);
       if (r) return r;
+      x.gated = true;
     }
   }
   ChunkRec& rc = x.rec[k];
@@ -1021,7 +1189,14 @@ static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
     }
   }
   iccl_result_t r = ICCL_SUCCESS;
-  if (k == x.nchunks - 1) {
+  if (k == x.nchunks - 1 && x.gated) {
+    // Some chunk of this attempt waits behind a closed gate: a switch will
+    // release that gate at once (a parked stream stalls unrelated streams),
+    // so done writes queued here would fire after the flushed stale copies —
+    // while the re-issued suffix is still writing the receiver's buffer and
+    // reading the sender's.  The attempt that completes the op writes them.
+    x.done_deferred = true;
+  } else if (k == x.nchunks - 1) {
     // completion (hostFunc#2 analog): join every stream that carried chunks of
     // this op, plus the fences of paths abandoned by a switch, then release
     // both user streams.
@@ -1052,10 +1227,23 @@ static iccl_result_t issue_chunk(iccl_comm* c, Channel& chn, Xfer& x, int k) {
 // done (contiguous delivered prefix) is where retransmission resumes; posted
 // and transmitted retreat to it; stale in-flight work on the abandoned path is
 // fenced so completion waits for it.
+//
+// Which transfers move: a watchdog switch (trigger 1: the path stalled)
+// migrates every unfinished transfer on the pair.  A voluntary switch (an API
+// switch_qp, trigger 0, or the switch back after a successful probe, trigger
+// 2) leaves a transfer whose done writes are already queued behind its last
+// chunk on a healthy path to finish there — re-issuing it would let those
+// writes release both user streams while the re-issued copies still run —
+// and moves the rest from their next chunk on, without retreat.  In-stream
+// transfers are never moved (their copies sit on the user's stream).
 static iccl_result_t switch_path(iccl_comm* c, Channel& chn, int to, int trigger) {
   PairState& ps = pair_of(c, chn.src, chn.dst);
+  const bool voluntary = trigger != 1;
+  auto movable = [&](const Xfer& x) {
+    return x.path != to && !x.instream && !(voluntary && x.done_enqueued && !x.gated);
+  };
   bool moves = false;
-  for (Xfer& x : chn.xfers) moves |= x.path != to;
+  for (Xfer& x : chn.xfers) moves |= movable(x);
   if (!moves && ps.active_path.load() == to) return ICCL_SUCCESS;
   const int from = to ^ 1;
   std::unique_lock<std::mutex> lk(c->fault_mu);
@@ -1063,7 +1251,18 @@ static iccl_result_t switch_path(iccl_comm* c, Channel& chn, int to, int trigger
   int resume = -1;
   int stale_gate = chn.fault[from].down ? chn.fault[from].gate : -1;
   for (Xfer& x : chn.xfers) {
-    if (x.path == to) continue;
+    if (!movable(x)) continue;
+    if (voluntary && !x.gated) {
+      // healthy path: chunks already queued there complete there; the rest
+      // (and the done writes, which join every stream the op used) go on the
+      // new path
+      if (resume < 0) resume = x.next_issue;
+      x.path = to;
+      x.switches++;
+      x.last_progress = now_ns();
+      publish(c, x);
+      continue;
+    }
     // fence: an event after everything already queued on the abandoned path
     bool had_work = x.next_issue > x.completed || x.done_enqueued;
     if (had_work) {
@@ -1080,6 +1279,8 @@ static iccl_result_t switch_path(iccl_comm* c, Channel& chn, int to, int trigger
     x.next_issue = x.completed;
     x.path = to;
     x.done_enqueued = false;
+    x.gated = false;
+    x.done_deferred = false;
     x.switches++;
     x.last_progress = now_ns();
     publish(c, x);
@@ -1098,6 +1299,7 @@ static iccl_result_t switch_path(iccl_comm* c, Channel& chn, int to, int trigger
   chn.failed_over = (to == 1 && trigger == 1);
   ps.active_path.store(to);
   ps.switches.fetch_add(1);
+  route_update(ps);
   chn.probe_out = false;  // abandon the outstanding probe
   chn.last_probe = now_ns();
   ICCL_TRACE("switch pair %d->%d to path %d at chunk %d (trigger %d, detect %llu ns)", chn.src, chn.dst, to, resume,
@@ -1218,6 +1420,20 @@ static iccl_result_t progress_channel(iccl_comm* c, Channel& chn, bool* busy) {
       x.last_progress = tnow;
       *busy = true;
     }
+    if (x.done_deferred && !x.done_enqueued && x.completed == x.nchunks) {
+      // every chunk of a gated attempt landed (its gate opened): release both
+      // user streams from the host once the fenced stale copies (if any) and
+      // the relay's forwarding drained
+      bool drained = !(x.relay_r >= 0 && !cyc_geq(__atomic_load_n(&relay_out(c, x.relay_r, c->rank)->v,
+                                                                  __ATOMIC_ACQUIRE), x.relay_last_q));
+      for (cudaEvent_t fe : x.fences) drained = drained && cudaEventQuery(fe) == cudaSuccess;
+      if (drained) {
+        __atomic_store_n(&flags_of(c, x.dst_rank)->done[x.r_done_slot], x.r_done_gen, __ATOMIC_SEQ_CST);
+        __atomic_store_n(&flags_of(c, x.src_rank)->done[x.s_slot], x.s_gen, __ATOMIC_SEQ_CST);
+        x.done_enqueued = true;
+        *busy = true;
+      }
+    }
     publish(c, x);
   }
   // 3. retire completed xfers (their done writes are queued on the device)
@@ -1258,8 +1474,9 @@ static iccl_result_t progress_channel(iccl_comm* c, Channel& chn, bool* busy) {
     }
     if (stalled || x.next_issue < x.nchunks) break;
   }
-  // 5. watchdog + probe (check_receiver_timeout)
-  if (!chn.xfers.empty()) {
+  // 5. watchdog + probe (check_receiver_timeout); in-stream
+  // transfers cannot be migrated, so they are not watched
+  if (!chn.xfers.empty() && !chn.xfers.front().instream) {
     Xfer& x = chn.xfers.front();
     bool elig = cyc_geq(flags_of(c, x.src_rank)->ready[x.s_slot], x.s_gen) &&
                 cyc_geq(flags_of(c, x.dst_rank)->ready[x.r_ready_slot], x.r_ready_gen);
@@ -1315,6 +1532,36 @@ static iccl_result_t monitor_failed_link(iccl_comm* c, Channel& chn) {
   return ICCL_SUCCESS;
 }
 
+// Monitor records of K5 sends and K6 ops (the proxy does not track them as
+// transfers): emitted once the kernel's t2 stamp lands, in completion order.
+static bool drain_kstamps(iccl_comm* c) {
+  std::lock_guard<std::mutex> g(c->mon_mu);
+  bool any = false;
+  for (auto it = c->krecs.begin(); it != c->krecs.end();) {
+    KernelStamp* st = &c->stamps[it->stamp];
+    const unsigned long long t2 = __atomic_load_n(&st->t2, __ATOMIC_ACQUIRE);
+    if (!t2) {
+      ++it;
+      continue;
+    }
+    const unsigned long long t1 = __atomic_load_n(&st->t1, __ATOMIC_ACQUIRE);
+    iccl_mon_rec_t m{};
+    m.t1_ns = (uint64_t)((int64_t)(t1 ? t1 : t2) + c->gtimer_offset);
+    m.t2_ns = (uint64_t)((int64_t)t2 + c->gtimer_offset);
+    m.bytes = it->bytes;
+    m.peer = it->peer;
+    m.path = ICCL_PATH_PRIMARY;
+    m.chunk = 0;
+    m.dir = it->dir;
+    m.op_seq = it->op_seq;
+    c->mon.push_back(m);
+    if (c->mon.size() > (1u << 20)) c->mon.pop_front();
+    it = c->krecs.erase(it);
+    any = true;
+  }
+  return any;
+}
+
 static void proxy_loop(iccl_comm* c) {
   cudaSetDevice(c->dev);
   if (c->cfg.proxy_cpu >= 0) {
@@ -1348,6 +1595,7 @@ static void proxy_loop(iccl_comm* c) {
     }
     fire_time_faults(c);
     busy |= premap_peer_buffers(c);
+    busy |= drain_kstamps(c);
     for (int ci = 0; ci < 2 * c->nranks; ci++) {
       Channel& chn = c->ch[ci];
       int req = c->path_req[ci].exchange(-1);
@@ -1438,20 +1686,32 @@ static bool rzv_claim(RzvEntry& e, uint64_t k) {
   return e.claimed.compare_exchange_strong(g, g + 1, std::memory_order_acq_rel);
 }
 
-// Issue the whole transfer of rendezvous entry k of the pair (as `kind`: 0 =
-// push by the sender, 1 = pull by the receiver) after winning its claim:
-// every chunk goes to the channel's copy stream behind waits on both user
-// streams' ready flags, the last one writes both done flags.  From the API
-// thread the transfer is handed to the proxy; from the proxy it is tracked
-// in place.
+// The entry holds op k's halves once both sides arrived for its previous
+// generation and that transfer was claimed (its halves were copied out).
+static bool rzv_free(const RzvEntry& e, uint64_t k) {
+  const uint64_t g = k / kRzvDepth;
+  return e.arrivals.load(std::memory_order_acquire) >= 2 * g && e.claimed.load(std::memory_order_acquire) >= g;
+}
+
+// Count my arrival at op k (my half is already in e.side): the side that
+// arrives second copies both halves out and claims the transfer; true then.
+static bool rzv_arrive(RzvEntry& e, uint64_t k, RzvSide snap[2]) {
+  const uint64_t g = k / kRzvDepth;
+  if (e.arrivals.fetch_add(1, std::memory_order_acq_rel) != 2 * g + 1) return false;
+  snap[0] = e.side[0];  // before the claim: after it a peer kRzvDepth ops ahead may reuse the entry
+  snap[1] = e.side[1];
+  return rzv_claim(e, k);  // cannot fail: the first side never claims
+}
+
 // Build the transfer of rendezvous entry k of the pair (as `kind`: 0 = push
-// by the sender, 1 = pull by the receiver) after winning its claim; no
-// device work yet.
-static iccl_result_t rzv_build(iccl_comm* c, int kind, int peer, uint64_t k, uint64_t op_seq, bool group, Xfer* out) {
-  RzvEntry& e = rzv_entry(c, kind, peer, k);
+// by the sender, 1 = pull by the receiver) from the entry's two halves
+// `side`, copied out of the shared entry before the claim (after the claim a
+// peer up to kRzvDepth ops ahead may already reuse it); no device work yet.
+static iccl_result_t rzv_build(iccl_comm* c, int kind, int peer, uint64_t k, uint64_t op_seq, bool group,
+                               const RzvSide* side, Xfer* out) {
   const int src = kind == 0 ? c->rank : peer, dst = kind == 0 ? peer : c->rank;
-  const RzvSide& snd = e.side[0];
-  const RzvSide& rcv = e.side[1];
+  const RzvSide& snd = side[0];
+  const RzvSide& rcv = side[1];
   if (snd.bytes != rcv.bytes) {
     // release both streams so nothing hangs, and report the mismatch
     __atomic_store_n(&flags_of(c, src)->done[snd.slot], snd.gen, __ATOMIC_SEQ_CST);
@@ -1471,9 +1731,9 @@ static iccl_result_t rzv_build(iccl_comm* c, int kind, int peer, uint64_t k, uin
   x.dst_rank = dst;
   x.chan = ci;
   char* other = nullptr;
-  iccl_result_t r = open_peer_buffer(c, chn, e.side[kind ^ 1], &other);
+  iccl_result_t r = open_peer_buffer(c, chn, side[kind ^ 1], &other);
   if (r) return r;
-  char* own = (char*)(uintptr_t)e.side[kind].direct_ptr;
+  char* own = (char*)(uintptr_t)side[kind].direct_ptr;
   x.src = kind == 0 ? own : other;
   x.dst = kind == 0 ? other : own;
   x.bytes = snd.bytes;
@@ -1499,9 +1759,25 @@ static iccl_result_t rzv_build(iccl_comm* c, int kind, int peer, uint64_t k, uin
   return ICCL_SUCCESS;
 }
 
-// Enqueue every chunk of a built transfer (each behind waits on both user
-// streams' ready flags, the last one writing both done flags) and hand it to
-// the proxy — or, issued by the proxy itself, track it in place.
+// Hand an issued transfer to the proxy (completions, six pointers, monitor,
+// watchdog) — or, issued by the proxy itself, track it in place.
+static void rzv_track(iccl_comm* c, Xfer&& x, bool on_proxy) {
+  publish(c, x);
+  c->pending_xfers.fetch_add(1);
+  if (on_proxy) {
+    c->ch[x.chan].xfers.push_back(std::move(x));
+    return;
+  }
+  {
+    std::lock_guard<std::mutex> gl(c->qmu);
+    c->handoff.push_back(std::move(x));
+  }
+  c->qcv.notify_one();
+}
+
+// Enqueue every chunk of a built transfer on the side streams (each behind
+// waits on both user streams' ready flags, the last one writing both done
+// flags) and hand it to the proxy.
 static iccl_result_t rzv_launch(iccl_comm* c, Xfer&& x, bool on_proxy) {
   Channel& chn = c->ch[x.chan];
   while (x.next_issue < x.nchunks) {
@@ -1510,31 +1786,560 @@ static iccl_result_t rzv_launch(iccl_comm* c, Xfer&& x, bool on_proxy) {
     if (r) return r;
     x.next_issue++;
   }
-  publish(c, x);
-  c->pending_xfers.fetch_add(1);
-  if (on_proxy) {
-    chn.xfers.push_back(std::move(x));
-    return ICCL_SUCCESS;
-  }
-  {
-    std::lock_guard<std::mutex> gl(c->qmu);
-    c->handoff.push_back(std::move(x));
-  }
-  c->qcv.notify_one();
+  rzv_track(c, std::move(x), on_proxy);
   return ICCL_SUCCESS;
 }
 
-static iccl_result_t rzv_issue(iccl_comm* c, int kind, int peer, uint64_t k, uint64_t op_seq, bool on_proxy,
-                               bool group = false, cudaStream_t user_s = nullptr) {
+static iccl_result_t rzv_issue(iccl_comm* c, int kind, int peer, uint64_t k, uint64_t op_seq, const RzvSide* side,
+                               cudaStream_t user_s) {
   Xfer x;
-  iccl_result_t r = rzv_build(c, kind, peer, k, op_seq, group, &x);
+  iccl_result_t r = rzv_build(c, kind, peer, k, op_seq, false, side, &x);
   if (r) return r;
   if (user_s && c->event_ready && peer != c->rank) {
     x.own_ready = get_event(c);
     x.own_side = kind;
     ICCL_CHECK_CUDA(cudaEventRecord(x.own_ready, user_s));
   }
-  return rzv_launch(c, std::move(x), on_proxy);
+  return rzv_launch(c, std::move(x), false);
+}
+
+// ---------------------------------------------------------------- in-stream issue
+// May the issuing side put the copy on its own user stream?  Only for a
+// healthy pair that no fault script names (a stalled in-stream copy could not
+// be migrated: its successors are the caller's own work) on the copy-engine
+// transport — and, for a self pair, only when the other half's done wait
+// cannot sit in front of the copy on that same stream (it does when it was
+// posted outside this group on this stream).
+static bool instream_ok(iccl_comm* c, int kind, int peer, const RzvSide* side, bool other_in_group,
+                        cudaStream_t user_s) {
+  if (!c->instream_ce) return false;
+  if (peer == c->rank && !other_in_group && side[kind ^ 1].stream == (uint64_t)(uintptr_t)user_s) return false;
+  return true;
+}
+
+// Is the transfer's pair armed for failover (a fault script names it, it
+// runs on its backup path, or one of its paths is Down right now)?
+static bool xfer_armed(iccl_comm* c, int kind, int peer) {
+  const int src = kind == 0 ? c->rank : peer, dst = kind == 0 ? peer : c->rank;
+  if (pair_armed(pair_of(c, src, dst))) return true;
+  std::lock_guard<std::mutex> g(c->fault_mu);
+  const Channel& chn = c->ch[2 * peer + kind];
+  return chn.fault[0].down || chn.fault[1].down;
+}
+
+// The issuing side's wait for the other side's ready flag (hostFunc #1).
+static void instream_ready_param(iccl_comm* c, const Xfer& x, int kind, std::vector<CUstreamBatchMemOpParams>& p) {
+  CUstreamBatchMemOpParams w;
+  memset(&w, 0, sizeof(w));
+  w.waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
+  w.waitValue.address = kind == 0 ? (CUdeviceptr)&flags_of(c, x.dst_rank)->ready[x.r_ready_slot]
+                                  : (CUdeviceptr)&flags_of(c, x.src_rank)->ready[x.s_slot];
+  w.waitValue.value = kind == 0 ? x.r_ready_gen : x.s_gen;
+  w.waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+  p.push_back(w);
+}
+
+// Both done flags (hostFunc #2): the other side's user stream waits on its
+// own; this side's is for iccl_req_test / slot reuse.
+static void instream_done_params(iccl_comm* c, const Xfer& x, std::vector<CUstreamBatchMemOpParams>& p) {
+  CUstreamBatchMemOpParams w;
+  memset(&w, 0, sizeof(w));
+  w.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+  w.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
+  w.writeValue.address = (CUdeviceptr)&flags_of(c, x.dst_rank)->done[x.r_done_slot];
+  w.writeValue.value = x.r_done_gen;
+  p.push_back(w);
+  w.writeValue.address = (CUdeviceptr)&flags_of(c, x.src_rank)->done[x.s_slot];
+  w.writeValue.value = x.s_gen;
+  p.push_back(w);
+}
+
+static iccl_result_t batch_memops(cudaStream_t s, std::vector<CUstreamBatchMemOpParams>& p) {
+  for (size_t i = 0; i < p.size(); i += 128) {
+    unsigned n = (unsigned)std::min<size_t>(128, p.size() - i);
+    ICCL_CHECK_CU(driver()->cuStreamBatchMemOp((CUstream)s, n, p.data() + i, 0));
+  }
+  p.clear();
+  return ICCL_SUCCESS;
+}
+
+// The chunk copies of an in-stream transfer on user stream s — copy-engine
+// copies, or K1 launches for the SM transport / small messages — each
+// followed by its WC: an event after a copy (with the monitor on, the
+// direction's monitor stream records a timing event behind every WC and an
+// anchor at the op's start, so chunk times come from the device with nothing
+// timed between the copies), or K1's own %globaltimer stamp (K4).
+static iccl_result_t instream_copies(iccl_comm* c, Xfer& x, cudaStream_t s) {
+  Channel& chn = c->ch[x.chan];
+  const bool mon = c->monitor_enabled.load(std::memory_order_relaxed);
+  const int eng = path_engine(c, chn, 0, x.bytes);
+  cudaStream_t ms = c->streams[chn.mon_stream].s;
+  cudaEvent_t last = nullptr;
+  if (mon && eng == ENG_CE) {
+    last = get_tevent(c);
+    x.anchors.push_back(last);
+    ICCL_CHECK_CUDA(cudaEventRecord(chn.bridge, s));
+    ICCL_CHECK_CUDA(cudaStreamWaitEvent(ms, chn.bridge, 0));
+    ICCL_CHECK_CUDA(cudaEventRecord(last, ms));
+  }
+  for (int k = 0; k < x.nchunks; k++) {
+    const size_t off = (size_t)k * x.chunk, n = std::min(x.chunk, x.bytes - off);
+    ChunkRec& rc = x.rec[k];
+    rc.t1 = now_ns();
+    rc.path = 0;
+    rc.stream = -1;
+    rc.stamp = -1;
+    rc.done = false;
+    c->copies_issued += 1;
+    c->bytes_issued += n;
+    if (eng == ENG_SM) {
+      KernelStamp* st = nullptr;
+      if (mon) {
+        rc.stamp = c->next_stamp.fetch_add(1) % kStampSlots;
+        st = &c->stamps[rc.stamp];
+        memset((void*)st, 0, sizeof(KernelStamp));
+      }
+      int grid = 0;
+      ICCL_CHECK_CUDA(launch_copy(x.src + off, x.dst + off, n, c->cfg.sm_cap, st, s, &grid));
+      c->kernels_launched += 1;
+      c->ctas_launched += grid;
+      if (st) continue;  // the stamp is the WC
+    } else {
+      ICCL_CHECK_CU(driver()->cuMemcpyDtoDAsync((CUdeviceptr)(x.dst + off), (CUdeviceptr)(x.src + off), n,
+                                                (CUstream)s));
+    }
+    if (!rc.ev) rc.ev = get_event(c);
+    ICCL_CHECK_CUDA(cudaEventRecord(rc.ev, s));
+    if (mon && eng == ENG_CE) {
+      rc.tev = get_tevent(c);
+      ICCL_CHECK_CUDA(cudaStreamWaitEvent(ms, rc.ev, 0));
+      ICCL_CHECK_CUDA(cudaEventRecord(rc.tev, ms));
+      rc.t1ev = last;
+      last = rc.tev;
+    }
+  }
+  x.next_issue = x.nchunks;
+  x.instream = true;
+  x.ustream = s;
+  x.done_enqueued = true;
+  return ICCL_SUCCESS;
+}
+
+// One in-stream transfer outside a group: ready wait, copies, done writes.
+static iccl_result_t issue_instream(iccl_comm* c, Xfer&& x, int kind, cudaStream_t s) {
+  std::vector<CUstreamBatchMemOpParams> p;
+  instream_ready_param(c, x, kind, p);
+  iccl_result_t r = batch_memops(s, p);
+  if (r) return r;
+  r = instream_copies(c, x, s);
+  if (r) return r;
+  instream_done_params(c, x, p);
+  r = batch_memops(s, p);
+  if (r) return r;
+  rzv_track(c, std::move(x), false);
+  return ICCL_SUCCESS;
+}
+
+// ---------------------------------------------------------------- armed transfers
+// A transfer on a pair armed for failover (a fault script names it) carries
+// both attempts on the device from the start, so the failover needs no CUDA
+// call at run time: a user thread sitting in a synchronous CUDA call (a
+// pageable copy, .item()) behind the failing op blocks every other CUDA call
+// of its process, and a proxy that still had to enqueue the backup would
+// deadlock with it (probes/p2p_probe6, tests/test_gpu_failover.py).
+//
+//   primary, on the issuer's user stream U (in-stream) or the channel's copy
+//   stream (then behind waits on both ready flags):
+//     wait the other side's ready flag; per chunk k: [fault gate, if Down]
+//     copy k, prog := k + 1; then p_fin := 1, probe_go := 1, go := 1;
+//     wait ns (no-switch gate, open); both done flags; fin := 1
+//   backup, on the channel's backup stream B:
+//     wait probe_go; [fault gate, if Down] 16-byte CTS probe over the primary
+//     path; probe_done := 1; wait go; per chunk k: K1 copying chunk k only if
+//     k >= resume (resume = N unless switched), its K4 stamp is the WC;
+//     b_fin := 1
+//
+// No fault: the primary releases both sides itself (one memop wait on an open
+// gate more than a plain in-stream transfer); B's K1 launches find resume = N
+// and return at once.  A stall (both ready flags set, no progress for delta):
+// the watchdog thread opens probe_go; a probe that does not land within delta
+// means the path is dead — the primary is then parked on
+// the same gate, in front of ns — so, with host stores only: ns := 0,
+// resume := completed (the receiver's breakpoint), go := 1, and
+// the stale gate opens: the primary's flushed copies rewrite bytes B
+// delivers.  Once every backup chunk landed and p_fin is set,
+// the watchdog writes both done flags and reopens ns.
+static iccl_result_t backup_stream(iccl_comm* c, Channel& chn, cudaStream_t* out) {
+  if (chn.b_si < 0) {
+    int lo, hi;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    StreamCtx sc;
+    ICCL_CHECK_CUDA(cudaStreamCreateWithPriority(&sc.s, cudaStreamNonBlocking, hi));
+    ICCL_CHECK_CUDA(cudaEventCreateWithFlags(&sc.ev, cudaEventDisableTiming));
+    sc.engine = ENG_SM;
+    c->streams.push_back(sc);
+    chn.b_si = (int)c->streams.size() - 1;
+  }
+  *out = c->streams[chn.b_si].s;
+  return ICCL_SUCCESS;
+}
+
+// The device-driven failover covers a transfer that starts on the primary
+// with the SM backup; the relay backup and transfers issued on the backup
+// path run the proxy-driven chunk pipeline (rzv_launch).
+static bool armed_eligible(iccl_comm* c, const Xfer& x) {
+  return x.path == 0 && c->cfg.backup_kind == ICCL_BACKUP_SM;
+}
+
+static CUstreamBatchMemOpParams wparam(uint32_t* addr, uint32_t v) {
+  CUstreamBatchMemOpParams q;
+  memset(&q, 0, sizeof(q));
+  q.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+  q.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
+  q.writeValue.address = (CUdeviceptr)addr;
+  q.writeValue.value = v;
+  return q;
+}
+
+// instream: the primary goes on the issuer's user stream `us` (waiting on
+// the other side's ready flag only); else on the channel's copy stream behind
+// waits on both ready flags (the issuer's own op then carries markers).
+static iccl_result_t armed_launch(iccl_comm* c, Xfer&& x, int kind, cudaStream_t us, bool instream) {
+  Channel& chn = c->ch[x.chan];
+  uint64_t t0 = now_ns();
+  int slot = -1;
+  while (slot < 0) {
+    for (int i = 0; i < kArmedSlots && slot < 0; i++) {
+      const uint32_t j = (c->armed_next + i) % kArmedSlots;
+      if (!__atomic_load_n(&c->armed_used[j], __ATOMIC_ACQUIRE)) slot = (int)j;
+    }
+    ICCL_RETURN_IF(slot < 0 && now_ns() - t0 > 60ull * 1000000000ull, ICCL_ERR_TIMEOUT,
+                   "more than 1024 armed transfers in flight for 60 s");
+    if (slot < 0) sched_yield();
+  }
+  c->armed_next = (uint32_t)(slot + 1) % kArmedSlots;
+  __atomic_store_n(&c->armed_used[slot], (uint8_t)1, __ATOMIC_RELEASE);
+  ArmedWords* w = &c->armed_words[slot];
+  memset((void*)w, 0, sizeof(*w));
+  w->resume = (uint32_t)x.nchunks;
+  w->ns = 1;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  x.armed = true;
+  x.aw = slot;
+  // primary attempt
+  const int eng = path_engine(c, chn, 0, x.bytes);
+  cudaStream_t ps = instream ? us : c->streams[stream_for(c, chn, 0, ENG_CE, 0)].s;
+  std::vector<CUstreamBatchMemOpParams> p;
+  iccl_result_t r;
+  if (instream) {
+    // this side's ready flag too (the watchdog tells an upstream stall of
+    // either side by the two flags), then the wait on the other side's
+    p.push_back(kind == 0 ? wparam(&flags_of(c, x.src_rank)->ready[x.s_slot], x.s_gen)
+                          : wparam(&flags_of(c, x.dst_rank)->ready[x.r_ready_slot], x.r_ready_gen));
+    instream_ready_param(c, x, kind, p);
+    r = batch_memops(ps, p);
+  } else {
+    r = wait_both_ready(c, ps, x);
+  }
+  if (r) return r;
+  for (int k = 0; k < x.nchunks; k++) {
+    const size_t off = (size_t)k * x.chunk, n = std::min(x.chunk, x.bytes - off);
+    {
+      std::lock_guard<std::mutex> g(c->fault_mu);
+      if (x.fault_ops_index >= 0) fire_chunk_faults(c, chn, x.fault_ops_index, k, 0);
+      if (chn.fault[0].down) {
+        r = memop_wait(ps, &c->gate_words[chn.fault[0].gate], 1);
+        if (r) return r;
+        x.gated = true;
+      }
+    }
+    x.rec[k].t1 = now_ns();
+    x.rec[k].path = 0;
+    if (eng == ENG_SM) {
+      int grid = 0;
+      ICCL_CHECK_CUDA(launch_copy(x.src + off, x.dst + off, n, c->cfg.sm_cap, nullptr, ps, &grid));
+      c->kernels_launched += 1;
+      c->ctas_launched += grid;
+    } else {
+      ICCL_CHECK_CU(driver()->cuMemcpyDtoDAsync((CUdeviceptr)(x.dst + off), (CUdeviceptr)(x.src + off), n,
+                                                (CUstream)ps));
+    }
+    c->copies_issued += 1;
+    c->bytes_issued += n;
+    r = memop_write(ps, &w->prog, (uint32_t)(k + 1));
+    if (r) return r;
+  }
+  p.push_back(wparam(&w->p_fin, 1));
+  p.push_back(wparam(&w->probe_go, 1));
+  p.push_back(wparam(&w->go, 1));
+  r = batch_memops(ps, p);
+  if (r) return r;
+  r = memop_wait(ps, &w->ns, 1);
+  if (r) return r;
+  instream_done_params(c, x, p);
+  p.push_back(wparam(&w->fin, 1));
+  r = batch_memops(ps, p);
+  if (r) return r;
+  x.next_issue = x.nchunks;
+  x.instream = instream;
+  x.ustream = instream ? us : nullptr;
+  // backup attempt
+  cudaStream_t bs = nullptr;
+  r = backup_stream(c, chn, &bs);
+  if (r) return r;
+  r = memop_wait(bs, &w->probe_go, 1);
+  if (r) return r;
+  {
+    std::lock_guard<std::mutex> g(c->fault_mu);
+    if (chn.fault[0].down) {  // the CTS crosses the primary path: a Down path loses it
+      r = memop_wait(bs, &c->gate_words[chn.fault[0].gate], 1);
+      if (r) return r;
+    }
+  }
+  if (chn.dir == 0)
+    ICCL_CHECK_CU(driver()->cuMemcpyDtoDAsync((CUdeviceptr)chn.peer_scratch, (CUdeviceptr)c->scratch, 16, (CUstream)bs));
+  else
+    ICCL_CHECK_CU(driver()->cuMemcpyDtoDAsync((CUdeviceptr)(c->scratch + 2048 + 16 * chn.peer),
+                                              (CUdeviceptr)chn.peer_scratch, 16, (CUstream)bs));
+  r = memop_write(bs, &w->probe_done, 1);
+  if (r) return r;
+  r = memop_wait(bs, &w->go, 1);
+  if (r) return r;
+  {
+    std::lock_guard<std::mutex> g(c->fault_mu);
+    if (chn.fault[1].down) {  // the backup path itself is Down
+      r = memop_wait(bs, &c->gate_words[chn.fault[1].gate], 1);
+      if (r) return r;
+    }
+  }
+  x.bstamp.assign(x.nchunks, -1);
+  for (int k = 0; k < x.nchunks; k++) {
+    const size_t off = (size_t)k * x.chunk, n = std::min(x.chunk, x.bytes - off);
+    const int st = c->next_stamp.fetch_add(1) % kStampSlots;
+    memset((void*)&c->stamps[st], 0, sizeof(KernelStamp));
+    x.bstamp[k] = st;
+    int grid = 0;
+    ICCL_CHECK_CUDA(launch_copy(x.src + off, x.dst + off, n, c->cfg.sm_cap, &c->stamps[st], bs, &grid, &w->resume,
+                                (uint32_t)k));
+    c->kernels_launched += 1;
+    c->ctas_launched += grid;
+  }
+  r = memop_write(bs, &w->b_fin, 1);
+  if (r) return r;
+  x.done_enqueued = true;
+  x.t_obs = now_ns();
+  publish(c, x);
+  c->pending_xfers.fetch_add(1);
+  {
+    std::lock_guard<std::mutex> g(c->amu);
+    c->ahandoff.push_back(std::move(x));
+  }
+  return ICCL_SUCCESS;
+}
+
+// ---------------------------------------------------------------- watchdog thread
+static void armed_record(iccl_comm* c, const Channel& chn, const Xfer& x, int k, uint64_t t1, uint64_t t2) {
+  iccl_mon_rec_t m{};
+  m.t1_ns = t1;
+  m.t2_ns = t2;
+  m.bytes = std::min(x.chunk, x.bytes - (size_t)k * x.chunk);
+  m.peer = chn.peer;
+  m.path = x.switched && k >= (int)c->armed_words[x.aw].resume ? ICCL_PATH_BACKUP : ICCL_PATH_PRIMARY;
+  m.chunk = k;
+  m.dir = chn.dir;
+  m.op_seq = x.op_seq;
+  std::lock_guard<std::mutex> g(c->mon_mu);
+  c->mon.push_back(m);
+  if (c->mon.size() > (1u << 20)) c->mon.pop_front();
+}
+
+// switch_qp of an armed transfer whose primary is parked on a dead path
+// (SPEC.md:255-263): host stores only.
+static void armed_switch(iccl_comm* c, Channel& chn, Xfer& x) {
+  ArmedWords* w = &c->armed_words[x.aw];
+  const uint64_t t = now_ns();
+  uint64_t detect = 0;
+  int stale = -1;
+  {
+    std::lock_guard<std::mutex> g(c->fault_mu);
+    if (chn.fault[0].down) {
+      detect = t - chn.fault[0].down_at;
+      stale = chn.fault[0].gate;
+      chn.fault[0].gate = alloc_gate(c);  // later work on the still-Down path waits on a fresh epoch
+    }
+  }
+  __atomic_store_n(&w->ns, 0u, __ATOMIC_SEQ_CST);  // the primary (parked on the gate) must not release the op
+  __atomic_store_n(&w->resume, (uint32_t)x.completed, __ATOMIC_SEQ_CST);  // breakpoint = receiver done
+  __atomic_store_n(&w->go, 1u, __ATOMIC_SEQ_CST);
+  __atomic_store_n(&w->probe_go, 1u, __ATOMIC_SEQ_CST);
+  if (stale >= 0) release_gate(c, stale);  // the primary drains: its flushed copies rewrite delivered bytes
+  x.switched = true;
+  x.path = 1;
+  x.switches++;
+  x.last_progress = t;
+  publish(c, x);
+  PairState& ps = pair_of(c, chn.src, chn.dst);
+  if (ps.active_path.exchange(1) != 1) {
+    ps.switches.fetch_add(1);
+    route_update(ps);
+  }
+  chn.armed_failed_over = true;
+  chn.armed_last_probe = t;
+  ICCL_TRACE("armed switch pair %d->%d to backup at chunk %d", chn.src, chn.dst, x.completed);
+  push_switch_event(c, chn.peer, 1, x.completed, 1, detect);
+}
+
+// One watchdog pass over a channel's armed transfers.
+static bool armed_progress(iccl_comm* c, Channel& chn) {
+  bool busy = false;
+  const uint64_t tnow = now_ns();
+  const bool mon = c->monitor_enabled.load(std::memory_order_relaxed);
+  for (Xfer& x : chn.armed) {
+    ArmedWords* w = &c->armed_words[x.aw];
+    if (!x.switched) {
+      // primary chunks: t2 = when this (spinning) thread saw the progress
+      // word move; chunks seen landing in one pass share the interval evenly
+      const int p = std::min((int)__atomic_load_n(&w->prog, __ATOMIC_ACQUIRE), x.nchunks);
+      const int m = p - x.completed;
+      for (int j = 0; j < m; j++) {
+        const uint64_t a = x.t_obs + (tnow - x.t_obs) * j / m, b = x.t_obs + (tnow - x.t_obs) * (j + 1) / m;
+        if (mon) armed_record(c, chn, x, x.completed, a, b);
+        x.completed++;
+      }
+      if (m > 0) {
+        x.t_obs = tnow;
+        x.last_progress = tnow;
+        busy = true;
+      }
+    } else {
+      while (x.completed < x.nchunks) {
+        KernelStamp* st = &c->stamps[x.bstamp[x.completed]];
+        const unsigned long long t2 = __atomic_load_n(&st->t2, __ATOMIC_ACQUIRE);
+        if (!t2) break;
+        if (mon) {
+          const unsigned long long t1 = __atomic_load_n(&st->t1, __ATOMIC_ACQUIRE);
+          armed_record(c, chn, x, x.completed, (uint64_t)((int64_t)(t1 ? t1 : t2) + c->gtimer_offset),
+                       (uint64_t)((int64_t)t2 + c->gtimer_offset));
+        }
+        x.completed++;
+        x.last_progress = tnow;
+        busy = true;
+      }
+      if (x.completed == x.nchunks && __atomic_load_n(&w->ns, __ATOMIC_ACQUIRE) == 0 &&
+          __atomic_load_n(&w->p_fin, __ATOMIC_ACQUIRE)) {
+        // every backup chunk landed and the primary drained: complete the op
+        __atomic_store_n(&flags_of(c, x.dst_rank)->done[x.r_done_slot], x.r_done_gen, __ATOMIC_SEQ_CST);
+        __atomic_store_n(&flags_of(c, x.src_rank)->done[x.s_slot], x.s_gen, __ATOMIC_SEQ_CST);
+        __atomic_store_n(&w->ns, 1u, __ATOMIC_SEQ_CST);  // lets the parked primary pass (its done writes repeat)
+        busy = true;
+      }
+    }
+    publish(c, x);
+  }
+  // retire: the primary passed its done writes and the backup drained
+  while (!chn.armed.empty()) {
+    Xfer& x = chn.armed.front();
+    ArmedWords* w = &c->armed_words[x.aw];
+    if (!__atomic_load_n(&w->fin, __ATOMIC_ACQUIRE) || !__atomic_load_n(&w->b_fin, __ATOMIC_ACQUIRE)) break;
+    if (!x.switched) {  // the last primary chunks may land between two passes
+      const int m = x.nchunks - x.completed;
+      for (int j = 0; j < m; j++) {
+        const uint64_t a = x.t_obs + (tnow - x.t_obs) * j / m, b = x.t_obs + (tnow - x.t_obs) * (j + 1) / m;
+        if (mon) armed_record(c, chn, x, x.completed, a, b);
+        x.completed++;
+      }
+    }
+    x.completed = x.nchunks;
+    publish(c, x);
+    __atomic_store_n(&c->armed_used[x.aw], (uint8_t)0, __ATOMIC_RELEASE);
+    chn.armed.pop_front();
+    c->pending_xfers.fetch_sub(1);
+    busy = true;
+  }
+  // watchdog + CTS probe (check_receiver_timeout) on the front
+  if (!chn.armed.empty()) {
+    Xfer& x = chn.armed.front();
+    ArmedWords* w = &c->armed_words[x.aw];
+    const bool elig = cyc_geq(flags_of(c, x.src_rank)->ready[x.s_slot], x.s_gen) &&
+                      cyc_geq(flags_of(c, x.dst_rank)->ready[x.r_ready_slot], x.r_ready_gen);
+    if (!elig) {
+      x.last_progress = tnow;  // innocent stall upstream: a side's stream has not reached the op
+      x.t_obs = tnow;
+    } else if (!x.eligible) {
+      x.eligible = true;
+      x.last_progress = tnow;
+      x.t_obs = tnow;
+    }
+    const uint64_t delta = c->cfg.delta_us * 1000ull;
+    if (elig && x.completed < x.nchunks && tnow - x.last_progress > delta) {
+      if (!x.switched) {
+        if (!x.probing && !x.probe_ok) {
+          __atomic_store_n(&w->probe_go, 1u, __ATOMIC_SEQ_CST);
+          x.probing = true;
+          x.probe_t = tnow;
+        } else if (x.probing && __atomic_load_n(&w->probe_done, __ATOMIC_ACQUIRE)) {
+          x.probing = false;  // CTS ok: an innocent stall
+          x.probe_ok = true;
+          x.last_progress = tnow;
+        } else if (x.probing && tnow - x.probe_t > delta) {
+          x.probing = false;
+          armed_switch(c, chn, x);  // CTS lost: the path is dead
+          busy = true;
+        }
+      } else {
+        bool backup_down;
+        {
+          std::lock_guard<std::mutex> g(c->fault_mu);
+          backup_down = chn.fault[1].down;
+        }
+        if (backup_down)  // both paths dead
+          set_async(c, ICCL_ERR_CONNECTION_FAILED, "both paths of pair " + std::to_string(chn.src) + "->" +
+                                                       std::to_string(chn.dst) + " are down");
+      }
+    }
+  }
+  // monitor_failed_link: once the primary is healthy again,
+  // later transfers use it (in-flight ones finish on the backup)
+  if (chn.armed_failed_over && tnow - chn.armed_last_probe >= c->cfg.probe_period_us * 1000ull) {
+    chn.armed_last_probe = tnow;
+    bool up;
+    {
+      std::lock_guard<std::mutex> g(c->fault_mu);
+      up = !chn.fault[0].down;
+    }
+    PairState& ps = pair_of(c, chn.src, chn.dst);
+    if (up) {
+      chn.armed_failed_over = false;
+      if (ps.active_path.exchange(0) != 0) {
+        ps.switches.fetch_add(1);
+        route_update(ps);
+      }
+      push_switch_event(c, chn.peer, 0, -1, 2, 0);
+    }
+  }
+  return busy;
+}
+
+static void watch_loop(iccl_comm* c) {
+  std::vector<Xfer> batch;
+  while (!c->stop.load(std::memory_order_relaxed)) {
+    {
+      std::lock_guard<std::mutex> g(c->amu);
+      batch.swap(c->ahandoff);
+    }
+    for (Xfer& x : batch) c->ch[x.chan].armed.push_back(std::move(x));
+    batch.clear();
+    bool any = false, busy = false;
+    for (Channel& chn : c->ch) {
+      if (chn.armed.empty() && !chn.armed_failed_over) continue;
+      any = true;
+      busy |= armed_progress(c, chn);
+    }
+    // spin while armed transfers are in flight (the monitor's host-observed
+    // t2 for primary chunks is as fine as this loop), nap otherwise
+    if (!any) std::this_thread::sleep_for(std::chrono::microseconds(50));
+    else if (!busy) sched_yield();
+  }
 }
 
 static size_t ll_slot_offset(int src, uint32_t seq) {
@@ -1555,10 +2360,26 @@ static size_t dflag_done_offset(int nranks, uint32_t slot) {
   return ll_credit_offset(nranks, nranks) + ((size_t)kSlots + slot) * 4;
 }
 
+// Monitor on: a K4 stamp slot for a K5 send / K6 op, whose record the proxy
+// emits once the kernel's t2 lands (drain_kstamps).
+static KernelStamp* alloc_kstamp(iccl_comm* c, OpDesc& op) {
+  if (!c->monitor_enabled.load(std::memory_order_relaxed)) return nullptr;
+  op.kstamp = c->next_stamp.fetch_add(1) % kStampSlots;
+  KernelStamp* st = &c->stamps[op.kstamp];
+  memset((void*)st, 0, sizeof(KernelStamp));
+  return st;
+}
+
+static void push_krec(iccl_comm* c, const OpDesc& op, int dir) {
+  if (op.kstamp < 0) return;
+  std::lock_guard<std::mutex> g(c->mon_mu);
+  c->krecs.push_back(iccl_comm::KRec{op.kstamp, op.bytes, op.op_seq, op.peer, dir});
+}
+
 // Rendezvous of the k-th op of an ordered pair (SPEC.md:194's RTS / CTS): post
 // my half (IPC handle, offset, op slot); the side that arrives second has
-// both halves and issues every chunk of the transfer right here, from its own
-// API call — a push by the sender or a pull by the receiver.
+// both halves and issues the transfer right here, from its own API call — a
+// push by the sender or a pull by the receiver.
 //
 // Why the API call and not the proxy: while any thread of a process sits in a
 // synchronous CUDA call on a stream parked behind one of our ops (a pageable
@@ -1566,6 +2387,14 @@ static size_t dflag_done_offset(int nranks, uint32_t slot) {
 // kernel launch, stream memop, event record alike (probes/p2p_probe6.cu).  A
 // proxy that still had to enqueue the copy deadlocks with such a user; with
 // all device work enqueued before the API returns nothing can.
+//
+// What the issuer enqueues: on a healthy pair no fault script names, the
+// copy-engine copies go on its own user stream (in-stream: one wait on the
+// other side's ready flag, the copies, one write of both done flags — the
+// stream orders the rest); otherwise on the channel's side streams behind
+// waits on both ready flags, where gates, the watchdog, switch_qp and the
+// monitor's re-issue apply.  Mid-size ops take K6 on the user stream unless
+// the pair is armed.
 //
 // Why senders try to come second: a copy-engine pull runs ~5% slower than a
 // push (probes/p2p_probe6.cu), and the paper's transfers are sender-driven.
@@ -1579,20 +2408,14 @@ static size_t dflag_done_offset(int nranks, uint32_t slot) {
 // 4-rank alltoallv ended up pushing into the same receiver at once (incast,
 // each at half rate: MoE records, profiles/r01/README.md).  On one stream the
 // rotated order of iccl_alltoallv (step k: rank i -> i + k) holds, so at each
-// step every receiver has one sender.  The pulls a group's recvs end up
-// issuing (their sender posted first) go the same way, on a second stream:
-// issued one by one on per-peer streams at enqueue they ran the 4-rank
-// alltoallv at less than half speed (profiles/r01/README.md).
-static iccl_result_t rzv_post(iccl_comm* c, OpDesc& op, uint64_t wait_us, bool group = false,
-                              cudaStream_t user_s = nullptr) {
+// step every receiver has one sender.
+static iccl_result_t rzv_post(iccl_comm* c, OpDesc& op, uint64_t wait_us, bool group, cudaStream_t user_s) {
   const int peer = op.peer, kind = op.kind;
   const uint64_t k = kind == 0 ? c->pair_sends[peer]++ : c->pair_recvs[peer]++;
   RzvEntry& e = rzv_entry(c, kind, peer, k);
   const uint64_t g = k / kRzvDepth;
-  // the entry is reused once both sides arrived for its previous generation
-  // and that transfer was claimed
   uint64_t t0 = now_ns();
-  while (e.arrivals.load(std::memory_order_acquire) < 2 * g || e.claimed.load(std::memory_order_acquire) < g) {
+  while (!rzv_free(e, k)) {
     if (c->async_err.load() != ICCL_SUCCESS) return (iccl_result_t)c->async_err.load();
     if (c->hdr->abort.load()) return ICCL_ERR_ABORTED;
     if (now_ns() - t0 > 60ull * 1000000000ull) {
@@ -1614,6 +2437,7 @@ static iccl_result_t rzv_post(iccl_comm* c, OpDesc& op, uint64_t wait_us, bool g
   mine.slot = op.slot;
   mine.gen = op.gen;
   mine.direct_ptr = (uint64_t)(uintptr_t)op.src;
+  mine.stream = (uint64_t)(uintptr_t)user_s;
   mine.buffer_id = 0;
   mine.base_offset = 0;
   if (peer != c->rank) {
@@ -1621,19 +2445,20 @@ static iccl_result_t rzv_post(iccl_comm* c, OpDesc& op, uint64_t wait_us, bool g
     if (r) return r;
     announce_buffer(c, peer, mine);
   }
-  if (e.arrivals.fetch_add(1, std::memory_order_acq_rel) != 2 * g + 1) {
+  RzvSide side[2];
+  if (!rzv_arrive(e, k, side)) {
     ICCL_TRACE("%s %d->%d #%llu posted first", kind == 0 ? "send" : "recv", kind == 0 ? c->rank : peer,
                kind == 0 ? peer : c->rank, (unsigned long long)k);
     return ICCL_SUCCESS;  // first: the peer issues
   }
-  if (!rzv_claim(e, k)) return ICCL_SUCCESS;  // cannot happen: the first side never claims
   if (kind == 1 && peer != c->rank) c->pulls_issued += 1;
-  if (op.direct) {
-    const RzvSide& other = e.side[kind ^ 1];
+  const int src = kind == 0 ? c->rank : peer, dst = kind == 0 ? peer : c->rank;
+  if (op.direct && !pair_armed(pair_of(c, src, dst))) {
+    const RzvSide& other = side[kind ^ 1];
     // K6's TMA ring needs both tensors at the same alignment mod 16 (an IPC
     // mapping is page-aligned, so the peer's offset decides); else the copy
     // engine path below takes it
-    if (((uintptr_t)op.src & 15) == (other.base_offset & 15) && e.side[0].bytes == e.side[1].bytes) {
+    if (((uintptr_t)op.src & 15) == (other.base_offset & 15) && side[0].bytes == side[1].bytes) {
       char* mapped = nullptr;
       Channel& chn = c->ch[2 * peer + kind];
       iccl_result_t r = open_peer_buffer(c, chn, other, &mapped);
@@ -1656,19 +2481,43 @@ static iccl_result_t rzv_post(iccl_comm* c, OpDesc& op, uint64_t wait_us, bool g
       d.counter = c->ll_counters + (c->ll_ctr_next++ % kLLCounters);
       d.go = c->ll_counters + kLLCounters + (op.slot % kLLCounters);
       d.error = c->ll_error;
+      d.stamp = alloc_kstamp(c, op);
       op.issued_direct = true;
-      ICCL_TRACE("direct %s pair %d->%d #%llu, %zu B", kind == 0 ? "push" : "pull", kind == 0 ? c->rank : peer,
-                 kind == 0 ? peer : c->rank, (unsigned long long)k, op.bytes);
+      ICCL_TRACE("direct %s pair %d->%d #%llu, %zu B", kind == 0 ? "push" : "pull", src, dst,
+                 (unsigned long long)k, op.bytes);
       return ICCL_SUCCESS;
     }
   }
   if (group) {
-    // a group's pushes are launched together once the whole group has met
+    // a group's transfers are launched together once the whole group has met
     // its peers (iccl_group_end): all ready waits first, then the copies
-    c->group_jobs.push_back({kind, peer, k, op.op_seq});
+    iccl_comm::GroupJob j{kind, peer, k, op.op_seq, {side[0], side[1]}, user_s};
+    c->group_jobs.push_back(j);
     return ICCL_SUCCESS;
   }
-  return rzv_issue(c, kind, peer, k, op.op_seq, false, false, user_s);
+  // the issue decision: armed pairs take the device-driven failover pipeline,
+  // healthy ones the plain in-stream copy; the side-stream pipeline covers the
+  // rest (a self pair whose other half waits on this very stream, the relay
+  // backup, transfers issued on the backup path)
+  const bool stream_ok = instream_ok(c, kind, peer, side, false, user_s);
+  if (xfer_armed(c, kind, peer)) {
+    Xfer x;
+    iccl_result_t r = rzv_build(c, kind, peer, k, op.op_seq, false, side, &x);
+    if (r) return r;
+    if (armed_eligible(c, x)) {
+      op.issued_instream = stream_ok;
+      return armed_launch(c, std::move(x), kind, user_s, stream_ok);
+    }
+    return rzv_launch(c, std::move(x), false);
+  }
+  if (stream_ok) {
+    Xfer x;
+    iccl_result_t r = rzv_build(c, kind, peer, k, op.op_seq, false, side, &x);
+    if (r) return r;
+    op.issued_instream = true;
+    return issue_instream(c, std::move(x), kind, user_s);
+  }
+  return rzv_issue(c, kind, peer, k, op.op_seq, side, user_s);
 }
 
 // K6 for every op of `ops` this side issues directly, on stream s.
@@ -1681,6 +2530,7 @@ static iccl_result_t launch_direct_ops(iccl_comm* c, cudaStream_t s, const std::
     c->ctas_launched += grid;
     c->copies_issued += 1;
     c->bytes_issued += op.bytes;
+    push_krec(c, op, op.kind);  // dir: 0 pushed by this rank, 1 pulled
   }
   return ICCL_SUCCESS;
 }
@@ -1738,10 +2588,8 @@ static iccl_result_t stream_markers(iccl_comm* c, cudaStream_t s, const std::vec
     w.waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
     p.push_back(w);
   }
-  for (size_t i = 0; i < p.size(); i += 128) {
-    unsigned n = (unsigned)std::min<size_t>(128, p.size() - i);
-    ICCL_CHECK_CU(driver()->cuStreamBatchMemOp((CUstream)s, n, p.data() + i, 0));
-  }
+  iccl_result_t r = batch_memops(s, p);
+  if (r) return r;
   if (wl.n > 0) kwaits.push_back(wl);
   for (const WaitList& w : kwaits) {
     ICCL_CHECK_CUDA(launch_wait(w, s));
@@ -1753,7 +2601,7 @@ static iccl_result_t stream_markers(iccl_comm* c, cudaStream_t s, const std::vec
 
 // One fused K5 launch per (stream, group): every LL op of the group gets its
 // own CTAs (1..kLLMaxBlk by size), so sends and recvs progress concurrently.
-static iccl_result_t launch_ll_ops(iccl_comm* c, cudaStream_t s, const std::vector<OpDesc>& ops) {
+static iccl_result_t launch_ll_ops(iccl_comm* c, cudaStream_t s, std::vector<OpDesc>& ops) {
   RankFlags* mine = flags_of(c, c->rank);
   size_t i = 0;
   while (i < ops.size()) {
@@ -1761,8 +2609,9 @@ static iccl_result_t launch_ll_ops(iccl_comm* c, cudaStream_t s, const std::vect
     memset(&b, 0, sizeof(b));
     b.error = c->ll_error;
     uint32_t blocks = 0;
+    const size_t first = i;
     for (; i < ops.size() && b.n < kLLMaxOps; i++) {
-      const OpDesc& op = ops[i];
+      OpDesc& op = ops[i];
       const size_t lines = (op.bytes + 3) / 4;
       const uint32_t nblk = (uint32_t)std::min<size_t>(kLLMaxBlk, std::max<size_t>(1, (lines + kLLLinesPerBlk - 1) /
                                                                                           kLLLinesPerBlk));
@@ -1775,9 +2624,11 @@ static iccl_result_t launch_ll_ops(iccl_comm* c, cudaStream_t s, const std::vect
       if (op.kind == 0) {
         d.slot = c->peer_ll[op.peer] + ll_slot_offset(c->rank, op.ll_seq);
         d.credit = (unsigned int*)(c->ll_region + ll_credit_offset(c->nranks, op.peer));
+        d.stamp = alloc_kstamp(c, op);  // the sender's record: first line out -> last line out
       } else {
         d.slot = c->ll_region + ll_slot_offset(op.peer, op.ll_seq);
         d.credit = (unsigned int*)(c->peer_ll[op.peer] + ll_credit_offset(c->nranks, c->rank));
+        d.stamp = nullptr;
       }
       d.done_flag = &mine->done[op.slot];
       d.done_gen = op.gen;
@@ -1789,8 +2640,26 @@ static iccl_result_t launch_ll_ops(iccl_comm* c, cudaStream_t s, const std::vect
     ICCL_CHECK_CUDA(launch_ll(b, s));
     c->kernels_launched += 1;
     c->ctas_launched += blocks;
+    for (size_t j = first; j < i; j++)
+      if (ops[j].kind == 0) push_krec(c, ops[j], 0);
   }
   return ICCL_SUCCESS;
+}
+
+// Six-pointer record of an op nobody else publishes yet: one chunk, posted
+// once its kernel or copy is queued (the issuer's proxy overwrites it with
+// the real chunk pointers when the op runs on the chunked path).
+static void publish_simple(iccl_comm* c, const OpDesc& op, int posted) {
+  XferPub& p = flags_of(c, c->rank)->pub[op.slot];
+  __atomic_store_n(&p.gen, 0u, __ATOMIC_RELEASE);
+  p.kind = op.kind;
+  p.total = 1;
+  p.posted = posted;
+  p.done = 0;
+  p.path = 0;
+  p.switches = 0;
+  p.bytes = op.bytes;
+  __atomic_store_n(&p.gen, op.gen, __ATOMIC_RELEASE);
 }
 
 static iccl_result_t enqueue_op(iccl_comm* c, int kind, const void* buf, size_t bytes, int peer, cudaStream_t s,
@@ -1811,22 +2680,19 @@ static iccl_result_t enqueue_op(iccl_comm* c, int kind, const void* buf, size_t 
   op.bytes = bytes;
   iccl_result_t r = next_slot(c, &op.slot, &op.gen, &op.op_seq);
   if (r) return r;
-  {
-    XferPub& p = flags_of(c, c->rank)->pub[op.slot];
-    __atomic_store_n(&p.gen, 0u, __ATOMIC_RELEASE);
-    p.kind = kind;
-  }
+  publish_simple(c, op, 0);
   // Small messages between different GPUs take the LL kernel path (K5) unless
-  // the copy-engine transport is forced; both sides classify by the same byte
-  // count, so the k-th LL send of a pair always meets the k-th LL recv.
-  op.ll = peer != c->rank && c->cfg.transport != ICCL_TRANSPORT_CE && bytes <= c->cfg.sm_small_bytes &&
-          bytes <= kLLMaxBytes && c->ll_region != nullptr;
-  op.direct = !op.ll && peer != c->rank && c->cfg.transport == ICCL_TRANSPORT_AUTO &&
+  // the copy-engine transport is forced or the pair is armed for failover
+  // (route_small: both sides route the pair's q-th small op alike).
+  const bool small = peer != c->rank && c->cfg.transport != ICCL_TRANSPORT_CE && bytes <= c->cfg.sm_small_bytes &&
+                     bytes <= kLLMaxBytes && c->ll_region != nullptr;
+  op.ll = small && !route_small(pair_of(c, kind == 0 ? c->rank : peer, kind == 0 ? peer : c->rank), kind);
+  op.direct = !small && peer != c->rank && c->cfg.transport == ICCL_TRANSPORT_AUTO &&
               bytes <= (size_t)c->cfg.direct_max_kib * 1024;
   if (op.ll) {
     op.ll_seq = kind == 0 ? ++c->ll_sent[peer] : ++c->ll_recvd[peer];
   } else if (kind == 1 || c->group_depth == 0) {
-    r = rzv_post(c, op, kind == 0 ? kSendWaitUs : 0, c->group_depth > 0, c->group_depth > 0 ? nullptr : s);
+    r = rzv_post(c, op, kind == 0 ? kSendWaitUs : 0, c->group_depth > 0, s);
     if (r) return r;
   }  // a send inside a group posts at group_end, after every recv of the group
   c->ranks[c->rank].op_count.fetch_add(1, std::memory_order_relaxed);
@@ -1835,8 +2701,13 @@ static iccl_result_t enqueue_op(iccl_comm* c, int kind, const void* buf, size_t 
     c->group_ops.emplace_back(op, s);
     return ICCL_SUCCESS;
   }
-  if (op.ll) return launch_ll_ops(c, s, {op});
-  if (op.issued_direct) return launch_direct_ops(c, s, {op});
+  if (op.ll || op.issued_direct) {
+    std::vector<OpDesc> one{op};
+    r = op.ll ? launch_ll_ops(c, s, one) : launch_direct_ops(c, s, one);
+    if (!r) publish_simple(c, op, 1);
+    return r;
+  }
+  if (op.issued_instream) return ICCL_SUCCESS;  // copies + done writes already on s
   return stream_markers(c, s, {op});
 }
 
@@ -1917,10 +2788,12 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
   c->rings = (RzvRing*)((char*)m + L.off_rings);
   // device-visible control block: every rank's copy streams write flags here
   ICCL_CHECK_CUDA(cudaHostRegister(m, L.total, cudaHostRegisterMapped | cudaHostRegisterPortable));
-  c->pinned_bytes = 64 * 1024 + sizeof(KernelStamp) * kStampSlots + kGateWords * 4;
+  c->pinned_bytes = 64 * 1024 + sizeof(KernelStamp) * kStampSlots + kGateWords * 4 + sizeof(ArmedWords) * kArmedSlots;
   ICCL_CHECK_CUDA(cudaHostAlloc((void**)&c->pinned, c->pinned_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
   memset(c->pinned, 0, c->pinned_bytes);
   c->gate_words = (volatile uint32_t*)((char*)c->pinned + 64 * 1024 + sizeof(KernelStamp) * kStampSlots);
+  c->armed_words = (ArmedWords*)((char*)c->gate_words + kGateWords * 4);
+  c->armed_used.assign(kArmedSlots, 0);
   c->gate_closed.assign(kGateWords, 0);
   c->stamps = (KernelStamp*)((char*)c->pinned + 64 * 1024);
   c->gtimer = (unsigned long long*)((char*)c->pinned + 48 * 1024);
@@ -1979,8 +2852,12 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
   if (r) return r;
   if (rank == 0) shm_unlink(b.shm_name);
 
-  // streams: per channel (peer x {push, pull}) S copy-engine streams + 1 SM
-  // stream + 1 probe stream (+ 1 relay stream for a push channel)
+  // streams: per channel (peer x {push, pull}) S copy-engine streams; per
+  // rank the group streams, one backup SM-kernel stream, one probe stream, a
+  // monitor stream per direction and (relay backup) a hop-1 stream plus a
+  // forwarding stream per source — 22 streams at N = 8 (29 with the relay),
+  // within CUDA_DEVICE_MAX_CONNECTIONS = 32, so no stream shares a hardware
+  // queue with a parked one
   int prio_lo, prio_hi;
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   c->ch.resize(2 * nranks);
@@ -2003,6 +2880,12 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
   for (int d = 0; d < 2; d++)
     for (int l = 0; l < lanes; l++) group_si[d].push_back(mk_stream(ENG_CE_GROUP));
   c->group_lanes = lanes;
+  c->sm_si = mk_stream(ENG_SM);
+  c->probe_si = mk_stream(ENG_CE);
+  c->mon_si[0] = mk_stream(ENG_CE);
+  c->mon_si[1] = mk_stream(ENG_CE);
+  if (c->relay_buf) c->relay_si = mk_stream(ENG_RELAY);
+  c->instream_ce = env_us("ICCL_INSTREAM", 1) != 0;
   std::vector<char*> peer_scratch(nranks, nullptr);
   for (int p = 0; p < nranks; p++) {
     if (p == rank) {
@@ -2030,16 +2913,14 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
       chn.path_streams[0].push_back(si);
       chn.path_streams[1].push_back(si);
     }
-    int sm = mk_stream(ENG_SM);
-    chn.path_streams[0].push_back(sm);
-    chn.path_streams[1].push_back(sm);
+    chn.path_streams[1].push_back(c->sm_si);
     if (c->relay_buf && p != rank && chn.dir == 0) {
       for (int q = 0; q < nranks; q++)
         if (q != rank && q != p) {
           chn.relay_rank = q;  // lowest-index GPU that is not an endpoint
           break;
         }
-      chn.path_streams[1].push_back(mk_stream(ENG_RELAY));
+      chn.path_streams[1].push_back(c->relay_si);
     }
     if (p != rank) {
       for (int gs : group_si[chn.dir]) {
@@ -2047,8 +2928,8 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
         chn.path_streams[1].push_back(gs);
       }
     }
-    chn.probe_stream = mk_stream(ENG_CE);
-    chn.mon_stream = mk_stream(ENG_CE);
+    chn.probe_stream = c->probe_si;
+    chn.mon_stream = c->mon_si[chn.dir];
     ICCL_CHECK_CUDA(cudaEventCreateWithFlags(&chn.bridge, cudaEventDisableTiming));
     c->all_events.push_back(chn.bridge);
   }
@@ -2076,19 +2957,27 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
   r = shm_barrier(c);
   if (r) return r;
   c->proxy = std::thread(proxy_loop, c);
+  c->watchdog = std::thread(watch_loop, c);
   *out = c;
   return ICCL_SUCCESS;
 }
 
-static void teardown(iccl_comm* c) {
+// sync = false (abort): the side streams may be parked for good on a wait
+// for a peer that died (its ready flag, a relay counter), so they are
+// destroyed without synchronising; CUDA releases them once they drain.
+static void teardown(iccl_comm* c, bool sync = true) {
   if (c->proxy.joinable()) {
     c->stop.store(true);
     c->qcv.notify_one();
     c->proxy.join();
   }
+  if (c->watchdog.joinable()) {
+    c->stop.store(true);
+    c->watchdog.join();
+  }
   for (auto& sc : c->streams) {
     if (sc.s) {
-      cudaStreamSynchronize(sc.s);
+      if (sync) cudaStreamSynchronize(sc.s);
       cudaStreamDestroy(sc.s);
     }
     if (sc.ev) cudaEventDestroy(sc.ev);
@@ -2128,6 +3017,7 @@ iccl_result_t iccl_comm_destroy(iccl_comm_t c) {
     c->qcv.notify_one();
     c->proxy.join();
   }
+  if (c->watchdog.joinable()) c->watchdog.join();
   // Injected faults may still hold probes behind a closed gate; no data copy
   // is gated any more (stale copies are flushed before their op completes),
   // so open every gate and let the side streams drain.
@@ -2149,7 +3039,24 @@ iccl_result_t iccl_comm_abort(iccl_comm_t c) {
   for (uint64_t s = c->op_seq > (uint64_t)kSlots ? c->op_seq - kSlots : 0; s < c->op_seq; s++)
     __atomic_store_n(&mine->done[s % kSlots], (uint32_t)(s + 1), __ATOMIC_SEQ_CST);
   for (int g = 0; g < kGateWords; g++) __atomic_store_n((uint32_t*)&c->gate_words[g], 1u, __ATOMIC_SEQ_CST);
-  teardown(c);
+  for (int i = 0; i < kArmedSlots; i++) {  // unpark every armed attempt (the backups copy nothing)
+    ArmedWords* w = &c->armed_words[i];
+    __atomic_store_n(&w->resume, 0xffffffffu, __ATOMIC_SEQ_CST);
+    __atomic_store_n(&w->go, 1u, __ATOMIC_SEQ_CST);
+    __atomic_store_n(&w->probe_go, 1u, __ATOMIC_SEQ_CST);
+    __atomic_store_n(&w->ns, 1u, __ATOMIC_SEQ_CST);
+  }
+  // mapped peer memory and the control block stay mapped (leaked): a parked
+  // stream may still touch them when it drains
+  c->peer_ipc.clear();
+  c->peer_scratch_base.clear();
+  c->peer_ll.clear();
+  c->peer_relay.clear();
+  c->shm = nullptr;
+  c->scratch = c->ll_region = c->relay_buf = nullptr;
+  c->ll_counters = nullptr;
+  c->pinned = nullptr;
+  teardown(c, false);
   delete c;
   return ICCL_SUCCESS;
 }
@@ -2210,9 +3117,23 @@ iccl_result_t iccl_register(iccl_comm_t c, void* ptr, size_t bytes, uint64_t* ha
   return ICCL_SUCCESS;
 }
 
+// The caller promises no op in flight uses the buffer: drop the export and
+// tell every peer that mapped it to close its mapping (their proxies do it).
 iccl_result_t iccl_deregister(iccl_comm_t c, uint64_t handle) {
   if (!c) return ICCL_ERR_INVALID_ARGUMENT;
-  ICCL_RETURN_IF(!c->export_cache.erase(handle), ICCL_ERR_UNREGISTERED_REGION, "unknown registration handle");
+  auto it = c->export_cache.find(handle);
+  ICCL_RETURN_IF(it == c->export_cache.end(), ICCL_ERR_UNREGISTERED_REGION, "unknown registration handle");
+  const cudaIpcMemHandle_t h = it->second;
+  c->export_cache.erase(it);
+  for (int p = 0; p < c->nranks; p++) {
+    if (p == c->rank || !c->announced[p].count(handle)) continue;
+    uint64_t t0 = now_ns();
+    while (!announce_entry(c, p, AnnEntry{handle, 1, h})) {  // the ring drains in the peer's proxy
+      ICCL_RETURN_IF(now_ns() - t0 > 10ull * 1000000000ull, ICCL_ERR_TIMEOUT, "peer did not drain its announcements");
+      usleep(50);
+    }
+    c->announced[p].erase(handle);
+  }
   return ICCL_SUCCESS;
 }
 
@@ -2242,51 +3163,107 @@ iccl_result_t iccl_group_end(iccl_comm_t c) {
   for (auto& p : ops) {
     if (p.first.kind != 0 || p.first.ll) continue;
     const uint64_t t = now_ns();
-    iccl_result_t r = rzv_post(c, p.first, t < deadline ? (deadline - t) / 1000 : 0, true);
+    iccl_result_t r = rzv_post(c, p.first, t < deadline ? (deadline - t) / 1000 : 0, true, p.second);
     if (r) return r;
   }
+  // every transfer this side issues for the group: in-stream on the op's own
+  // stream where the pair allows it, else on the side streams
+  std::vector<iccl_comm::GroupJob> jobs;
+  jobs.swap(c->group_jobs);
+  auto find_op = [&](int kind, int peer, const RzvSide& s) -> OpDesc* {
+    for (auto& p : ops)
+      if (p.first.kind == kind && p.first.peer == peer && p.first.slot == s.slot && p.first.gen == s.gen)
+        return &p.first;
+    return nullptr;
+  };
+  // mode per job: 1 plain in-stream, 2 armed in-stream, 3 armed on the side
+  // streams, 0 the proxy-driven side-stream pipeline (see rzv_post)
+  std::vector<Xfer> xs(jobs.size());
+  std::vector<char> mode(jobs.size(), 0), elide(jobs.size(), 0);
+  for (size_t i = 0; i < jobs.size(); i++) {
+    const auto& j = jobs[i];
+    iccl_result_t r = rzv_build(c, j.kind, j.peer, j.k, j.op_seq, true, j.side, &xs[i]);
+    if (r) return r;
+    const RzvSide& other = j.side[j.kind ^ 1];
+    OpDesc* oth = j.peer == c->rank ? find_op(j.kind ^ 1, j.peer, other) : nullptr;
+    const bool stream_ok = instream_ok(c, j.kind, j.peer, j.side, oth != nullptr, j.stream);
+    if (xfer_armed(c, j.kind, j.peer))
+      mode[i] = armed_eligible(c, xs[i]) ? (stream_ok ? 2 : 3) : 0;
+    else
+      mode[i] = stream_ok ? 1 : 0;
+    if (mode[i] != 1 && mode[i] != 2) continue;
+    if (OpDesc* me = find_op(j.kind, j.peer, j.side[j.kind])) me->issued_instream = true;
+    if (mode[i] == 1 && oth && other.stream == (uint64_t)(uintptr_t)j.stream) {
+      // self pair, both halves of one group on one stream: the stream already
+      // orders the copy after both ops' positions — no markers, no waits
+      oth->markers_elided = true;
+      elide[i] = 1;
+    }
+  }
   {
-    // The group's pushes share one stream (rzv_post): enqueue every ready
-    // wait first, then the copies back to back — a wait placed between two
-    // copies would cost each a copy-engine drain (~15 us per peer in the
-    // 4-rank alltoallv records).
-    std::vector<Xfer> xs(c->group_jobs.size());
-    for (size_t i = 0; i < xs.size(); i++) {
-      const auto& j = c->group_jobs[i];
-      iccl_result_t r = rzv_build(c, j.kind, j.peer, j.k, j.op_seq, true, &xs[i]);
-      if (r) return r;
-    }
-    c->group_jobs.clear();
+    // Side-stream transfers: a group's pushes share one stream (rzv_post):
+    // enqueue every ready wait first, then the copies back to back — a wait
+    // placed between two copies would cost each a copy-engine drain (~15 us
+    // per peer in the 4-rank alltoallv records).  Armed ones go to their
+    // channel's own streams.
     int nth[2] = {0, 0};
-    for (Xfer& x : xs)
-      if (x.group_stream) x.group_lane = nth[c->ch[x.chan].dir]++ % c->group_lanes;
-    for (Xfer& x : xs) {
-      iccl_result_t r = ready_waits(c, c->ch[x.chan], x);
+    for (size_t i = 0; i < xs.size(); i++) {
+      if (mode[i] == 3) xs[i].group_stream = false;
+      if (mode[i] == 0 && xs[i].group_stream) xs[i].group_lane = nth[c->ch[xs[i].chan].dir]++ % c->group_lanes;
+    }
+    for (size_t i = 0; i < xs.size(); i++) {
+      if (mode[i] != 0) continue;
+      iccl_result_t r = ready_waits(c, c->ch[xs[i].chan], xs[i]);
       if (r) return r;
     }
-    for (Xfer& x : xs) {
-      iccl_result_t r = rzv_launch(c, std::move(x), false);
+    for (size_t i = 0; i < xs.size(); i++) {
+      iccl_result_t r = ICCL_SUCCESS;
+      if (mode[i] == 0) r = rzv_launch(c, std::move(xs[i]), false);
+      if (mode[i] == 3) r = armed_launch(c, std::move(xs[i]), jobs[i].kind, jobs[i].stream, false);
       if (r) return r;
     }
   }
-  // per stream: ready markers of the ops waiting on a peer (copy engine, or
-  // K6 run by the peer), then the kernels (LL, K6 this side runs), then the
-  // done waits — no kernel of ours ever sits in front of a ready flag a peer
-  // needs
-  // one batched marker set per distinct stream
+  // Per user stream: ready markers of the ops a peer (or a side stream)
+  // issues, then the kernels (LL, K6 this side runs), then this side's
+  // in-stream transfers (their ready waits hoisted in front of the copies, the
+  // done writes batched behind them), then the done waits — no kernel or copy
+  // of ours ever sits in front of a ready flag a peer needs.
   std::vector<cudaStream_t> order;
   for (auto& p : ops)
     if (std::find(order.begin(), order.end(), p.second) == order.end()) order.push_back(p.second);
   for (cudaStream_t s : order) {
     std::vector<OpDesc> ce, ll, direct;
-    for (auto& p : ops)
-      if (p.second == s) (p.first.ll ? ll : p.first.issued_direct ? direct : ce).push_back(p.first);
+    for (auto& p : ops) {
+      if (p.second != s || p.first.issued_instream || p.first.markers_elided) continue;
+      (p.first.ll ? ll : p.first.issued_direct ? direct : ce).push_back(p.first);
+    }
     iccl_result_t r = ICCL_SUCCESS;
     if (!ce.empty()) r = stream_markers(c, s, ce, 1);  // ready
     if (!r && !ll.empty()) r = launch_ll_ops(c, s, ll);
     if (!r && !direct.empty()) r = launch_direct_ops(c, s, direct);
-    if (!r && !ce.empty()) r = stream_markers(c, s, ce, 2);  // done waits
     if (r) return r;
+    std::vector<CUstreamBatchMemOpParams> p;
+    std::vector<size_t> mine;
+    for (size_t i = 0; i < jobs.size(); i++)
+      if (mode[i] == 1 && jobs[i].stream == s) mine.push_back(i);
+    if (!mine.empty()) {
+      for (size_t i : mine)
+        if (!elide[i]) instream_ready_param(c, xs[i], jobs[i].kind, p);
+      r = batch_memops(s, p);
+      for (size_t i : mine)
+        if (!r) r = instream_copies(c, xs[i], s);
+      for (size_t i : mine) instream_done_params(c, xs[i], p);
+      if (!r) r = batch_memops(s, p);
+      if (r) return r;
+      for (size_t i : mine) rzv_track(c, std::move(xs[i]), false);
+    }
+    for (size_t i = 0; i < jobs.size() && !r; i++)
+      if (mode[i] == 2 && jobs[i].stream == s) r = armed_launch(c, std::move(xs[i]), jobs[i].kind, s, true);
+    if (r) return r;
+    if (!ce.empty()) r = stream_markers(c, s, ce, 2);  // done waits
+    if (r) return r;
+    for (const OpDesc& o : ll) publish_simple(c, o, 1);
+    for (const OpDesc& o : direct) publish_simple(c, o, 1);
   }
   return ICCL_SUCCESS;
 }
@@ -2381,6 +3358,7 @@ iccl_result_t iccl_req_state(iccl_comm_t c, iccl_req_t req, iccl_xfer_state_t* s
 iccl_result_t iccl_path_switch(iccl_comm_t c, int peer, int to) {
   if (!c || peer < 0 || peer >= c->nranks || (to != 0 && to != 1)) return ICCL_ERR_INVALID_ARGUMENT;
   pair_of(c, c->rank, peer).active_path.store(to);
+  route_update(pair_of(c, c->rank, peer));
   c->path_req[2 * peer + 0].store(to);
   if (peer == c->rank) c->path_req[2 * peer + 1].store(to);  // a self pair is also issued by its pull side
   c->qcv.notify_one();
@@ -2395,15 +3373,28 @@ iccl_result_t iccl_path_active(iccl_comm_t c, int peer, int* path) {
 
 iccl_result_t iccl_fault_set(iccl_comm_t c, const iccl_fault_t* f, int n) {
   if (!c || (n > 0 && !f) || n < 0) return ICCL_ERR_INVALID_ARGUMENT;
-  std::lock_guard<std::mutex> g(c->fault_mu);
-  c->faults.clear();
-  for (int i = 0; i < n; i++) {
+  for (int i = 0; i < n; i++)
     ICCL_RETURN_IF(f[i].src < 0 || f[i].src >= c->nranks || f[i].dst < 0 || f[i].dst >= c->nranks,
                    ICCL_ERR_INVALID_ARGUMENT, "fault names an unknown path (UnknownPort)");
-    c->faults.push_back(Fault{f[i], false});
+  std::vector<std::pair<int, int>> touched;
+  {
+    std::lock_guard<std::mutex> g(c->fault_mu);
+    // the pairs a script names are armed for failover on both endpoints: their
+    // ops (every size class) take the chunked path where the gates apply
+    for (const Fault& old : c->faults) {
+      pair_of(c, old.f.src, old.f.dst).faults_armed.fetch_sub(1);
+      touched.emplace_back(old.f.src, old.f.dst);
+    }
+    c->faults.clear();
+    for (int i = 0; i < n; i++) {
+      c->faults.push_back(Fault{f[i], false});
+      pair_of(c, f[i].src, f[i].dst).faults_armed.fetch_add(1);
+      touched.emplace_back(f[i].src, f[i].dst);
+    }
+    c->faults_t0 = now_ns();
+    for (auto& chn : c->ch) chn.fault_seq_base = chn.dir == 0 ? c->pair_sends[chn.peer] : c->pair_recvs[chn.peer];
   }
-  c->faults_t0 = now_ns();
-  for (auto& chn : c->ch) chn.fault_seq_base = chn.dir == 0 ? c->pair_sends[chn.peer] : c->pair_recvs[chn.peer];
+  for (auto& t : touched) route_update(pair_of(c, t.first, t.second));
   return ICCL_SUCCESS;
 }
 
@@ -2452,6 +3443,31 @@ iccl_result_t iccl_monitor_config(iccl_comm_t c, int enabled, int window) {
   c->monitor_enabled.store(enabled ? 1 : 0);
   c->cfg.monitor_window = window;
   return ICCL_SUCCESS;
+}
+
+// ---- self-test hooks: the shared-memory protocols on plain host memory ----
+size_t iccl_selftest_pair_bytes(void) { return sizeof(PairState); }
+size_t iccl_selftest_rzv_bytes(void) { return sizeof(RzvEntry); }
+
+int iccl_selftest_route_small(void* pair, int side) { return route_small(*(PairState*)pair, side & 1) ? 1 : 0; }
+
+void iccl_selftest_route_arm(void* pair, int faults_delta, int active_path) {
+  PairState& ps = *(PairState*)pair;
+  ps.faults_armed.fetch_add(faults_delta);
+  if (active_path >= 0) ps.active_path.store(active_path);
+  route_update(ps);
+}
+
+int iccl_selftest_rzv_post(void* entry, int kind, uint64_t k, uint64_t bytes, uint64_t* other_bytes) {
+  RzvEntry& e = *(RzvEntry*)entry;
+  while (!rzv_free(e, k)) sched_yield();
+  e.side[kind & 1].bytes = bytes;
+  e.side[kind & 1].slot = (uint32_t)(k % kSlots);
+  e.side[kind & 1].gen = (uint32_t)(k + 1);
+  RzvSide snap[2];
+  if (!rzv_arrive(e, k, snap)) return 0;
+  if (other_bytes) *other_bytes = snap[(kind & 1) ^ 1].bytes;
+  return snap[0].gen == snap[1].gen ? 1 : -1;  // both halves belong to op k
 }
 
 iccl_result_t iccl_monitor_read(iccl_comm_t c, iccl_mon_rec_t* recs, int max, int* n) {

@@ -64,6 +64,24 @@ def scatter_rows(src: torch.Tensor, idx: torch.Tensor, out: torch.Tensor, ctas: 
     return out
 
 
+def config4_routing(rank: int, T: int = 4096, k: int = 8, E: int = 64, device="cuda") -> torch.Tensor:
+    """BASELINE config 4's routing: expert popularity
+    p_e ~ (e+1)^-0.8, permuted by seed 0; top-k experts per token by
+    multinomial sampling with seed 1000 + rank.  Returns [T, k] int64."""
+    g = torch.Generator().manual_seed(0)
+    p = torch.arange(1, E + 1, dtype=torch.float64) ** -0.8
+    p = p[torch.randperm(E, generator=g)]
+    g = torch.Generator().manual_seed(1000 + rank)
+    return torch.multinomial(p.expand(T, E), k, replacement=False, generator=g).to(device)
+
+
+def config4_tokens(rank: int, T: int = 4096, H: int = 7168, device="cuda") -> torch.Tensor:
+    """Config 4's token payload: uniform random int16 bits (seed 2000 + rank)
+    viewed as bf16 [T, H], so every bit pattern (NaN, Inf, denormals) occurs."""
+    g = torch.Generator(device=device).manual_seed(2000 + rank)
+    return torch.randint(-32768, 32767, (T, H), dtype=torch.int16, device=device, generator=g).view(torch.bfloat16)
+
+
 @dataclass
 class DispatchPlan:
     order: torch.Tensor          # [T*k] int64: flattened (token, k) index of each packed row

@@ -1,0 +1,45 @@
+#!/bin/bash
+# One parameterised GPU-box runner (replaces round 1's one-off scripts).
+#   gpurun -- 'bash scripts/gpu.sh TAG STEP [STEP ...]'
+# Every step logs to gpurun_out/TAG_STEP.log and appends its rc; a failing
+# step does not stop the next.  Steps:
+#   pytest      pytest -m gpu (all tests; ranks share the visible GPUs)
+#   pytest:EXPR pytest -m gpu -k EXPR
+#   smoke       __graft_entry__.smoke()
+#   bench1      bench.py N=1 (+ the reference arm)
+#   bench2      bench.py N=2 over torchrun (needs 2 GPUs)
+#   sweep       benchmarks/p2p_sweep.py (2 ranks)
+#   launches    ncu launch list of smoke() (gpu__time_duration, no replay of waits)
+#   ncuprobe    probes/ncu_xproc under ncu (cross-process serialisation)
+#   sanitize    compute-sanitizer memcheck/racecheck/synccheck on benchmarks/kernels.py
+#   cmd:...     any command (quoted)
+set -u
+TAG=$1; shift
+export PYTHONUNBUFFERED=1
+mkdir -p gpurun_out
+NG=$(nvidia-smi -L | wc -l)
+R() { python -m torch.distributed.run --nnodes=1 --nproc-per-node "$1" --master-addr 127.0.0.1 --master-port "$2" "${@:3}"; }
+for STEP in "$@"; do
+  LOG=gpurun_out/${TAG}_${STEP//[^A-Za-z0-9_.-]/_}.log
+  LOG=${LOG:0:120}
+  echo "== $STEP (gpus=$NG)" > "$LOG"
+  case "$STEP" in
+    pytest) timeout 1500 python -m pytest tests -q -m gpu -p no:cacheprovider --timeout 300 >> "$LOG" 2>&1 ;;
+    pytest:*) timeout 1500 python -m pytest tests -q -m gpu -p no:cacheprovider --timeout 300 -k "${STEP#pytest:}" >> "$LOG" 2>&1 ;;
+    smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" >> "$LOG" 2>&1 ;;
+    bench1) timeout 300 python bench.py >> "$LOG" 2>&1; timeout 300 python bench.py --impl reference >> "$LOG" 2>&1 ;;
+    bench2) timeout 300 R 2 29671 bench.py --gpus 2 >> "$LOG" 2>&1 ;;
+    sweep) timeout 900 R 2 29672 benchmarks/p2p_sweep.py --impl iccl-auto --min-pow 3 --max-pow 28 >> "$LOG" 2>&1 ;;
+    launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --target-processes all -c 2000 --csv \
+                --log-file gpurun_out/${TAG}_launches.csv python -c "import __graft_entry__ as g; g.smoke()" >> "$LOG" 2>&1 ;;
+    ncuprobe) ./probes/ncu_xproc >> "$LOG" 2>&1; timeout 120 ncu --target-processes all --metrics gpu__time_duration.sum \
+                ./probes/ncu_xproc >> "$LOG" 2>&1 ;;
+    sanitize) for T in memcheck racecheck synccheck; do
+                timeout 600 compute-sanitizer --tool $T --error-exitcode 9 python benchmarks/kernels.py --quick >> "$LOG" 2>&1
+                echo "$T rc=$?" >> "$LOG"; done ;;
+    cmd:*) timeout 1800 bash -c "${STEP#cmd:}" >> "$LOG" 2>&1 ;;
+    *) echo "unknown step $STEP" >> "$LOG" ;;
+  esac
+  echo "rc=$?" >> "$LOG"
+  tail -3 "$LOG"
+done

@@ -100,3 +100,13 @@ def dev_of(rank: int):
     """The GPU rank `rank` runs on (round-robin over the visible GPUs)."""
     import torch
     return torch.device("cuda", rank % torch.cuda.device_count())
+
+
+def fault_delta_us(world: int) -> int:
+    """Watchdog delta for the failover tests.  On separate GPUs 300 us.  When
+    ranks share a GPU, their processes' kernels and copies are time-sliced:
+    a rank spinning in a kernel (K7, an LL receive, a device sleep) holds the
+    GPU for whole time slices, so an innocent chunk (and its CTS probe) can
+    wait milliseconds — delta must exceed that or innocent stalls switch."""
+    import torch
+    return 300 if torch.cuda.device_count() >= world else 20_000

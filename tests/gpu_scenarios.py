@@ -178,3 +178,320 @@ def direct_mixed(comm, rank, world, sizes, rounds=2):
         out[f"single_{i}"] = r.cpu().numpy()
     out["kernels"] = np.array([comm.stats()["kernels_launched"]], np.int64)
     return out
+
+
+def _records(comm):
+    return [(r.size, r.peer, r.dir, r.path, r.chunk) for r in comm.monitor.drain()]
+
+
+def failover_reuse(comm, rank, world, nbytes, fault_chunk, reps=1):
+    """0 -> 1 with the primary path Down at `fault_chunk` of the first send
+    (ADVICE r1 high).  Right after each op completes on its stream, the sender
+    overwrites its source and the receiver copies the received bytes out and
+    then overwrites its buffer with a marker: a stale or re-issued copy still
+    in flight after completion would corrupt the copy-out (sender side) or the
+    marker (receiver side)."""
+    from paper_2510_00991_b200 import FaultScript
+    dev = dev_of(rank)
+    comm.set_faults(FaultScript().down(0, 1, chunk=fault_chunk, op_index=0))
+    out = {}
+    s = torch.cuda.current_stream()
+    for it in range(reps):
+        if rank == 0:
+            src = to_dev(payload(nbytes, seed=500 + it), dev)
+            comm.send(src, 1)
+            # a synchronous pageable copy behind the failing op: while it
+            # waits, every other CUDA call of this process blocks — the
+            # failover must not need one
+            int(src[:1].cpu()[0])
+            src.fill_(0x5A)  # stream-ordered after the send completed
+        elif rank == 1:
+            r = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+            comm.recv(r, 0)
+            int(r[:1].cpu()[0])
+            got = r.clone()        # stream-ordered after the recv completed
+            r.fill_(0xA5)
+            torch.cuda.synchronize()
+            import time
+            time.sleep(0.3)        # time for any late stale write to land
+            torch.cuda.synchronize()
+            out[f"recv{it}"] = got.cpu().numpy()
+            out[f"marker_ok{it}"] = np.array([bool((r == 0xA5).all().item())])
+    torch.cuda.synchronize()
+    import time
+    time.sleep(0.05)
+    ev = [e for e in comm.switch_events() if e["peer"] == 1 - rank]
+    out["switch_to"] = np.array([0 if e["to"] == "primary" else 1 for e in ev], np.int32)
+    out["resume"] = np.array([e["resume_chunk"] for e in ev], np.int32)
+    return out
+
+
+def fault_size_class(comm, rank, world, nbytes, fault_chunk):
+    """One 0 -> 1 op of a size that would take K5 (LL) or K6 (direct) on a
+    healthy pair, with a fault script naming the pair: the op must take the
+    chunked path, stall at `fault_chunk`, switch and complete bit-exact; the
+    monitor yields one record per chunk."""
+    from paper_2510_00991_b200 import FaultScript
+    dev = dev_of(rank)
+    comm.set_faults(FaultScript().down(0, 1, chunk=fault_chunk, op_index=0))
+    out = {}
+    stats0 = comm.stats()
+    if rank == 0:
+        comm.send(to_dev(payload(nbytes, seed=nbytes), dev), 1)
+    elif rank == 1:
+        r = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+        comm.recv(r, 0)
+        torch.cuda.synchronize()
+        out["recv"] = r.cpu().numpy()
+    torch.cuda.synchronize()
+    import time
+    time.sleep(0.05)
+    ev = [e for e in comm.switch_events() if e["peer"] == 1 - rank]
+    out["switch_to"] = np.array([0 if e["to"] == "primary" else 1 for e in ev], np.int32)
+    out["resume"] = np.array([e["resume_chunk"] for e in ev], np.int32)
+    out["records"] = np.array([r[0] for r in _records(comm)], np.int64)
+    st = comm.stats()
+    out["ll_or_direct_kernels"] = np.array([st["kernels_launched"] - stats0["kernels_launched"]], np.int64)
+    return out
+
+
+def monitor_every_op(comm, rank, world, sizes):
+    """Healthy pair, monitor on: every op of every size class (K5 LL, K6
+    direct, copy engine) yields exactly one record (default chunk), and
+    iccl_req_state reports each finished op as done."""
+    from paper_2510_00991_b200 import P2POp
+    dev = dev_of(rank)
+    peer = 1 - rank
+    out = {}
+    works = []
+    for i, n in enumerate(sizes):
+        s = to_dev(payload(n, seed=30_000 * rank + i), dev)
+        r = torch.zeros(n, dtype=torch.uint8, device=dev)
+        ops = [P2POp("isend", s, peer), P2POp("irecv", r, peer)] if rank == 0 else \
+              [P2POp("irecv", r, peer), P2POp("isend", s, peer)]
+        works += comm.batch_isend_irecv(ops)
+        torch.cuda.synchronize()
+        out[f"r{i}"] = r.cpu().numpy()
+    for i, n in enumerate(sizes):  # single ops too
+        s = to_dev(payload(n, seed=40_000 + i), dev)
+        r = torch.zeros(n, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            works.append(comm.isend(s, 1))
+            works.append(comm.irecv(r, 1))
+        else:
+            works.append(comm.irecv(r, 0))
+            works.append(comm.isend(s, 0))
+        torch.cuda.synchronize()
+        out[f"s{i}"] = r.cpu().numpy()
+    torch.cuda.synchronize()
+    import time
+    time.sleep(0.1)
+    recs = _records(comm)
+    out["rec_bytes"] = np.array(sorted(r[0] for r in recs), np.int64)
+    states = [w.state() for w in works]
+    out["state_done"] = np.array([s["done"] for s in states], np.int64)
+    out["state_total"] = np.array([s["total_chunks"] for s in states], np.int64)
+    return out
+
+
+def api_switch_mid_size(comm, rank, world, sizes):
+    """switch_qp ToBackup applies to every size class (K5/K6 sizes take the
+    chunked backup path), then ToPrimary restores the fast paths."""
+    dev = dev_of(rank)
+    out = {}
+    if rank == 0:
+        comm.switch_qp(1, "ToBackup")
+    import time
+    time.sleep(0.05)
+    for phase in range(2):
+        for i, n in enumerate(sizes):
+            if rank == 0:
+                comm.send(to_dev(payload(n, seed=60_000 + 100 * phase + i), dev), 1)
+            else:
+                r = torch.zeros(n, dtype=torch.uint8, device=dev)
+                comm.recv(r, 0)
+                torch.cuda.synchronize()
+                out[f"p{phase}_{i}"] = r.cpu().numpy()
+        torch.cuda.synchronize()
+        if phase == 0 and rank == 0:
+            out["path_after_switch"] = np.array([1 if comm.active_path(1) == "backup" else 0], np.int32)
+            comm.switch_qp(1, "ToPrimary")
+        time.sleep(0.05)
+    return out
+
+
+def ll_route_toggle(comm, rank, world, n_msgs, size):
+    """Small messages 0 -> 1 while rank 0 toggles the pair between primary and
+    backup (switch_qp) every few sends: both sides must route each small op
+    the same way (LL or rendezvous) or the op would hang."""
+    dev = dev_of(rank)
+    out = {}
+    if rank == 0:
+        for i in range(n_msgs):
+            if i % 5 == 2:
+                comm.switch_qp(1, "ToBackup" if (i // 5) % 2 == 0 else "ToPrimary")
+            comm.send(to_dev(payload(size, seed=70_000 + i), dev), 1)
+        comm.switch_qp(1, "ToPrimary")
+    else:
+        bufs = []
+        for i in range(n_msgs):
+            r = torch.zeros(size, dtype=torch.uint8, device=dev)
+            comm.recv(r, 0)
+            bufs.append(r)
+        torch.cuda.synchronize()
+        out["recv"] = np.stack([b.cpu().numpy() for b in bufs])
+    torch.cuda.synchronize()
+    return out
+
+
+def register_deregister(comm, rank, world, nbytes):
+    """MemoryRegion: register, send, deregister (peer closes its mapping),
+    then a fresh buffer; UnregisteredRegion for a range past its allocation."""
+    import ctypes as C
+    from paper_2510_00991_b200._lib import lib
+    dev = dev_of(rank)
+    out = {}
+    for it in range(3):
+        if rank == 0:
+            t = to_dev(payload(nbytes, seed=80_000 + it), dev)
+            h = comm.register(t)
+            comm.send(t, 1)
+            torch.cuda.synchronize()
+            import time
+            time.sleep(0.05)
+            comm.deregister(h)
+        else:
+            r = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+            comm.recv(r, 0)
+            torch.cuda.synchronize()
+            out[f"recv{it}"] = r.cpu().numpy()
+    t = torch.zeros(1024, dtype=torch.uint8, device=dev)
+    h = C.c_uint64()
+    rc = lib.iccl_register(comm._h, C.c_void_p(t.data_ptr()), 1 << 40, C.byref(h))
+    out["unregistered_rc"] = np.array([rc], np.int32)
+    return out
+
+
+def innocent_stall(comm, rank, world, trials, delta_us):
+    """AC4 on the product: the pair is armed (a fault that never
+    fires keeps it on the watchdog-covered chunked path); in every trial one
+    side's stream is held upstream for 1.5-6 x delta by a device-side sleep
+    before its op — the sender's data (or the receiver's buffer) is simply not
+    ready.  No trial may switch paths, and every trial lands bit-exact."""
+    from paper_2510_00991_b200 import FaultScript
+    dev = dev_of(rank)
+    comm.set_faults(FaultScript().down(0, 1, chunk=0, op_index=1 << 30))
+    rng = np.random.default_rng(4242)
+    ok = []
+    cycles_per_us = 1900
+    for t in range(trials):
+        n = int(rng.integers(1, 8 << 20))
+        stall_us = int(delta_us * rng.uniform(1.5, 6.0))
+        who = int(rng.integers(0, 2))  # 0: the sender is held upstream, 1: the receiver
+        if rank == who:
+            torch.cuda._sleep(stall_us * cycles_per_us)
+        if rank == 0:
+            comm.send(to_dev(payload(n, seed=90_000 + t), dev), 1)
+        else:
+            r = torch.empty(n, dtype=torch.uint8, device=dev)
+            comm.recv(r, 0)
+            ok.append(bool(torch.equal(r, to_dev(payload(n, seed=90_000 + t), dev))))
+    torch.cuda.synchronize()
+    import time
+    time.sleep(0.05)
+    return {"ok": np.array(ok, bool), "switches": np.array([len(comm.switch_events())], np.int64)}
+
+
+def monitor_accuracy(comm, rank, world, nchunks, chunk, stall_chunk, up_us):
+    """AC5 on the product: rank 0 pushes `nchunks` chunks in one
+    op, the monitor on.  With stall_chunk < 0 the flow is steady; otherwise the
+    pair's primary path is gated at that chunk and re-opened `up_us` after the
+    script is installed (a disturbance; delta is large, so no switch).  Returns
+    the sender-side records (t1, t2, bytes)."""
+    from paper_2510_00991_b200 import FaultScript
+    dev = dev_of(rank)
+    if stall_chunk >= 0:
+        comm.set_faults(FaultScript().down(0, 1, chunk=stall_chunk, op_index=0).up(0, 1, t_us=up_us))
+    n = nchunks * chunk
+    out = {}
+    src = to_dev(payload(n, seed=5), dev) if rank == 0 else None
+    dst = torch.empty(n, dtype=torch.uint8, device=dev) if rank == 1 else None
+    torch.cuda.synchronize()
+    comm.monitor.drain()
+    if rank == 0:
+        comm.send(src, 1)
+    else:
+        comm.recv(dst, 0)
+    torch.cuda.synchronize()
+    import time
+    time.sleep(0.05)
+    recs = [r for r in comm.monitor.drain() if r.peer == 1 - rank]
+    recs.sort(key=lambda r: r.t2)
+    out["t1"] = np.array([r.t1 for r in recs], np.int64)
+    out["t2"] = np.array([r.t2 for r in recs], np.int64)
+    out["bytes"] = np.array([r.size for r in recs], np.int64)
+    out["switches"] = np.array([len(comm.switch_events())], np.int64)
+    if rank == 1:
+        out["ok"] = np.array([bool(torch.equal(dst, to_dev(payload(n, seed=5), dev)))])
+    return out
+
+
+def moe_config4(comm, rank, world, T, k=8, E=64, H=7168, fault=None, keep_bytes=True):
+    """BASELINE config 4 at `world` ranks: K2 pack (expand), dispatch
+    alltoallv, combine alltoallv, K3 unpack, with the §8(d) routing and
+    payload.  Checks on the device, at any size: every rank's received rows
+    equal the rows every source rank routed to it (regenerated from the
+    sources' seeds), and the combine round trip restores (token, k) order.
+    With keep_bytes the packed send rows and the received rows come back for
+    the oracle comparison.  `fault` = (src, dst, chunk): a FaultScript Down on
+    that pair's primary path at that chunk of its first transfer (config 5)."""
+    from paper_2510_00991_b200 import FaultScript
+    from paper_2510_00991_b200.moe import (config4_routing, config4_tokens, expand_rows, plan_dispatch,
+                                           scatter_rows)
+    dev = dev_of(rank)
+    experts = config4_routing(rank, T, k, E, dev)
+
+    def exchange(send_counts):
+        s = torch.tensor(send_counts, dtype=torch.int64, device=dev)
+        r = torch.empty_like(s)
+        comm.alltoall(r, s)  # the one exchange step, through the product's own alltoall
+        torch.cuda.synchronize()
+        return r.tolist()
+
+    plan = plan_dispatch(experts, E, world, exchange)
+    tokens = config4_tokens(rank, T, H, dev)
+    if fault is not None:
+        comm.set_faults(FaultScript().down(fault[0], fault[1], chunk=fault[2], op_index=0))
+    torch.cuda.synchronize()
+    packed = torch.empty(T * k, H, dtype=tokens.dtype, device=dev)
+    recv = torch.empty(sum(plan.recv_counts), H, dtype=tokens.dtype, device=dev)
+    back = torch.empty_like(packed)
+    out = torch.empty_like(packed)
+    expand_rows(tokens, plan.pos, k, packed)
+    comm.alltoallv(recv, packed, plan.recv_counts, plan.send_counts)
+    comm.alltoallv(back, recv, plan.send_counts, plan.recv_counts)
+    scatter_rows(back, plan.order, out)
+    torch.cuda.synchronize()
+    # device-side expected rows: what every source i routed to this rank
+    per_rank = E // world
+    exp = []
+    for i in range(world):
+        ex_i = config4_routing(i, T, k, E, dev).reshape(-1)
+        order_i = torch.sort(ex_i, stable=True).indices
+        mine = torch.div(ex_i[order_i], per_rank, rounding_mode="floor") == rank
+        exp.append(config4_tokens(i, T, H, dev)[torch.div(order_i[mine], k, rounding_mode="floor")])
+    exp = torch.cat(exp)
+    res = {"recv_ok": np.array([bool(torch.equal(recv.view(torch.int16), exp.view(torch.int16)))]),
+           "roundtrip_ok": np.array([bool(torch.equal(out.view(T, k, H).view(torch.int16),
+                                                      tokens.view(torch.int16).unsqueeze(1).expand(T, k, H)))]),
+           "send_counts": np.array(plan.send_counts, np.int64)}
+    if keep_bytes:
+        res["packed"] = packed.view(torch.uint8).cpu().numpy().reshape(-1)
+        res["recv"] = recv.view(torch.uint8).cpu().numpy().reshape(-1)
+    import time
+    time.sleep(0.05)
+    ev = comm.switch_events()
+    res["switch_peers"] = np.array([e["peer"] for e in ev], np.int64)
+    res["switch_to"] = np.array([0 if e["to"] == "primary" else 1 for e in ev], np.int64)
+    res["records"] = np.array([len(comm.monitor.drain())], np.int64)
+    return res
