@@ -16,6 +16,7 @@ import ctypes as C
 import mmap
 import multiprocessing as mp
 import random
+import time
 
 import numpy as np
 import pytest
@@ -39,6 +40,10 @@ def _rzv_side(shared, out, kind, n, seed):
         if rng.random() < 0.3:
             for _ in range(rng.randint(1, 200)):
                 pass
+        if rng.random() < 0.02:
+            time.sleep(0.0005)
+        if kind == 0 and k == n // 2:
+            time.sleep(0.2)  # the side that started first pauses: the other overtakes, both orders occur
         r = lib.iccl_selftest_rzv_post(entry + (k % 1024) * lib.iccl_selftest_rzv_bytes(), kind, k,
                                        1000 + 7 * k + (k % 3), C.byref(other))
         res[kind, k, 0] = r
