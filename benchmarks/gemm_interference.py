@@ -29,7 +29,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--impl", choices=["iccl-ce", "iccl-sm", "nccl", "none"], required=True)
+    ap.add_argument("--impl", choices=["iccl-ce", "iccl-sm", "iccl-auto", "nccl", "none"], required=True)
     ap.add_argument("--reps", type=int, default=30)
     ap.add_argument("--gemms", type=int, default=4)
     ap.add_argument("--msg-mib", type=float, default=256.0,

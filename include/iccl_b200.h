@@ -168,7 +168,8 @@ typedef struct {
   uint64_t ctas_launched;  /* CTAs of those kernels (the "SMs used" of the SM paths) */
   uint64_t pulls_issued;   /* transfers this rank issued as the receiver (it reached the rendezvous second) */
   uint64_t cts_timeouts;   /* sends that stopped waiting for the receiver's half and posted first */
-  uint64_t reserved[2];
+  uint64_t pending_xfers;  /* transfers this rank issued that the proxy / watchdog has not retired yet */
+  uint64_t reserved[1];
 } iccl_stats_t;
 iccl_result_t iccl_comm_stats(iccl_comm_t comm, iccl_stats_t* stats);
 
@@ -203,6 +204,10 @@ iccl_result_t iccl_path_switch(iccl_comm_t comm, int peer, int to_path);
 iccl_result_t iccl_path_active(iccl_comm_t comm, int peer, int* path);
 iccl_result_t iccl_fault_set(iccl_comm_t comm, const iccl_fault_t* faults, int n);
 iccl_result_t iccl_switch_events(iccl_comm_t comm, iccl_switch_event_t* ev, int max, int* n);
+
+/* Chunk size (SPEC.md:228-236's chunk_size, ICCL_CHUNK_BYTES) of the transfers
+ * this rank issues from now on; same validation as iccl_config_t.chunk_bytes. */
+iccl_result_t iccl_comm_set_chunk_bytes(iccl_comm_t comm, uint64_t chunk_bytes);
 
 /* ---- window monitor ------------------------------------ */
 iccl_result_t iccl_monitor_config(iccl_comm_t comm, int enabled, int window);

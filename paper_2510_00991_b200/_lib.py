@@ -76,7 +76,7 @@ class SwitchEvent(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("kernels_launched", C.c_uint64), ("copies_issued", C.c_uint64), ("bytes_issued", C.c_uint64),
                 ("ctas_launched", C.c_uint64), ("pulls_issued", C.c_uint64), ("cts_timeouts", C.c_uint64),
-                ("reserved", C.c_uint64 * 2)]
+                ("pending_xfers", C.c_uint64), ("reserved", C.c_uint64 * 1)]
 
 
 _c = C.c_int  # iccl_result_t
@@ -117,6 +117,7 @@ PROTOTYPES = {
     "iccl_fault_set": (_c, [_p, C.POINTER(Fault), C.c_int]),
     "iccl_switch_events": (_c, [_p, C.POINTER(SwitchEvent), C.c_int, C.POINTER(C.c_int)]),
     "iccl_monitor_config": (_c, [_p, C.c_int, C.c_int]),
+    "iccl_comm_set_chunk_bytes": (_c, [_p, _u64]),
     "iccl_monitor_read": (_c, [_p, C.POINTER(MonRec), C.c_int, C.POINTER(C.c_int)]),
     "iccl_gather_rows": (_c, [_p, _p, _p, _i64, _i64, C.c_int, _p]),
     "iccl_scatter_rows": (_c, [_p, _p, _p, _i64, _i64, C.c_int, _p]),

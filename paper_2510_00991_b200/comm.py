@@ -292,6 +292,12 @@ class Communicator:
         raise_for(lib.iccl_path_active(self._h, int(peer), C.byref(p)), "iccl_path_active")
         return "primary" if p.value == 0 else "backup"
 
+    def set_chunk_bytes(self, chunk_bytes: int) -> None:
+        """Chunk size of the transfers this rank issues from now on (the
+        SPEC's chunk_size; config.chunk_bytes at init)."""
+        raise_for(lib.iccl_comm_set_chunk_bytes(self._h, int(chunk_bytes)), "iccl_comm_set_chunk_bytes")
+        self.config.chunk_bytes = int(chunk_bytes)
+
     def set_faults(self, script: FaultScript) -> None:
         script.validate(self.world_size)
         arr = (_CFault * max(1, len(script.entries)))()
@@ -312,12 +318,14 @@ class Communicator:
     def stats(self) -> dict:
         """Work this rank issued: SM kernels launched (K1, K5, K6) and their
         CTAs, copy-engine copies and payload bytes; transfers issued as the
-        receiver (pulls) and sends whose wait for the receiver timed out."""
+        receiver (pulls), sends whose wait for the receiver timed out, and
+        issued transfers not yet retired by the proxy / watchdog."""
         from ._lib import Stats
         s = Stats()
         raise_for(lib.iccl_comm_stats(self._h, C.byref(s)), "iccl_comm_stats")
         return dict(kernels_launched=s.kernels_launched, ctas_launched=s.ctas_launched, copies_issued=s.copies_issued,
-                    bytes_issued=s.bytes_issued, pulls_issued=s.pulls_issued, cts_timeouts=s.cts_timeouts)
+                    bytes_issued=s.bytes_issued, pulls_issued=s.pulls_issued, cts_timeouts=s.cts_timeouts,
+                    pending_xfers=s.pending_xfers)
 
     def op_counts(self) -> dict:
         arr = (C.c_uint64 * self.world_size)()

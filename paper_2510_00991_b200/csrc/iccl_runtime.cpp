@@ -3095,6 +3095,7 @@ iccl_result_t iccl_comm_stats(iccl_comm_t c, iccl_stats_t* s) {
   s->bytes_issued = c->bytes_issued.load();
   s->pulls_issued = c->pulls_issued.load();
   s->cts_timeouts = c->cts_timeouts.load();
+  s->pending_xfers = c->pending_xfers.load();
   return ICCL_SUCCESS;
 }
 
@@ -3435,6 +3436,14 @@ iccl_result_t iccl_expand_rows(const void* src, void* dst, const int64_t* pos, i
 iccl_result_t iccl_copy_sm(const void* src, void* dst, size_t bytes, int ctas, cudaStream_t s) {
   if (bytes > 0 && (!src || !dst)) return ICCL_ERR_INVALID_ARGUMENT;
   ICCL_CHECK_CUDA(launch_copy(src, dst, bytes, ctas > 0 ? ctas : 16, nullptr, s));
+  return ICCL_SUCCESS;
+}
+
+iccl_result_t iccl_comm_set_chunk_bytes(iccl_comm_t c, uint64_t chunk_bytes) {
+  if (!c) return ICCL_ERR_INVALID_ARGUMENT;
+  ICCL_RETURN_IF(chunk_bytes < 4096 || (chunk_bytes & 15), ICCL_ERR_INVALID_CONFIG,
+                 "chunk_bytes must be >= 4096 and a multiple of 16");
+  c->cfg.chunk_bytes = chunk_bytes;  // read by the API thread only (rzv_build)
   return ICCL_SUCCESS;
 }
 

@@ -9,6 +9,10 @@
 #   bench1      bench.py N=1 (+ the reference arm)
 #   bench2      bench.py N=2 over torchrun (needs 2 GPUs)
 #   sweep       benchmarks/p2p_sweep.py (2 ranks)
+#   sweeps      p2p_sweep: iccl-auto, nccl, nccl-zero (zero-CTA), nccl-ce; unidirectional and --bidir
+#   gemm        gemm_interference on all GPUs: none, iccl-ce 256 MiB, iccl-auto / nccl at 4 and 16 MiB
+#   failover    benchmarks/failover.py on all GPUs (sm backup; relay when >= 3 GPUs)
+#   moe         benchmarks/moe_alltoallv.py on all GPUs, iccl and nccl
 #   launches    ncu launch list of smoke() (gpu__time_duration, no replay of waits)
 #   ncuprobe    probes/ncu_xproc under ncu (cross-process serialisation)
 #   sanitize    compute-sanitizer memcheck/racecheck/synccheck on benchmarks/kernels.py
@@ -18,7 +22,7 @@ TAG=$1; shift
 export PYTHONUNBUFFERED=1
 mkdir -p gpurun_out
 NG=$(nvidia-smi -L | wc -l)
-R() { python -m torch.distributed.run --nnodes=1 --nproc-per-node "$1" --master-addr 127.0.0.1 --master-port "$2" "${@:3}"; }
+TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
 for STEP in "$@"; do
   LOG=gpurun_out/${TAG}_${STEP//[^A-Za-z0-9_.-]/_}.log
   LOG=${LOG:0:120}
@@ -28,8 +32,22 @@ for STEP in "$@"; do
     pytest:*) timeout 1500 python -m pytest tests -q -m gpu -p no:cacheprovider --timeout 300 -k "${STEP#pytest:}" >> "$LOG" 2>&1 ;;
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" >> "$LOG" 2>&1 ;;
     bench1) timeout 300 python bench.py >> "$LOG" 2>&1; timeout 300 python bench.py --impl reference >> "$LOG" 2>&1 ;;
-    bench2) timeout 300 R 2 29671 bench.py --gpus 2 >> "$LOG" 2>&1 ;;
-    sweep) timeout 900 R 2 29672 benchmarks/p2p_sweep.py --impl iccl-auto --min-pow 3 --max-pow 28 >> "$LOG" 2>&1 ;;
+    bench2) timeout 300 $TR --nproc-per-node 2 --master-port 29671 bench.py --gpus 2 >> "$LOG" 2>&1 ;;
+    sweep) timeout 900 $TR --nproc-per-node 2 --master-port 29672 benchmarks/p2p_sweep.py --impl iccl-auto --min-pow 3 --max-pow 28 >> "$LOG" 2>&1 ;;
+    sweeps) for I in iccl-auto nccl nccl-zero nccl-ce; do
+              for B in "" --bidir; do
+                echo "## $I $B" >> "$LOG"
+                timeout 900 $TR --nproc-per-node 2 --master-port 29673 benchmarks/p2p_sweep.py --impl $I $B --min-pow 3 --max-pow 30 >> "$LOG" 2>&1
+              done; done ;;
+    gemm) echo "## none" >> "$LOG"; timeout 600 $TR --nproc-per-node $NG --master-port 29674 benchmarks/gemm_interference.py --impl none >> "$LOG" 2>&1
+          echo "## iccl-ce 256" >> "$LOG"; timeout 600 $TR --nproc-per-node $NG --master-port 29675 benchmarks/gemm_interference.py --impl iccl-ce >> "$LOG" 2>&1
+          for M in 4 16; do for I in iccl-auto nccl; do
+            echo "## $I $M" >> "$LOG"
+            timeout 600 $TR --nproc-per-node $NG --master-port 29676 benchmarks/gemm_interference.py --impl $I --msg-mib $M >> "$LOG" 2>&1
+          done; done ;;
+    failover) timeout 600 $TR --nproc-per-node $NG --master-port 29677 benchmarks/failover.py >> "$LOG" 2>&1
+              [ "$NG" -ge 3 ] && timeout 600 $TR --nproc-per-node $NG --master-port 29678 benchmarks/failover.py --backup relay >> "$LOG" 2>&1 ;;
+    moe) for I in iccl nccl; do timeout 600 $TR --nproc-per-node $NG --master-port 29679 benchmarks/moe_alltoallv.py --impl $I >> "$LOG" 2>&1; done ;;
     launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --target-processes all -c 2000 --csv \
                 --log-file gpurun_out/${TAG}_launches.csv python -c "import __graft_entry__ as g; g.smoke()" >> "$LOG" 2>&1 ;;
     ncuprobe) ./probes/ncu_xproc >> "$LOG" 2>&1; timeout 120 ncu --target-processes all --metrics gpu__time_duration.sum \

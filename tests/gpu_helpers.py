@@ -46,6 +46,7 @@ def _worker(rank, world, port, fn, outdir, kwargs):
         from paper_2510_00991_b200 import Communicator, IcclConfig
         cfg = IcclConfig.defaults(**kwargs.pop("config", {}))
         comm = Communicator(rank, world, dev, cfg, store=store)
+        comm._test_store = store  # scenarios may barrier through it
         res = fn(comm, rank, world, **kwargs)
         torch.cuda.synchronize()
         comm.destroy()

@@ -495,3 +495,97 @@ def moe_config4(comm, rank, world, T, k=8, E=64, H=7168, fault=None, keep_bytes=
     res["switch_to"] = np.array([0 if e["to"] == "primary" else 1 for e in ev], np.int64)
     res["records"] = np.array([len(comm.monitor.drain())], np.int64)
     return res
+
+
+def _store_barrier(comm, tag):
+    import time
+    st = comm._test_store
+    st.add(tag, 1)
+    while int(st.add(tag, 0)) < comm.world_size:
+        time.sleep(0.0002)
+
+
+def _wait_retired(comm, timeout_s=5.0):
+    import time
+    t0 = time.time()
+    while comm.stats()["pending_xfers"] and time.time() - t0 < timeout_s:
+        time.sleep(0.0005)
+
+
+def fuzz_failover(comm, rank, world, trials, seed, delta_us):
+    """AC3 on the product: `trials` randomised 0 -> 1 transfers,
+    sizes log-uniform 1 KiB - 64 MiB, chunk sizes 16 KiB - 4 MiB, and a fault
+    script per trial: the primary Down at a random chunk (or at a chunk past
+    the end: armed, never fires), Down before the op (time-triggered), or Down
+    at a chunk and restored (Up) at a random time around delta.  Before each
+    trial the primary is restored and the pair is back on it.  Per trial the
+    receiver checks the bytes on its GPU, and both sides return the chunk
+    indices of their monitor records for the op (the delivered sequence: the
+    test checks it is 0..N-1, gapless and duplicate-free) and the sender's
+    six-pointer state.  Payloads are generated on the GPU from a seeded
+    generator on both sides (the same Philox stream)."""
+    import time
+    from paper_2510_00991_b200 import FaultScript
+    dev = dev_of(rank)
+    peer = 1 - rank
+    out = {"n": [], "nchunks": [], "mode": [], "ok": [], "state_done": [], "state_total": []}
+    chunks_all, chunks_off = [], [0]
+    for t in range(trials):
+        rng = np.random.default_rng(seed + t)
+        size = min(64 << 20, int(2.0 ** rng.uniform(10.0, 26.0)))
+        chunk = 1 << int(rng.integers(14, 23))
+        while (size + chunk - 1) // chunk > 256:
+            chunk <<= 1
+        nch = (size + chunk - 1) // chunk
+        mode = int(rng.integers(0, 4))
+        f = int(rng.integers(0, nch + 1))
+        # restore the primary a previous trial left Down, and wait until the
+        # pair is back on it (monitor_failed_link's probe, SPEC.md:264-273)
+        comm.set_faults(FaultScript().up(0, 1, t_us=0))
+        time.sleep(0.002)
+        if rank == 0:
+            t0 = time.time()
+            while comm.active_path(1) != "primary" and time.time() - t0 < 10:
+                time.sleep(0.0005)
+        _store_barrier(comm, f"fz{t}a")
+        fs = FaultScript()
+        if mode == 0:
+            fs.down(0, 1, chunk=f, op_index=0)
+        elif mode == 1:
+            fs.down(0, 1, t_us=0)
+        elif mode == 2:
+            fs.down(0, 1, chunk=f, op_index=0).up(0, 1, t_us=int(delta_us * rng.uniform(0.2, 4.0)))
+        comm.set_faults(fs)  # mode 3: an empty script (the pair is healthy)
+        comm.set_chunk_bytes(chunk)
+        if mode == 1:
+            time.sleep(0.001)
+        _store_barrier(comm, f"fz{t}b")
+        comm.monitor.drain()
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed * 7919 + t)
+        ref = torch.randint(0, 256, (size,), dtype=torch.uint8, device=dev, generator=g)
+        if rank == 0:
+            w = comm.isend(ref, 1)
+        else:
+            r = torch.full((size,), 0xEE, dtype=torch.uint8, device=dev)
+            w = comm.irecv(r, 0)
+        torch.cuda.synchronize()
+        _wait_retired(comm)
+        _store_barrier(comm, f"fz{t}c")
+        _wait_retired(comm)
+        st = w.state()
+        recs = [x for x in comm.monitor.drain() if x.peer == peer]
+        chunks_all.extend(x.chunk for x in recs)
+        chunks_off.append(len(chunks_all))
+        out["n"].append(size)
+        # a healthy pair (mode 3) sends <= direct_max_kib through K5 / K6: one record, one chunk
+        out["nchunks"].append(1 if mode == 3 and size <= comm.config.direct_max_kib * 1024 else nch)
+        out["mode"].append(mode)
+        out["ok"].append(rank == 0 or bool(torch.equal(r, ref)))
+        out["state_done"].append(st["done"])
+        out["state_total"].append(st["total_chunks"])
+    comm.set_faults(FaultScript().up(0, 1, t_us=0))
+    res = {k: np.array(v) for k, v in out.items()}
+    res["chunks"] = np.array(chunks_all, np.int64)
+    res["chunks_off"] = np.array(chunks_off, np.int64)
+    return res
