@@ -168,7 +168,8 @@ typedef struct {
   uint64_t ctas_launched;  /* CTAs of those kernels (the "SMs used" of the SM paths) */
   uint64_t pulls_issued;   /* transfers this rank issued as the receiver (it reached the rendezvous second) */
   uint64_t cts_timeouts;   /* sends that stopped waiting for the receiver's half and posted first */
-  uint64_t pending_xfers;  /* transfers this rank issued that the proxy / watchdog has not retired yet */
+  uint64_t pending_xfers;  /* transfers this rank issued that the proxy / watchdog has not retired yet
+                              (kernel-path ops until their monitor record is emitted) */
   uint64_t reserved[1];
 } iccl_stats_t;
 iccl_result_t iccl_comm_stats(iccl_comm_t comm, iccl_stats_t* stats);
@@ -212,6 +213,21 @@ iccl_result_t iccl_comm_set_chunk_bytes(iccl_comm_t comm, uint64_t chunk_bytes);
 /* ---- window monitor ------------------------------------ */
 iccl_result_t iccl_monitor_config(iccl_comm_t comm, int enabled, int window);
 iccl_result_t iccl_monitor_read(iccl_comm_t comm, iccl_mon_rec_t* recs, int max, int* n);
+
+/* ---- fused MoE dispatch (K8) ---------------------------------------------
+ * Collective over the communicator, stream-ordered on s.  Result identical to
+ *   iccl_expand_rows(tokens -> packed, pos, n_tokens, k)   (packed row pos[t*k+j] = token t)
+ *   iccl_alltoallv(packed, scounts, sdispls = prefix(scounts),
+ *                  rbuf, rcounts, rdispls = prefix(rcounts), row_bytes)
+ * but in one kernel with no packed buffer: every routed row is stored
+ * straight into the receive buffer of the rank owning its packed position
+ * (NVLink stores into an IPC mapping; PAPER.md:214-217's zero staging).
+ * Replaces the dispatch pack + alltoall of SPEC.md:427-444 / SURVEY.md §2.4.
+ * Pairs armed for failover take the unfused form (same result).  k <= 32,
+ * row_bytes a multiple of 16, tokens / rbuf 16-byte aligned. */
+iccl_result_t iccl_dispatch_rows(iccl_comm_t comm, const void* tokens, int64_t n_tokens, int32_t k,
+                                 const int64_t* pos, const size_t* scounts, void* rbuf, const size_t* rcounts,
+                                 int64_t row_bytes, cudaStream_t s);
 
 /* ---- MoE pack / unpack permutation kernels (K2 / K3), stream-ordered ----
  * dst row i <- src row idx[i] (gather, dispatch pack); dst row idx[i] <- src

@@ -151,6 +151,38 @@ cudaError_t launch_gather_rows(const void* src, void* dst, const int64_t* idx, i
 // K2 expand form: dst_rows[pos[t*k + j]] <- src_rows[t] for j < k (each source row read once).
 cudaError_t launch_expand_rows(const void* src, void* dst, const int64_t* pos, int64_t n_src, int k,
                                int64_t row_bytes, int ctas, cudaStream_t st);
+// K8: fused MoE dispatch (K2 expand form + the alltoallv push, no staging).
+// Packed row p (the send layout: rows grouped by destination rank) goes to
+// the rank d with lo[d] <= p < hi[d], as row p - lo[d] of seg (that rank's
+// receive segment for this source: IPC-mapped, or local for the self one).
+constexpr int kMaxFusedRanks = 64;
+struct FusedDest {
+  char* seg;
+  int64_t lo, hi;
+  const uint32_t* ready;  // the destination's recv-op ready flag (host-mapped), null for the self segment
+  uint32_t ready_gen;
+  uint32_t done_gen;
+  uint32_t* done;         // the destination's recv-op done flag, or null
+  uint32_t* my_done;      // this rank's send-op done flag, or null
+  uint32_t my_done_gen;
+  uint32_t pad;
+};
+struct DispatchOp {
+  const int4* tokens;
+  const int64_t* pos;  // [n_tokens * k]: packed row of (token, j)
+  int64_t n_tokens;
+  int32_t k, n;        // top-k (<= 32), ranks
+  int64_t row16;
+  int32_t parts;       // column parts per token row (one warp each)
+  uint32_t go_gen;
+  unsigned int* ticket;   // entry ticket (0 between uses): the first CTA polls the ready flags
+  unsigned int* counter;  // exit counter (0 between uses)
+  unsigned int* go;       // poller -> other CTAs (gen-tagged)
+  unsigned int* error;    // host-mapped: set to 1 if a wait timed out
+  KernelStamp* stamp;
+  FusedDest d[kMaxFusedRanks];
+};
+cudaError_t launch_dispatch(const DispatchOp& op, int ctas, cudaStream_t st, int* grid_out = nullptr);
 cudaError_t launch_scatter_rows(const void* src, void* dst, const int64_t* idx, int64_t n_rows, int64_t row_bytes,
                                 int ctas, cudaStream_t st);
 }  // namespace iccl

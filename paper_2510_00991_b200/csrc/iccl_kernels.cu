@@ -15,6 +15,9 @@
 //                     move yields a WR/WC record.
 // K2  gather rows     MoE dispatch pack: dst[i] = src[idx[i]] (16 B vectors).
 // K3  scatter rows    MoE combine unpack: dst[idx[i]] = src[i].
+// K8  dispatch push   fused MoE dispatch: K2's expand form storing every
+//                     routed row straight into the owning rank's receive
+//                     buffer (NVLink), with K6's ready / done handshake.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -326,6 +329,130 @@ __global__ void __launch_bounds__(256) iccl_expand_rows(const int4* __restrict__
   }
 }
 
+// K8: fused MoE dispatch (K2's expand form + the alltoallv push in one
+// kernel, no staging buffer): each token row is read once and each of its k
+// routed copies is stored straight into the receive buffer of the rank that
+// owns the copy's packed position — over NVLink into an IPC mapping of the
+// peer's tensor, or locally for the self segment (no
+// intermediate buffer between the producer and the wire).
+//
+// Entry: the first CTA to arrive (a ticket, not blockIdx 0, so no CTA waits
+// on one that is not resident yet) polls every destination's ready flag (its
+// user stream reached the receive) and releases the others through a
+// gen-tagged word in local HBM.  Body: a warp per (token, column part); lanes
+// 0..k-1 resolve the k destination row pointers once (binary search of the
+// packed row over the per-rank ranges, in shared memory) and the warp
+// broadcasts them with shuffles.  Exit: the last CTA releases every
+// destination's done flag and this rank's send-op done flags (system scope,
+// after a system fence, like K6).
+__device__ __forceinline__ int fused_dest_of(const int64_t* hi, int n, int64_t p) {
+  int lo = 0, up = n - 1;  // first d with p < hi[d]
+  while (lo < up) {
+    const int mid = (lo + up) >> 1;
+    if (p < hi[mid]) up = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256) iccl_dispatch_push(const __grid_constant__ DispatchOp op) {
+  __shared__ int64_t s_lo[kMaxFusedRanks], s_hi[kMaxFusedRanks];
+  __shared__ int4* s_seg[kMaxFusedRanks];
+  for (int d = threadIdx.x; d < op.n; d += blockDim.x) {
+    s_lo[d] = op.d[d].lo;
+    s_hi[d] = op.d[d].hi;
+    s_seg[d] = (int4*)op.d[d].seg;
+  }
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = globaltimer();
+    if (atomicAdd(op.ticket, 1u) == 0) {
+      for (int d = 0; d < op.n; d++) {
+        if (!op.d[d].ready) continue;
+        uint32_t v;
+        do {
+          asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(op.d[d].ready) : "memory");
+          if ((int32_t)(v - op.d[d].ready_gen) < 0 && globaltimer() - t0 > 10000000000ull) {
+            *op.error = 1;
+            break;
+          }
+        } while ((int32_t)(v - op.d[d].ready_gen) < 0);
+      }
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(op.go), "r"(op.go_gen) : "memory");
+      if (op.stamp) {
+        const unsigned long long t = globaltimer();
+        asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(&op.stamp->t1), "l"(t) : "memory");
+      }
+    } else {
+      uint32_t v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(op.go) : "memory");
+        if (v != op.go_gen && globaltimer() - t0 > 10000000000ull) {
+          *op.error = 1;
+          break;
+        }
+      } while (v != op.go_gen);
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t row16 = op.row16;
+  const int64_t span = (row16 + op.parts - 1) / op.parts;
+  for (int64_t w = warp; w < op.n_tokens * op.parts; w += nwarps) {
+    const int64_t t = w / op.parts;
+    const int64_t c0 = (w % op.parts) * span, c1 = min(row16, c0 + span);
+    const int4* s = op.tokens + t * row16;
+    int4* mine = nullptr;
+    if (lane < op.k) {
+      const int64_t p = op.pos[t * op.k + lane];
+      const int d = fused_dest_of(s_hi, op.n, p);
+      mine = s_seg[d] + (p - s_lo[d]) * row16;
+    }
+    // warp-uniform loops: every lane takes part in the pointer shuffles
+    int64_t cb = c0;
+    for (; cb + 128 <= c1; cb += 128) {
+      const int64_t c = cb + lane;
+      const int4 v0 = ld_nc(s + c), v1 = ld_nc(s + c + 32), v2 = ld_nc(s + c + 64), v3 = ld_nc(s + c + 96);
+      for (int j = 0; j < op.k; j++) {
+        int4* d = (int4*)__shfl_sync(0xffffffffu, (unsigned long long)mine, j);
+        st_cs(d + c, v0);
+        st_cs(d + c + 32, v1);
+        st_cs(d + c + 64, v2);
+        st_cs(d + c + 96, v3);
+      }
+    }
+    for (; cb < c1; cb += 32) {
+      const int64_t c = cb + lane;
+      const int4 v = c < c1 ? ld_nc(s + c) : int4{0, 0, 0, 0};
+      for (int j = 0; j < op.k; j++) {
+        int4* d = (int4*)__shfl_sync(0xffffffffu, (unsigned long long)mine, j);
+        if (c < c1) st_cs(d + c, v);
+      }
+    }
+  }
+  __threadfence_system();  // every thread's row stores, before the CTA's arrival
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atomicAdd(op.counter, 1u) == gridDim.x - 1) {
+      atomicExch(op.counter, 0u);
+      atomicExch(op.ticket, 0u);
+      __threadfence_system();
+      if (op.stamp) {
+        const unsigned long long t = globaltimer();
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&op.stamp->t2), "l"(t) : "memory");
+      }
+      for (int d = 0; d < op.n; d++) {
+        if (op.d[d].done)
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(op.d[d].done), "r"(op.d[d].done_gen) : "memory");
+        if (op.d[d].my_done)
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(op.d[d].my_done), "r"(op.d[d].my_done_gen)
+                       : "memory");
+      }
+    }
+  }
+}
+
 // K3: inverse permutation (combine unpack), dst row idx[r] <- src row r.
 __global__ void __launch_bounds__(256) iccl_scatter_rows(const int4* __restrict__ src, int4* __restrict__ dst,
                                                         const int64_t* __restrict__ idx, int64_t n_rows,
@@ -536,7 +663,7 @@ cudaError_t preload_kernels() {
   const void* fns[] = {(const void*)iccl_copy_tma, (const void*)iccl_direct_copy,   (const void*)iccl_copy_unaligned,
                        (const void*)iccl_read_globaltimer, (const void*)iccl_gather_rows,
                        (const void*)iccl_scatter_rows, (const void*)iccl_expand_rows,
-                       (const void*)iccl_ll_group, (const void*)iccl_wait_flags};
+                       (const void*)iccl_ll_group, (const void*)iccl_wait_flags, (const void*)iccl_dispatch_push};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;
@@ -570,6 +697,27 @@ cudaError_t launch_gather_rows(const void* src, void* dst, const int64_t* idx, i
   if ((row_bytes & 15) || ((uintptr_t)src & 15) || ((uintptr_t)dst & 15)) return cudaErrorInvalidValue;
   iccl_gather_rows<<<rows_grid(n_rows, ctas), 256, 0, st>>>((const int4*)src, (int4*)dst, idx, n_rows,
                                                             row_bytes / 16);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dispatch(const DispatchOp& op, int ctas, cudaStream_t st, int* grid_out) {
+  if (grid_out) *grid_out = 0;
+  // launched even with no rows: its last CTA writes the done flags
+  if (op.k < 1 || op.k > 32 || op.n > kMaxFusedRanks || (op.row16 <= 0) || ((uintptr_t)op.tokens & 15)) return cudaErrorInvalidValue;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const int64_t warps = op.n_tokens * op.parts;
+  int64_t grid = (warps + 7) / 8;
+  const int64_t cap = ctas > 0 ? ctas : 4 * (int64_t)sms;  // 4 x 256-thread CTAs per SM resident
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  if (grid_out) *grid_out = (int)grid;
+  iccl_dispatch_push<<<(int)grid, 256, 0, st>>>(op);
   return cudaGetLastError();
 }
 

@@ -330,6 +330,7 @@ struct OpDesc {
   bool issued_direct = false;  // ... and that side is this one: K6 replaces this op's stream markers
   bool issued_instream = false;  // this side issued the copy on its own user stream (no markers)
   bool markers_elided = false;   // self pair, both halves on one stream in one group: no markers at all
+  bool fused = false;            // a send of a fused dispatch (K8 stores the rows; iccl_dispatch_rows)
   DirectOp dop{};        // K6 parameters when issued_direct
   int kstamp = -1;       // monitor on: K5 send / K6 stamp slot (K4), turned into a record by the proxy
 };
@@ -517,7 +518,17 @@ struct iccl_comm {
     cudaStream_t stream;  // this side's user stream
   };
   std::vector<GroupJob> group_jobs;  // copy-engine transfers this side issues for the open group
+  // fused MoE dispatch (iccl_dispatch_rows) in the open group: its sends
+  // rendezvous at group_end, then K8 runs on `stream` between the group's
+  // ready markers and its done waits
+  bool in_dispatch = false;   // ops posted now belong to a dispatch: no LL, K7 done waits
+  bool dispatch_fused = false;
+  cudaStream_t dispatch_stream = nullptr;
+  DispatchOp dispatch_op{};
+  char* dispatch_stage = nullptr;  // staging of the unfused fallback (an armed pair), grown on demand
+  size_t dispatch_stage_bytes = 0;
   int direct_ctas = 32;       // K6 grid (>= 16 CTAs keep NVLink busy, kernels bench)
+  int dispatch_ctas = 0;      // K8 grid cap (0: 4 CTAs per SM; ICCL_DISPATCH_CTAS)
   bool kernel_waits = true;   // K7 for the done waits of direct-class ops (ICCL_KERNEL_WAITS=0: memop waits)
   size_t k6_vec_bytes = 0;    // K6 copies ops up to this size with registers (ICCL_K6_VEC_KIB)
   bool device_flags = false;  // direct-class ready/done words also in GPU memory (ICCL_DEVICE_FLAGS=1; slower)
@@ -534,6 +545,7 @@ struct iccl_comm {
   // relay hop-1 stream
   int sm_si = -1, probe_si = -1, mon_si[2] = {-1, -1}, relay_si = -1;
   bool instream_ce = true;  // healthy pairs: the issuer enqueues the copy on its own user stream (ICCL_INSTREAM=0: off)
+  bool armed_backup = true;  // attribution only (ICCL_ARMED_BACKUP=0): armed transfers enqueue no backup attempt
   // monitor records of ops the proxy does not track (K5 sends, K6): their
   // %globaltimer stamps (K4), turned into records once t2 lands
   struct KRec {
@@ -542,6 +554,7 @@ struct iccl_comm {
     int peer, dir;
   };
   std::deque<KRec> krecs;  // mon_mu
+  std::atomic<uint64_t> krecs_pending{0};  // krecs.size(), readable without mon_mu (proxy nap, stats)
   std::thread proxy;
   std::atomic<bool> stop{false};
   std::mutex qmu;
@@ -1557,6 +1570,7 @@ static bool drain_kstamps(iccl_comm* c) {
     c->mon.push_back(m);
     if (c->mon.size() > (1u << 20)) c->mon.pop_front();
     it = c->krecs.erase(it);
+    c->krecs_pending.fetch_sub(1);
     any = true;
   }
   return any;
@@ -1576,7 +1590,8 @@ static void proxy_loop(iccl_comm* c) {
     bool busy = false;
     {
       std::unique_lock<std::mutex> lk(c->qmu);
-      if (c->handoff.empty() && c->pending_xfers.load() == 0 && now_ns() - idle_since > 200000) {
+      if (c->handoff.empty() && c->pending_xfers.load() == 0 && c->krecs_pending.load() == 0 &&
+          now_ns() - idle_since > 200000) {
         // a relay GPU has no transfers of its own: nap shorter so its
         // forwarding (hop 2) starts within ~50 us of a request
         c->qcv.wait_for(lk, std::chrono::microseconds(c->relay_buf ? 50 : 500));
@@ -2084,6 +2099,17 @@ static iccl_result_t armed_launch(iccl_comm* c, Xfer&& x, int kind, cudaStream_t
   x.instream = instream;
   x.ustream = instream ? us : nullptr;
   // backup attempt
+  if (!c->armed_backup) {  // attribution runs only: no failover possible
+    x.bstamp.assign(x.nchunks, -1);
+    __atomic_store_n(&w->b_fin, 1u, __ATOMIC_SEQ_CST);
+    x.done_enqueued = true;
+    x.t_obs = now_ns();
+    publish(c, x);
+    c->pending_xfers.fetch_add(1);
+    std::lock_guard<std::mutex> g(c->amu);
+    c->ahandoff.push_back(std::move(x));
+    return ICCL_SUCCESS;
+  }
   cudaStream_t bs = nullptr;
   r = backup_stream(c, chn, &bs);
   if (r) return r;
@@ -2374,6 +2400,7 @@ static void push_krec(iccl_comm* c, const OpDesc& op, int dir) {
   if (op.kstamp < 0) return;
   std::lock_guard<std::mutex> g(c->mon_mu);
   c->krecs.push_back(iccl_comm::KRec{op.kstamp, op.bytes, op.op_seq, op.peer, dir});
+  c->krecs_pending.fetch_add(1);
 }
 
 // Rendezvous of the k-th op of an ordered pair (SPEC.md:194's RTS / CTS): post
@@ -2518,6 +2545,83 @@ static iccl_result_t rzv_post(iccl_comm* c, OpDesc& op, uint64_t wait_us, bool g
     return issue_instream(c, std::move(x), kind, user_s);
   }
   return rzv_issue(c, kind, peer, k, op.op_seq, side, user_s);
+}
+
+// ---------------------------------------------------------------- fused dispatch (K8)
+// A send of a fused dispatch: its rows do not exist in any tensor yet (K8
+// produces them straight into the receiver's buffer), so it waits for the
+// receiver's half (CTS) unconditionally and always arrives second — the
+// receiver never issues.  The mapped receive segment and the two flags go
+// into the pending DispatchOp.  Every rank posts its dispatch receives
+// before any dispatch send waits (group order), so the wait cannot deadlock.
+static iccl_result_t fused_rendezvous(iccl_comm* c, OpDesc& op) {
+  const int peer = op.peer;
+  const uint64_t k = c->pair_sends[peer]++;
+  RzvEntry& e = rzv_entry(c, 0, peer, k);
+  const uint64_t g = k / kRzvDepth;
+  const uint64_t t0 = now_ns();
+  while (!rzv_free(e, k) || e.arrivals.load(std::memory_order_acquire) < 2 * g + 1) {
+    if (c->async_err.load() != ICCL_SUCCESS) return (iccl_result_t)c->async_err.load();
+    if (c->hdr->abort.load()) return ICCL_ERR_ABORTED;
+    if (now_ns() - t0 > 60ull * 1000000000ull) {
+      set_last_error("fused dispatch: rank " + std::to_string(peer) + " posted no matching receive within 60 s");
+      return ICCL_ERR_TIMEOUT;
+    }
+    sched_yield();
+  }
+  RzvSide& mine = e.side[0];
+  mine.bytes = op.bytes;
+  mine.slot = op.slot;
+  mine.gen = op.gen;
+  mine.direct_ptr = 0;
+  mine.stream = (uint64_t)(uintptr_t)c->dispatch_stream;
+  mine.buffer_id = 0;
+  mine.base_offset = 0;
+  RzvSide side[2];
+  ICCL_RETURN_IF(!rzv_arrive(e, k, side), ICCL_ERR_SYSTEM, "fused dispatch send arrived first");
+  const RzvSide& rcv = side[1];
+  if (rcv.bytes != op.bytes) {
+    __atomic_store_n(&flags_of(c, c->rank)->done[op.slot], op.gen, __ATOMIC_SEQ_CST);
+    __atomic_store_n(&flags_of(c, peer)->done[rcv.slot], rcv.gen, __ATOMIC_SEQ_CST);
+    std::string msg = "dispatch of " + std::to_string(op.bytes) + " B from rank " + std::to_string(c->rank) +
+                      " matched a receive of " + std::to_string(rcv.bytes) + " B on rank " + std::to_string(peer);
+    set_async(c, ICCL_ERR_SIZE_MISMATCH, msg);
+    set_last_error(msg);
+    return ICCL_ERR_SIZE_MISMATCH;
+  }
+  char* mapped = nullptr;
+  iccl_result_t r = open_peer_buffer(c, c->ch[2 * peer], rcv, &mapped);
+  if (r) return r;
+  FusedDest& d = c->dispatch_op.d[peer];
+  d.seg = mapped;
+  d.ready = &flags_of(c, peer)->ready[rcv.slot];
+  d.ready_gen = rcv.gen;
+  d.done = &flags_of(c, peer)->done[rcv.slot];
+  d.done_gen = rcv.gen;
+  d.my_done = &flags_of(c, c->rank)->done[op.slot];
+  d.my_done_gen = op.gen;
+  ICCL_TRACE("fused dispatch push %d->%d #%llu, %zu B", c->rank, peer, (unsigned long long)k, op.bytes);
+  return ICCL_SUCCESS;
+}
+
+// K8 for the pending dispatch on stream s (its remote sends: `sends`).
+static iccl_result_t launch_fused_dispatch(iccl_comm* c, cudaStream_t s, const std::vector<OpDesc>& sends) {
+  DispatchOp& op = c->dispatch_op;
+  OpDesc rec{};
+  op.stamp = alloc_kstamp(c, rec);
+  int grid = 0;
+  ICCL_CHECK_CUDA(launch_dispatch(op, c->dispatch_ctas, s, &grid));
+  c->kernels_launched += 1;
+  c->ctas_launched += grid;
+  c->dispatch_fused = false;  // launched
+  for (const OpDesc& o : sends) {
+    c->copies_issued += 1;
+    c->bytes_issued += o.bytes;
+    OpDesc m = o;
+    m.kstamp = rec.kstamp;
+    push_krec(c, m, 0);
+  }
+  return ICCL_SUCCESS;
 }
 
 // K6 for every op of `ops` this side issues directly, on stream s.
@@ -2684,11 +2788,17 @@ static iccl_result_t enqueue_op(iccl_comm* c, int kind, const void* buf, size_t 
   // Small messages between different GPUs take the LL kernel path (K5) unless
   // the copy-engine transport is forced or the pair is armed for failover
   // (route_small: both sides route the pair's q-th small op alike).
-  const bool small = peer != c->rank && c->cfg.transport != ICCL_TRANSPORT_CE && bytes <= c->cfg.sm_small_bytes &&
-                     bytes <= kLLMaxBytes && c->ll_region != nullptr;
+  // (a dispatch's segments never take LL: a fused sender has no source
+  // tensor to stream, and both sides must classify alike)
+  const bool small = !c->in_dispatch && peer != c->rank && c->cfg.transport != ICCL_TRANSPORT_CE &&
+                     bytes <= c->cfg.sm_small_bytes && bytes <= kLLMaxBytes && c->ll_region != nullptr;
   op.ll = small && !route_small(pair_of(c, kind == 0 ? c->rank : peer, kind == 0 ? peer : c->rank), kind);
   op.direct = !small && peer != c->rank && c->cfg.transport == ICCL_TRANSPORT_AUTO &&
               bytes <= (size_t)c->cfg.direct_max_kib * 1024;
+  if (c->in_dispatch && peer != c->rank) {
+    if (kind == 1) op.direct = true;  // done wait in K7 (whoever fills the segment)
+    op.fused = kind == 0 && c->dispatch_fused;
+  }
   if (op.ll) {
     op.ll_seq = kind == 0 ? ++c->ll_sent[peer] : ++c->ll_recvd[peer];
   } else if (kind == 1 || c->group_depth == 0) {
@@ -2815,6 +2925,7 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
     c->device_flags = env_us("ICCL_DEVICE_FLAGS", 0) != 0;
     c->event_ready = env_us("ICCL_EVENT_READY", 0) != 0;
     c->k6_vec_bytes = (size_t)env_us("ICCL_K6_VEC_KIB", 0) * 1024;
+    c->dispatch_ctas = (int)env_us("ICCL_DISPATCH_CTAS", 0);
     // kLLCounters arrival counters + kLLCounters K6 go words
     ICCL_CHECK_CUDA(cudaMalloc((void**)&c->ll_counters, 2 * kLLCounters * sizeof(unsigned int)));
     ICCL_CHECK_CUDA(cudaMemset(c->ll_counters, 0, 2 * kLLCounters * sizeof(unsigned int)));
@@ -2886,6 +2997,7 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
   c->mon_si[1] = mk_stream(ENG_CE);
   if (c->relay_buf) c->relay_si = mk_stream(ENG_RELAY);
   c->instream_ce = env_us("ICCL_INSTREAM", 1) != 0;
+  c->armed_backup = env_us("ICCL_ARMED_BACKUP", 1) != 0;
   std::vector<char*> peer_scratch(nranks, nullptr);
   for (int p = 0; p < nranks; p++) {
     if (p == rank) {
@@ -3095,7 +3207,7 @@ iccl_result_t iccl_comm_stats(iccl_comm_t c, iccl_stats_t* s) {
   s->bytes_issued = c->bytes_issued.load();
   s->pulls_issued = c->pulls_issued.load();
   s->cts_timeouts = c->cts_timeouts.load();
-  s->pending_xfers = c->pending_xfers.load();
+  s->pending_xfers = c->pending_xfers.load() + c->krecs_pending.load();  // K5 / K6 / K8 records not yet emitted count
   return ICCL_SUCCESS;
 }
 
@@ -3163,6 +3275,11 @@ iccl_result_t iccl_group_end(iccl_comm_t c) {
   const uint64_t deadline = now_ns() + kGroupSendWaitUs * 1000ull;
   for (auto& p : ops) {
     if (p.first.kind != 0 || p.first.ll) continue;
+    if (p.first.fused) {
+      iccl_result_t r = fused_rendezvous(c, p.first);
+      if (r) return r;
+      continue;
+    }
     const uint64_t t = now_ns();
     iccl_result_t r = rzv_post(c, p.first, t < deadline ? (deadline - t) / 1000 : 0, true, p.second);
     if (r) return r;
@@ -3233,15 +3350,16 @@ iccl_result_t iccl_group_end(iccl_comm_t c) {
   for (auto& p : ops)
     if (std::find(order.begin(), order.end(), p.second) == order.end()) order.push_back(p.second);
   for (cudaStream_t s : order) {
-    std::vector<OpDesc> ce, ll, direct;
+    std::vector<OpDesc> ce, ll, direct, fused;
     for (auto& p : ops) {
       if (p.second != s || p.first.issued_instream || p.first.markers_elided) continue;
-      (p.first.ll ? ll : p.first.issued_direct ? direct : ce).push_back(p.first);
+      (p.first.fused ? fused : p.first.ll ? ll : p.first.issued_direct ? direct : ce).push_back(p.first);
     }
     iccl_result_t r = ICCL_SUCCESS;
     if (!ce.empty()) r = stream_markers(c, s, ce, 1);  // ready
     if (!r && !ll.empty()) r = launch_ll_ops(c, s, ll);
     if (!r && !direct.empty()) r = launch_direct_ops(c, s, direct);
+    if (!r && c->dispatch_fused && c->dispatch_stream == s) r = launch_fused_dispatch(c, s, fused);
     if (r) return r;
     std::vector<CUstreamBatchMemOpParams> p;
     std::vector<size_t> mine;
@@ -3265,6 +3383,7 @@ iccl_result_t iccl_group_end(iccl_comm_t c) {
     if (r) return r;
     for (const OpDesc& o : ll) publish_simple(c, o, 1);
     for (const OpDesc& o : direct) publish_simple(c, o, 1);
+    for (const OpDesc& o : fused) publish_simple(c, o, 1);
   }
   return ICCL_SUCCESS;
 }
@@ -3287,6 +3406,109 @@ iccl_result_t iccl_alltoallv(iccl_comm_t c, const void* sbuf, const size_t* scou
   }
   iccl_result_t r2 = iccl_group_end(c);
   return r ? r : r2;
+}
+
+// Fused MoE dispatch (K8): see include/iccl_b200.h.  Equivalent to
+// iccl_expand_rows into a packed buffer followed by iccl_alltoallv of it, in
+// one kernel and without the packed buffer.  If a pair this rank sends to is
+// armed for failover (a fault script names it, or it runs on its backup
+// path), the call takes exactly that unfused form instead — K2 into a staging
+// buffer, then the alltoallv, where the gates, the watchdog and the switch
+// apply; receivers cannot tell the two forms apart.
+iccl_result_t iccl_dispatch_rows(iccl_comm_t c, const void* tokens, int64_t n_tokens, int32_t k, const int64_t* pos,
+                                 const size_t* scounts, void* rbuf, const size_t* rcounts, int64_t row_bytes,
+                                 cudaStream_t s) {
+  ICCL_RETURN_IF(!c || !scounts || !rcounts || n_tokens < 0 || k < 1 || k > 32 || row_bytes <= 0 || (row_bytes & 15),
+                 ICCL_ERR_INVALID_ARGUMENT, "dispatch: bad arguments (1 <= k <= 32, row_bytes a multiple of 16)");
+  ICCL_RETURN_IF(c->group_depth > 0, ICCL_ERR_INVALID_ARGUMENT, "dispatch inside a group");
+  ICCL_RETURN_IF(c->nranks > kMaxFusedRanks, ICCL_ERR_INVALID_ARGUMENT, "dispatch: more than 64 ranks");
+  ICCL_RETURN_IF(((uintptr_t)tokens & 15) || ((uintptr_t)rbuf & 15), ICCL_ERR_INVALID_ARGUMENT,
+                 "dispatch: tokens and the receive buffer must be 16-byte aligned");
+  int ae = c->async_err.load();
+  if (ae != ICCL_SUCCESS) {
+    set_last_error(c->async_msg);
+    return (iccl_result_t)ae;
+  }
+  const int n = c->nranks, me = c->rank;
+  std::vector<size_t> sd(n), rd(n);
+  size_t stot = 0, rtot = 0;
+  for (int d = 0; d < n; d++) {
+    sd[d] = stot;
+    rd[d] = rtot;
+    stot += scounts[d];
+    rtot += rcounts[d];
+  }
+  ICCL_RETURN_IF(stot != (size_t)n_tokens * (size_t)k, ICCL_ERR_INVALID_ARGUMENT,
+                 "dispatch: send counts must add up to n_tokens * k");
+  ICCL_RETURN_IF(scounts[me] != rcounts[me], ICCL_ERR_SIZE_MISMATCH, "dispatch: self send and receive counts differ");
+  ICCL_RETURN_IF(stot > 0 && (!tokens || !pos), ICCL_ERR_INVALID_ARGUMENT, "dispatch: null tokens / pos");
+  ICCL_RETURN_IF(rtot > 0 && !rbuf, ICCL_ERR_INVALID_ARGUMENT, "dispatch: null receive buffer");
+  bool fused = true;
+  for (int d = 0; d < n && fused; d++)
+    if (d != me && scounts[d] && xfer_armed(c, 0, d)) fused = false;
+  iccl_result_t r = ICCL_SUCCESS;
+  if (!fused) {
+    const size_t need = stot * (size_t)row_bytes;
+    if (need > c->dispatch_stage_bytes) {
+      if (c->dispatch_stage) {
+        ICCL_CHECK_CUDA(cudaStreamSynchronize(s));  // the previous fallback's copies may still read it
+        ICCL_CHECK_CUDA(cudaFree(c->dispatch_stage));
+        c->dispatch_stage = nullptr;
+      }
+      ICCL_CHECK_CUDA(cudaMalloc((void**)&c->dispatch_stage, need));
+      c->dispatch_stage_bytes = need;
+    }
+    if (stot) ICCL_CHECK_CUDA(launch_expand_rows(tokens, c->dispatch_stage, pos, n_tokens, k, row_bytes, 148 * 8, s));
+    c->in_dispatch = true;
+    r = iccl_alltoallv(c, c->dispatch_stage, scounts, sd.data(), rbuf, rcounts, rd.data(), (size_t)row_bytes, s);
+    c->in_dispatch = false;
+    return r;
+  }
+  // the dispatch's own op slot: its done flag (written by K8's last CTA)
+  // retires it, and it keys K8's go word
+  OpDesc dop{};
+  r = next_slot(c, &dop.slot, &dop.gen, &dop.op_seq);
+  if (r) return r;
+  DispatchOp& op = c->dispatch_op;
+  memset(&op, 0, sizeof(op));
+  op.tokens = (const int4*)tokens;
+  op.pos = pos;
+  op.n_tokens = n_tokens;
+  op.k = k;
+  op.n = n;
+  op.row16 = row_bytes / 16;
+  op.parts = (int)std::max<int64_t>(1, std::min<int64_t>(8, op.row16 / 128));
+  op.ticket = c->ll_counters + (c->ll_ctr_next++ % kLLCounters);
+  op.counter = c->ll_counters + (c->ll_ctr_next++ % kLLCounters);
+  op.go = c->ll_counters + kLLCounters + (dop.slot % kLLCounters);
+  op.go_gen = dop.gen;
+  op.error = c->ll_error;
+  for (int d = 0; d < n; d++) {
+    op.d[d].lo = (int64_t)sd[d];
+    op.d[d].hi = (int64_t)(sd[d] + scounts[d]);
+  }
+  op.d[me].seg = (char*)rbuf + rd[me] * (size_t)row_bytes;
+  op.d[me].my_done = &flags_of(c, me)->done[dop.slot];
+  op.d[me].my_done_gen = dop.gen;
+  c->dispatch_stream = s;
+  c->dispatch_fused = true;
+  c->in_dispatch = true;
+  r = iccl_group_start(c);
+  // rotated like iccl_alltoallv; the self segment is K8's local store
+  for (int kk = 1; kk < n && r == ICCL_SUCCESS; kk++) {
+    const int to = (me + kk) % n, from = (me - kk + n) % n;
+    if (rcounts[from]) r = iccl_recv(c, (char*)rbuf + rd[from] * (size_t)row_bytes, rcounts[from] * (size_t)row_bytes,
+                                     from, s, nullptr);
+    if (!r && scounts[to]) r = iccl_send(c, tokens, scounts[to] * (size_t)row_bytes, to, s, nullptr);
+  }
+  iccl_result_t r2 = iccl_group_end(c);
+  if (!r) r = r2;
+  // no remote send on s (a single rank, or every row stays here): K8 still
+  // stores the self segment
+  if (!r && c->dispatch_fused) r = launch_fused_dispatch(c, s, {});
+  c->dispatch_fused = false;
+  c->in_dispatch = false;
+  return r;
 }
 
 iccl_result_t iccl_alltoall(iccl_comm_t c, const void* sbuf, void* rbuf, size_t bytes_per_pair, cudaStream_t s) {

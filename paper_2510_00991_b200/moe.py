@@ -122,6 +122,32 @@ def moe_dispatch(comm, tokens: torch.Tensor, plan: DispatchPlan, packed: Optiona
     return packed, recv
 
 
+def moe_dispatch_fused(comm, tokens: torch.Tensor, plan: DispatchPlan, recv: Optional[torch.Tensor] = None,
+                       stream=None) -> torch.Tensor:
+    """The same result as :func:`moe_dispatch` (rows received from every
+    rank, grouped by source) in one kernel, K8 (``iccl_dispatch_rows``): each
+    token row is read once and each of its k routed copies is stored straight
+    into the receive buffer of the rank that owns it — over NVLink, with no
+    packed staging buffer.  Pairs armed for failover take
+    the unfused form inside the library, with the same result."""
+    if not tokens.is_cuda or not tokens.is_contiguous():
+        raise InvalidArgument("tokens must be a contiguous CUDA tensor")
+    T = tokens.shape[0]
+    k = plan.pos.numel() // T if T else 1
+    row = tokens[0].numel() * tokens.element_size() if T else 16
+    if recv is None:
+        recv = torch.empty((sum(plan.recv_counts),) + tuple(tokens.shape[1:]), dtype=tokens.dtype,
+                           device=tokens.device)
+    n = len(plan.send_counts)
+    Arr = C.c_size_t * n
+    sc = Arr(*[int(x) for x in plan.send_counts])
+    rc = Arr(*[int(x) for x in plan.recv_counts])
+    raise_for(lib.iccl_dispatch_rows(comm._h, C.c_void_p(tokens.data_ptr()), T, int(k),
+                                     C.c_void_p(plan.pos.data_ptr()), sc, C.c_void_p(recv.data_ptr()), rc, int(row),
+                                     _sh(stream)), "iccl_dispatch_rows")
+    return recv
+
+
 def moe_combine(comm, expert_out: torch.Tensor, plan: DispatchPlan, T: int, k: int,
                 back: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None, stream=None):
     """Reverse alltoallv with the same counts, then K3 puts every row back at

@@ -13,6 +13,9 @@
 #   gemm        gemm_interference on all GPUs: none, iccl-ce 256 MiB, iccl-auto / nccl at 4 and 16 MiB
 #   failover    benchmarks/failover.py on all GPUs (sm backup; relay when >= 3 GPUs)
 #   moe         benchmarks/moe_alltoallv.py on all GPUs, iccl and nccl
+#   armedexp    p2p_sweep 1-256 MiB: plain / armed (a never-firing fault script) / armed without the
+#               backup attempt (attribution), default and 8 MiB chunks, monitor on
+#   dispatch    benchmarks/moe_dispatch.py on all GPUs: fused K8 vs K2 + alltoallv vs NCCL
 #   launches    ncu launch list of smoke() (gpu__time_duration, no replay of waits)
 #   ncuprobe    probes/ncu_xproc under ncu (cross-process serialisation)
 #   sanitize    compute-sanitizer memcheck/racecheck/synccheck on benchmarks/kernels.py
@@ -46,7 +49,15 @@ for STEP in "$@"; do
             timeout 600 $TR --nproc-per-node $NG --master-port 29676 benchmarks/gemm_interference.py --impl $I --msg-mib $M >> "$LOG" 2>&1
           done; done ;;
     failover) timeout 600 $TR --nproc-per-node $NG --master-port 29677 benchmarks/failover.py >> "$LOG" 2>&1
-              [ "$NG" -ge 3 ] && timeout 600 $TR --nproc-per-node $NG --master-port 29678 benchmarks/failover.py --backup relay >> "$LOG" 2>&1 ;;
+              [ "$NG" -ge 3 ] && timeout 600 $TR --nproc-per-node $NG --master-port 29678 benchmarks/failover.py --backup relay >> "$LOG" 2>&1 || true ;;
+    armedexp) for V in "" "--armed" "--armed ICCL_ARMED_BACKUP=0" "--chunk-bytes 8388608" "--chunk-bytes 8388608 --armed" \
+                    "--chunk-bytes 8388608 --armed ICCL_ARMED_BACKUP=0" "--chunk-bytes 8388608 --monitor"; do
+                A=$(echo "$V" | sed 's/ICCL_ARMED_BACKUP=0//'); E=$(echo "$V" | grep -o 'ICCL_ARMED_BACKUP=0')
+                echo "## $V" >> "$LOG"
+                env $E timeout 600 $TR --nproc-per-node 2 --master-port 29681 benchmarks/p2p_sweep.py --impl iccl-auto \
+                  --min-pow 20 --max-pow 28 --step 2 $A >> "$LOG" 2>&1
+              done ;;
+    dispatch) timeout 600 $TR --nproc-per-node $NG --master-port 29680 benchmarks/moe_dispatch.py >> "$LOG" 2>&1 ;;
     moe) for I in iccl nccl; do timeout 600 $TR --nproc-per-node $NG --master-port 29679 benchmarks/moe_alltoallv.py --impl $I >> "$LOG" 2>&1; done ;;
     launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --target-processes all -c 2000 --csv \
                 --log-file gpurun_out/${TAG}_launches.csv python -c "import __graft_entry__ as g; g.smoke()" >> "$LOG" 2>&1 ;;

@@ -430,13 +430,16 @@ def monitor_accuracy(comm, rank, world, nchunks, chunk, stall_chunk, up_us):
     out["t1"] = np.array([r.t1 for r in recs], np.int64)
     out["t2"] = np.array([r.t2 for r in recs], np.int64)
     out["bytes"] = np.array([r.size for r in recs], np.int64)
-    out["switches"] = np.array([len(comm.switch_events())], np.int64)
+    ev = comm.switch_events()
+    out["switches"] = np.array([len(ev)], np.int64)
+    out["switch_desc"] = np.array([f"{e['trigger']}->{e['to']}@{e['resume_chunk']} after {e['detect_ns']} ns"
+                                   for e in ev] or [""])
     if rank == 1:
         out["ok"] = np.array([bool(torch.equal(dst, to_dev(payload(n, seed=5), dev)))])
     return out
 
 
-def moe_config4(comm, rank, world, T, k=8, E=64, H=7168, fault=None, keep_bytes=True):
+def moe_config4(comm, rank, world, T, k=8, E=64, H=7168, fault=None, keep_bytes=True, fused=False, reps=1):
     """BASELINE config 4 at `world` ranks: K2 pack (expand), dispatch
     alltoallv, combine alltoallv, K3 unpack, with the §8(d) routing and
     payload.  Checks on the device, at any size: every rank's received rows
@@ -444,14 +447,19 @@ def moe_config4(comm, rank, world, T, k=8, E=64, H=7168, fault=None, keep_bytes=
     sources' seeds), and the combine round trip restores (token, k) order.
     With keep_bytes the packed send rows and the received rows come back for
     the oracle comparison.  `fault` = (src, dst, chunk): a FaultScript Down on
-    that pair's primary path at that chunk of its first transfer (config 5)."""
+    that pair's primary path at that chunk of its first transfer (config 5).
+    fused: the dispatch is K8 (moe_dispatch_fused) instead of K2 + alltoallv;
+    `packed` is then built afterwards, for the oracle comparison only.  reps:
+    the dispatch runs that many times (buffers reused, the last one checked)."""
     from paper_2510_00991_b200 import FaultScript
-    from paper_2510_00991_b200.moe import (config4_routing, config4_tokens, expand_rows, plan_dispatch,
-                                           scatter_rows)
+    from paper_2510_00991_b200.moe import (config4_routing, config4_tokens, expand_rows, moe_dispatch_fused,
+                                           plan_dispatch, scatter_rows)
     dev = dev_of(rank)
     experts = config4_routing(rank, T, k, E, dev)
 
     def exchange(send_counts):
+        if world == 1:
+            return list(send_counts)
         s = torch.tensor(send_counts, dtype=torch.int64, device=dev)
         r = torch.empty_like(s)
         comm.alltoall(r, s)  # the one exchange step, through the product's own alltoall
@@ -467,8 +475,15 @@ def moe_config4(comm, rank, world, T, k=8, E=64, H=7168, fault=None, keep_bytes=
     recv = torch.empty(sum(plan.recv_counts), H, dtype=tokens.dtype, device=dev)
     back = torch.empty_like(packed)
     out = torch.empty_like(packed)
-    expand_rows(tokens, plan.pos, k, packed)
-    comm.alltoallv(recv, packed, plan.recv_counts, plan.send_counts)
+    for _ in range(reps):
+        if fused:
+            recv.fill_(0)
+            moe_dispatch_fused(comm, tokens, plan, recv)
+        else:
+            expand_rows(tokens, plan.pos, k, packed)
+            comm.alltoallv(recv, packed, plan.recv_counts, plan.send_counts)
+    if fused:
+        expand_rows(tokens, plan.pos, k, packed)
     comm.alltoallv(back, recv, plan.send_counts, plan.recv_counts)
     scatter_rows(back, plan.order, out)
     torch.cuda.synchronize()
@@ -494,6 +509,7 @@ def moe_config4(comm, rank, world, T, k=8, E=64, H=7168, fault=None, keep_bytes=
     res["switch_peers"] = np.array([e["peer"] for e in ev], np.int64)
     res["switch_to"] = np.array([0 if e["to"] == "primary" else 1 for e in ev], np.int64)
     res["records"] = np.array([len(comm.monitor.drain())], np.int64)
+    res["kernels"] = np.array([comm.stats()["kernels_launched"]], np.int64)
     return res
 
 

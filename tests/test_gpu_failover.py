@@ -150,7 +150,7 @@ def test_AC5_monitor_accuracy_and_smoothing(torch_cuda, tmp_path):
                     up_us=5000, config=cfg)
     t1, t2, b = _recs(res)
     assert len(b) == 128 and bool(res[1]["ok"][0])
-    assert int(res[0]["switches"][0]) + int(res[1]["switches"][0]) == 0
+    assert int(res[0]["switches"][0]) + int(res[1]["switches"][0]) == 0, (res[0]["switch_desc"], res[1]["switch_desc"])
     dur = t2 - t1
     k = int(np.argmax(dur))  # the disturbed record (waited behind the gate)
     assert dur[k] > 10 * np.median(dur), "the gate must show as one long record"
