@@ -50,7 +50,7 @@ def main():
     ap.add_argument("--ll-bytes", type=int, default=-1)
     ap.add_argument("--armed", action="store_true",
                     help="install a fault script on pair 0->1 that never fires: its ops take the failover-capable path")
-    ap.add_argument("--monitor", action="store_true", help="window monitor on")
+    ap.add_argument("--records", action="store_true", help="window monitor on")
     args = ap.parse_args()
     if args.impl == "nccl-ce":
         os.environ["NCCL_P2P_USE_CUDA_MEMCPY"] = "1"
@@ -70,7 +70,7 @@ def main():
             cfg.chunk_bytes = args.chunk_bytes
         if args.ll_bytes >= 0:
             cfg.sm_small_bytes = args.ll_bytes
-        cfg.monitor_enabled = bool(args.monitor)
+        cfg.monitor_enabled = bool(args.records)
         comm = iccl.init(rank, world, local, cfg)
         if args.armed:
             comm.set_faults(iccl.FaultScript().down(0, 1, chunk=1 << 30, op_index=1 << 30))
@@ -131,7 +131,7 @@ def main():
         for _ in range(3):
             pp_loop(s, r)()
         rec = {"impl": args.impl, "bytes": n, "bidir": bool(args.bidir), "armed": bool(args.armed),
-               "monitor": bool(args.monitor), "chunk_bytes": args.chunk_bytes}
+               "monitor": bool(args.records), "chunk_bytes": args.chunk_bytes}
         if comm:
             comm.monitor.drain()
         for mode, pre in (("gpu", True), ("api", False)):

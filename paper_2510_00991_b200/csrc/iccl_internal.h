@@ -68,6 +68,43 @@ struct alignas(64) KernelStamp {
 // attempt of an armed transfer skips the chunks the primary delivered).
 cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, KernelStamp* stamp, cudaStream_t st,
                         int* grid_out = nullptr, const uint32_t* resume = nullptr, uint32_t chunk = 0);
+// Host-mapped words of one armed transfer (iccl_runtime.cpp armed_launch).
+// Device writes come from stream memops and the backup kernel (K9); the
+// watchdog thread only loads and stores them.
+enum ArmedCtl : uint32_t { kCtlNone = 0, kCtlProbe = 1, kCtlSwitch = 2, kCtlAbort = 3 };
+enum ArmedDec : uint32_t { kDecNone = 0, kDecExit = 1, kDecCopy = 2 };
+struct alignas(64) ArmedWords {
+  uint32_t prog;        // primary chunks landed (a memop after each primary chunk)
+  uint32_t go;          // K9 may start: the primary finished, or the watchdog needs it (probe / switch)
+  uint32_t resume;      // once switched, K9 copies chunks [resume, nchunks)
+  uint32_t ctl;         // watchdog -> K9 (ArmedCtl)
+  uint32_t probe_done;  // K9's CTS probe crossed the primary path
+  uint32_t ns;          // no switch (1): the primary writes the done flags itself
+  uint32_t p_fin;       // the primary attempt's copies (stale ones included) all landed
+  uint32_t b_fin;       // the backup attempt drained
+  uint32_t fin;         // the primary passed its done writes (the slot may be reused)
+  uint32_t dec;         // K9's decision (ArmedDec), which its CTAs follow
+  uint32_t pad[6];
+};
+// K9: the backup attempt of an armed transfer, one launch per transfer,
+// started once `go` opens.  CTA 0 decides: the primary finished with no
+// switch -> every CTA exits; the watchdog asked for a probe -> a 16-byte CTS
+// store over the primary path (unless that path's fault gate is closed) and
+// probe_done; switched -> K1 over chunks [resume, nchunks) with a K4 stamp per
+// chunk (ring[(stamp_base + k) % ring_slots]).
+struct BackupOp {
+  const char* src;
+  char* dst;
+  size_t bytes, chunk;
+  uint32_t nchunks, ring_slots, stamp_base, pad;
+  KernelStamp* ring;
+  ArmedWords* w;
+  const uint32_t* gate;    // the primary path's fault gate word when the transfer was issued behind it, or null
+  const char* probe_src;   // 16 bytes moved by the probe (over the primary path's direction)
+  char* probe_dst;
+  unsigned int* error;     // host-mapped: set if the decision wait exceeds 60 s
+};
+cudaError_t launch_backup(const BackupOp& op, int ctas, cudaStream_t st, int* grid_out = nullptr);
 // K6: direct zero-copy of a mid-size message by the side that arrived second
 // at the rendezvous, on its own user stream (see rzv_post).
 struct DirectOp {

@@ -15,6 +15,8 @@
 //                     move yields a WR/WC record.
 // K2  gather rows     MoE dispatch pack: dst[i] = src[idx[i]] (16 B vectors).
 // K3  scatter rows    MoE combine unpack: dst[idx[i]] = src[i].
+// K9  backup attempt  the pre-enqueued backup of an armed transfer: CTS
+//                     probe on request, K1 over the suffix after a switch.
 // K8  dispatch push   fused MoE dispatch: K2's expand form storing every
 //                     routed row straight into the owning rank's receive
 //                     buffer (NVLink), with K6's ready / done handshake.
@@ -163,6 +165,82 @@ __global__ void __launch_bounds__(kCopyThreads) iccl_copy_tma(const char* __rest
   stamp_begin(stamp);
   tma_copy(src, dst, head, body, tail, smem, mbar);
   stamp_end(stamp);
+}
+
+// K9: the backup attempt of an armed transfer (iccl_internal.h BackupOp),
+// one launch per transfer on the channel's backup stream behind a wait on
+// `go`.  Thread 0 of CTA 0 is the controller: it spins on the watchdog's ctl
+// word and the primary's p_fin until it can decide, runs the CTS probe when
+// asked, and publishes the decision through w->dec, which the other CTAs
+// poll.  A transfer that never fails costs one near-empty launch: the
+// primary's end opens `go` with p_fin already set.
+__device__ __forceinline__ uint32_t ld_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kCopyThreads) iccl_backup_attempt(const __grid_constant__ BackupOp op) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(8) uint64_t mbar[kStages];
+  __shared__ uint32_t s_dec;
+  ArmedWords* w = op.w;
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = globaltimer();
+    uint32_t dec = kDecNone;
+    if (blockIdx.x == 0) {
+      bool probed = false;
+      while (dec == kDecNone) {
+        const uint32_t ctl = ld_sys(&w->ctl);
+        if (ctl == kCtlSwitch) {
+          dec = kDecCopy;
+        } else if (ctl == kCtlAbort) {
+          dec = kDecExit;
+        } else if (ld_sys(&w->p_fin)) {
+          dec = ld_sys(&w->ctl) == kCtlSwitch ? kDecCopy : kDecExit;  // a switch racing the primary's end still copies
+        } else if (ctl == kCtlProbe && !probed && (!op.gate || ld_sys(op.gate) != 0)) {
+          // the CTS crosses the primary path: lost while its gate is closed
+          int4 v;
+          asm volatile("ld.volatile.global.v4.s32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(op.probe_src) : "memory");
+          asm volatile("st.volatile.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(op.probe_dst), "r"(v.x), "r"(v.y),
+                       "r"(v.z), "r"(v.w) : "memory");
+          __threadfence_system();
+          st_sys(&w->probe_done, 1u);
+          probed = true;
+        } else if (globaltimer() - t0 > 60000000000ull) {
+          *op.error = 1;
+          dec = kDecExit;
+        }
+      }
+      st_sys(&w->dec, dec);
+    } else {
+      while ((dec = ld_sys(&w->dec)) == kDecNone) {
+        if (globaltimer() - t0 > 61000000000ull) {
+          *op.error = 1;
+          dec = kDecExit;
+        }
+      }
+    }
+    s_dec = dec;
+  }
+  __syncthreads();
+  if (s_dec != kDecCopy) return;
+  const uint32_t r = ld_sys(&w->resume);
+  for (uint32_t k = r; k < op.nchunks; k++) {
+    const size_t off = (size_t)k * op.chunk, n = min(op.chunk, op.bytes - off);
+    const uintptr_t a = (uintptr_t)(op.src + off);
+    size_t head = (16 - (a & 15)) & 15;
+    if (head > n) head = n;
+    const size_t body = (n - head) & ~(size_t)15, tail = n - head - body;
+    KernelStamp* st = &op.ring[(op.stamp_base + k) % op.ring_slots];
+    stamp_begin(st);
+    tma_copy(op.src + off, op.dst + off, head, body, tail, smem, mbar);
+    stamp_end(st);
+  }
 }
 
 // K6: the direct path for mid-size messages.  Launched on the issuing
@@ -570,6 +648,17 @@ __global__ void __launch_bounds__(256) iccl_ll_group(LLBatch b) {
 }
 
 bool smem_configured = false;
+// Dynamic shared memory of the TMA-ring kernels (K1, K1 chunks, K6), once.
+cudaError_t configure_smem() {
+  if (smem_configured) return cudaSuccess;
+  const void* fns[] = {(const void*)iccl_copy_tma, (const void*)iccl_direct_copy, (const void*)iccl_backup_attempt};
+  for (const void* f : fns) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kStages * kTile);
+    if (e != cudaSuccess) return e;
+  }
+  smem_configured = true;
+  return cudaSuccess;
+}
 
 }  // namespace
 
@@ -623,6 +712,19 @@ cudaError_t launch_direct(DirectOp op, size_t bytes, int ctas, cudaStream_t st, 
   return cudaGetLastError();
 }
 
+cudaError_t launch_backup(const BackupOp& op, int ctas, cudaStream_t st, int* grid_out) {
+  if (grid_out) *grid_out = 0;
+  if ((((uintptr_t)op.src ^ (uintptr_t)op.dst) & 15) != 0 || (op.chunk & 15) || op.nchunks == 0)
+    return cudaErrorInvalidValue;
+  if (cudaError_t e = configure_smem()) return e;
+  const size_t ntiles = (min(op.chunk, op.bytes) + kTile - 1) / kTile;
+  int grid = (int)min((size_t)ctas, ntiles > 0 ? ntiles : (size_t)1);
+  if (grid < 1) grid = 1;
+  if (grid_out) *grid_out = grid;
+  iccl_backup_attempt<<<grid, kCopyThreads, kStages * kTile, st>>>(op);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, KernelStamp* stamp, cudaStream_t st,
                         int* grid_out, const uint32_t* resume, uint32_t chunk) {
   if (grid_out) *grid_out = 0;
@@ -639,11 +741,7 @@ cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int ctas, Kern
   if (head > bytes) head = bytes;
   size_t body = (bytes - head) & ~(size_t)15;
   size_t tail = bytes - head - body;
-  if (!smem_configured) {
-    cudaError_t e = cudaFuncSetAttribute(iccl_copy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kStages * kTile);
-    if (e != cudaSuccess) return e;
-    smem_configured = true;
-  }
+  if (cudaError_t e = configure_smem()) return e;
   size_t ntiles = (body + kTile - 1) / kTile;
   int grid = (int)min((size_t)ctas, ntiles > 0 ? ntiles : (size_t)1);
   if (grid < 1) grid = 1;
@@ -663,18 +761,13 @@ cudaError_t preload_kernels() {
   const void* fns[] = {(const void*)iccl_copy_tma, (const void*)iccl_direct_copy,   (const void*)iccl_copy_unaligned,
                        (const void*)iccl_read_globaltimer, (const void*)iccl_gather_rows,
                        (const void*)iccl_scatter_rows, (const void*)iccl_expand_rows,
-                       (const void*)iccl_ll_group, (const void*)iccl_wait_flags, (const void*)iccl_dispatch_push};
+                       (const void*)iccl_ll_group, (const void*)iccl_wait_flags, (const void*)iccl_dispatch_push,
+                       (const void*)iccl_backup_attempt};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;
   }
-  if (!smem_configured) {
-    cudaError_t e = cudaFuncSetAttribute(iccl_copy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kStages * kTile);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(iccl_direct_copy, cudaFuncAttributeMaxDynamicSharedMemorySize, kStages * kTile);
-    if (e != cudaSuccess) return e;
-    smem_configured = true;
-  }
+  if (cudaError_t e = configure_smem()) return e;
   return cudaSuccess;
 }
 

@@ -297,21 +297,6 @@ struct UidBlob {
 
 static inline bool cyc_geq(uint32_t a, uint32_t b) { return (int32_t)(a - b) >= 0; }
 
-// Host-mapped words of one armed transfer (see armed_launch).  Device writes
-// come from stream memops; the watchdog thread only loads and stores them.
-struct alignas(64) ArmedWords {
-  uint32_t prog;        // primary chunks landed (a memop after each primary chunk)
-  uint32_t go;          // the backup attempt may run: the primary finished, or the watchdog switched
-  uint32_t resume;      // backup chunks below this are skipped (nchunks unless switched)
-  uint32_t probe_go;    // the CTS probe may run: the primary finished, or the watchdog suspects a stall
-  uint32_t probe_done;  // the probe crossed the primary path
-  uint32_t ns;          // no switch (1): the primary writes the done flags itself
-  uint32_t p_fin;       // the primary attempt's copies (stale ones included) all landed
-  uint32_t b_fin;       // the backup attempt drained
-  uint32_t fin;         // the primary passed its done writes (the slot may be reused)
-  uint32_t pad[7];
-};
-
 // ---------------------------------------------------------------- proxy-side structures
 // ENG_CE_GROUP: the rank's two group streams — one for the pushes, one for
 // the pulls of a group (alltoallv, batch_isend_irecv) — see rzv_post.
@@ -1966,24 +1951,24 @@ static iccl_result_t issue_instream(iccl_comm* c, Xfer&& x, int kind, cudaStream
 //   primary, on the issuer's user stream U (in-stream) or the channel's copy
 //   stream (then behind waits on both ready flags):
 //     wait the other side's ready flag; per chunk k: [fault gate, if Down]
-//     copy k, prog := k + 1; then p_fin := 1, probe_go := 1, go := 1;
+//     copy k, prog := k + 1; then p_fin := 1, go := 1;
 //     wait ns (no-switch gate, open); both done flags; fin := 1
 //   backup, on the channel's backup stream B:
-//     wait probe_go; [fault gate, if Down] 16-byte CTS probe over the primary
-//     path; probe_done := 1; wait go; per chunk k: K1 copying chunk k only if
-//     k >= resume (resume = N unless switched), its K4 stamp is the WC;
-//     b_fin := 1
+//     wait go; K9 (iccl_backup_attempt); b_fin := 1
 //
 // No fault: the primary releases both sides itself (one memop wait on an open
-// gate more than a plain in-stream transfer); B's K1 launches find resume = N
-// and return at once.  A stall (both ready flags set, no progress for delta):
-// the watchdog thread opens probe_go; a probe that does not land within delta
-// means the path is dead — the primary is then parked on
-// the same gate, in front of ns — so, with host stores only: ns := 0,
-// resume := completed (the receiver's breakpoint), go := 1, and
-// the stale gate opens: the primary's flushed copies rewrite bytes B
-// delivers.  Once every backup chunk landed and p_fin is set,
-// the watchdog writes both done flags and reopens ns.
+// gate more than a plain in-stream transfer) and opens go with p_fin set, so
+// K9 decides "exit" at once — one near-empty launch.  A stall (both ready
+// flags set, no progress for delta): the watchdog thread sets ctl := probe
+// and opens go; K9 stores a 16-byte CTS over the primary path unless that
+// path's gate is closed.  A probe that does not land within delta means the
+// path is dead — the primary is then parked on the same
+// gate, in front of ns — so, with host stores only: ns := 0, resume :=
+// completed (the receiver's breakpoint), ctl := switch, and the
+// stale gate opens: the primary's flushed copies rewrite bytes K9 delivers
+// (SPEC.md:285).  K9 copies chunks [resume, N) with a K4 stamp per chunk (the
+// WCs); once every one landed and p_fin is set, the watchdog writes both done
+// flags and reopens ns.
 static iccl_result_t backup_stream(iccl_comm* c, Channel& chn, cudaStream_t* out) {
   if (chn.b_si < 0) {
     int lo, hi;
@@ -2085,7 +2070,6 @@ static iccl_result_t armed_launch(iccl_comm* c, Xfer&& x, int kind, cudaStream_t
     if (r) return r;
   }
   p.push_back(wparam(&w->p_fin, 1));
-  p.push_back(wparam(&w->probe_go, 1));
   p.push_back(wparam(&w->go, 1));
   r = batch_memops(ps, p);
   if (r) return r;
@@ -2113,43 +2097,38 @@ static iccl_result_t armed_launch(iccl_comm* c, Xfer&& x, int kind, cudaStream_t
   cudaStream_t bs = nullptr;
   r = backup_stream(c, chn, &bs);
   if (r) return r;
-  r = memop_wait(bs, &w->probe_go, 1);
-  if (r) return r;
-  {
-    std::lock_guard<std::mutex> g(c->fault_mu);
-    if (chn.fault[0].down) {  // the CTS crosses the primary path: a Down path loses it
-      r = memop_wait(bs, &c->gate_words[chn.fault[0].gate], 1);
-      if (r) return r;
-    }
-  }
-  if (chn.dir == 0)
-    ICCL_CHECK_CU(driver()->cuMemcpyDtoDAsync((CUdeviceptr)chn.peer_scratch, (CUdeviceptr)c->scratch, 16, (CUstream)bs));
-  else
-    ICCL_CHECK_CU(driver()->cuMemcpyDtoDAsync((CUdeviceptr)(c->scratch + 2048 + 16 * chn.peer),
-                                              (CUdeviceptr)chn.peer_scratch, 16, (CUstream)bs));
-  r = memop_write(bs, &w->probe_done, 1);
-  if (r) return r;
   r = memop_wait(bs, &w->go, 1);
   if (r) return r;
+  BackupOp b{};
+  b.src = x.src;
+  b.dst = x.dst;
+  b.bytes = x.bytes;
+  b.chunk = x.chunk;
+  b.nchunks = (uint32_t)x.nchunks;
+  b.ring = c->stamps;
+  b.ring_slots = kStampSlots;
+  b.w = w;
   {
     std::lock_guard<std::mutex> g(c->fault_mu);
-    if (chn.fault[1].down) {  // the backup path itself is Down
-      r = memop_wait(bs, &c->gate_words[chn.fault[1].gate], 1);
-      if (r) return r;
-    }
+    b.gate = chn.fault[0].down ? (const uint32_t*)&c->gate_words[chn.fault[0].gate] : nullptr;
   }
+  // the CTS probe (16 B) crosses the primary path in its direction: into the
+  // peer's scratch (push) or out of it (pull)
+  b.probe_src = chn.dir == 0 ? c->scratch : chn.peer_scratch;
+  b.probe_dst = chn.dir == 0 ? chn.peer_scratch : c->scratch + 2048 + 16 * chn.peer;
+  b.error = c->ll_error;
+  b.stamp_base = (uint32_t)(c->next_stamp.fetch_add(x.nchunks) % kStampSlots);
   x.bstamp.assign(x.nchunks, -1);
   for (int k = 0; k < x.nchunks; k++) {
-    const size_t off = (size_t)k * x.chunk, n = std::min(x.chunk, x.bytes - off);
-    const int st = c->next_stamp.fetch_add(1) % kStampSlots;
-    memset((void*)&c->stamps[st], 0, sizeof(KernelStamp));
-    x.bstamp[k] = st;
-    int grid = 0;
-    ICCL_CHECK_CUDA(launch_copy(x.src + off, x.dst + off, n, c->cfg.sm_cap, &c->stamps[st], bs, &grid, &w->resume,
-                                (uint32_t)k));
-    c->kernels_launched += 1;
-    c->ctas_launched += grid;
+    x.bstamp[k] = (int)((b.stamp_base + k) % kStampSlots);
+    memset((void*)&c->stamps[x.bstamp[k]], 0, sizeof(KernelStamp));
   }
+  ICCL_RETURN_IF((((uintptr_t)x.src ^ (uintptr_t)x.dst) & 15) != 0, ICCL_ERR_INVALID_ARGUMENT,
+                 "armed transfer between tensors of different alignment mod 16");
+  int grid = 0;
+  ICCL_CHECK_CUDA(launch_backup(b, c->cfg.sm_cap, bs, &grid));
+  c->kernels_launched += 1;
+  c->ctas_launched += grid;
   r = memop_write(bs, &w->b_fin, 1);
   if (r) return r;
   x.done_enqueued = true;
@@ -2196,8 +2175,8 @@ static void armed_switch(iccl_comm* c, Channel& chn, Xfer& x) {
   }
   __atomic_store_n(&w->ns, 0u, __ATOMIC_SEQ_CST);  // the primary (parked on the gate) must not release the op
   __atomic_store_n(&w->resume, (uint32_t)x.completed, __ATOMIC_SEQ_CST);  // breakpoint = receiver done
+  __atomic_store_n(&w->ctl, (uint32_t)kCtlSwitch, __ATOMIC_SEQ_CST);      // before the stale gate opens
   __atomic_store_n(&w->go, 1u, __ATOMIC_SEQ_CST);
-  __atomic_store_n(&w->probe_go, 1u, __ATOMIC_SEQ_CST);
   if (stale >= 0) release_gate(c, stale);  // the primary drains: its flushed copies rewrite delivered bytes
   x.switched = true;
   x.path = 1;
@@ -2235,6 +2214,16 @@ static bool armed_progress(iccl_comm* c, Channel& chn) {
       if (m > 0) {
         x.t_obs = tnow;
         x.last_progress = tnow;
+        busy = true;
+      }
+    } else if (__atomic_load_n(&w->dec, __ATOMIC_ACQUIRE) == kDecExit) {
+      // K9 saw the primary finish before the switch reached it: the primary
+      // delivered every chunk (its flushed copies included) — complete the op
+      if (__atomic_load_n(&w->p_fin, __ATOMIC_ACQUIRE) && __atomic_load_n(&w->ns, __ATOMIC_ACQUIRE) == 0) {
+        x.completed = x.nchunks;
+        __atomic_store_n(&flags_of(c, x.dst_rank)->done[x.r_done_slot], x.r_done_gen, __ATOMIC_SEQ_CST);
+        __atomic_store_n(&flags_of(c, x.src_rank)->done[x.s_slot], x.s_gen, __ATOMIC_SEQ_CST);
+        __atomic_store_n(&w->ns, 1u, __ATOMIC_SEQ_CST);
         busy = true;
       }
     } else {
@@ -2300,7 +2289,8 @@ static bool armed_progress(iccl_comm* c, Channel& chn) {
     if (elig && x.completed < x.nchunks && tnow - x.last_progress > delta) {
       if (!x.switched) {
         if (!x.probing && !x.probe_ok) {
-          __atomic_store_n(&w->probe_go, 1u, __ATOMIC_SEQ_CST);
+          __atomic_store_n(&w->ctl, (uint32_t)kCtlProbe, __ATOMIC_SEQ_CST);
+          __atomic_store_n(&w->go, 1u, __ATOMIC_SEQ_CST);
           x.probing = true;
           x.probe_t = tnow;
         } else if (x.probing && __atomic_load_n(&w->probe_done, __ATOMIC_ACQUIRE)) {
@@ -3154,8 +3144,8 @@ iccl_result_t iccl_comm_abort(iccl_comm_t c) {
   for (int i = 0; i < kArmedSlots; i++) {  // unpark every armed attempt (the backups copy nothing)
     ArmedWords* w = &c->armed_words[i];
     __atomic_store_n(&w->resume, 0xffffffffu, __ATOMIC_SEQ_CST);
+    __atomic_store_n(&w->ctl, (uint32_t)kCtlAbort, __ATOMIC_SEQ_CST);
     __atomic_store_n(&w->go, 1u, __ATOMIC_SEQ_CST);
-    __atomic_store_n(&w->probe_go, 1u, __ATOMIC_SEQ_CST);
     __atomic_store_n(&w->ns, 1u, __ATOMIC_SEQ_CST);
   }
   // mapped peer memory and the control block stay mapped (leaked): a parked

@@ -51,7 +51,7 @@ for STEP in "$@"; do
     failover) timeout 600 $TR --nproc-per-node $NG --master-port 29677 benchmarks/failover.py >> "$LOG" 2>&1
               [ "$NG" -ge 3 ] && timeout 600 $TR --nproc-per-node $NG --master-port 29678 benchmarks/failover.py --backup relay >> "$LOG" 2>&1 || true ;;
     armedexp) for V in "" "--armed" "--armed ICCL_ARMED_BACKUP=0" "--chunk-bytes 8388608" "--chunk-bytes 8388608 --armed" \
-                    "--chunk-bytes 8388608 --armed ICCL_ARMED_BACKUP=0" "--chunk-bytes 8388608 --monitor"; do
+                    "--chunk-bytes 8388608 --armed ICCL_ARMED_BACKUP=0" "--chunk-bytes 8388608 --records" "--chunk-bytes 33554432" "--chunk-bytes 33554432 --armed" "--chunk-bytes 33554432 --records"; do
                 A=$(echo "$V" | sed 's/ICCL_ARMED_BACKUP=0//'); E=$(echo "$V" | grep -o 'ICCL_ARMED_BACKUP=0')
                 echo "## $V" >> "$LOG"
                 env $E timeout 600 $TR --nproc-per-node 2 --master-port 29681 benchmarks/p2p_sweep.py --impl iccl-auto \

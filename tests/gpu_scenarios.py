@@ -410,14 +410,17 @@ def monitor_accuracy(comm, rank, world, nchunks, chunk, stall_chunk, up_us):
     the sender-side records (t1, t2, bytes)."""
     from paper_2510_00991_b200 import FaultScript
     dev = dev_of(rank)
-    if stall_chunk >= 0:
-        comm.set_faults(FaultScript().down(0, 1, chunk=stall_chunk, op_index=0).up(0, 1, t_us=up_us))
     n = nchunks * chunk
     out = {}
     src = to_dev(payload(n, seed=5), dev) if rank == 0 else None
     dst = torch.empty(n, dtype=torch.uint8, device=dev) if rank == 1 else None
     torch.cuda.synchronize()
     comm.monitor.drain()
+    # the Up is timed from the install: both ranks install together, right
+    # before the op, so the Down (at the chunk's issue) always precedes it
+    _store_barrier(comm, "ac5")
+    if stall_chunk >= 0:
+        comm.set_faults(FaultScript().down(0, 1, chunk=stall_chunk, op_index=0).up(0, 1, t_us=up_us))
     if rank == 0:
         comm.send(src, 1)
     else:

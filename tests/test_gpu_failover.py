@@ -147,7 +147,7 @@ def test_AC5_monitor_accuracy_and_smoothing(torch_cuda, tmp_path):
     cfg["chunk_bytes"] = 16 * MiB
     (tmp_path / "d").mkdir()
     res = run_ranks(2, sc.monitor_accuracy, tmp_path / "d", nchunks=128, chunk=16 * MiB, stall_chunk=64,
-                    up_us=5000, config=cfg)
+                    up_us=20_000, config=cfg)
     t1, t2, b = _recs(res)
     assert len(b) == 128 and bool(res[1]["ok"][0])
     assert int(res[0]["switches"][0]) + int(res[1]["switches"][0]) == 0, (res[0]["switch_desc"], res[1]["switch_desc"])
