@@ -57,7 +57,8 @@ def timed(fn, reps, stream):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
-    ap.add_argument("--only", default="", help="comma list of k1_local,k1_peer,k1_pull,k2,k3")
+    ap.add_argument("--only", default="", help="comma list of k1_local,k1_peer,k1_pull,k2,k3,k8")
+    ap.add_argument("--quick", action="store_true", help="small shapes (compute-sanitizer runs)")
     args = ap.parse_args()
     from paper_2510_00991_b200 import gather_rows, scatter_rows
     from paper_2510_00991_b200._lib import lib
@@ -67,7 +68,7 @@ def main():
     s = torch.cuda.current_stream()
     sh = C.c_void_p(int(s.cuda_stream))
     out = []
-    n = 256 * MiB
+    n = (16 if args.quick else 256) * MiB
     g = torch.Generator(device="cuda").manual_seed(1)
     src = torch.randint(-128, 127, (n,), dtype=torch.int8, device="cuda", generator=g)
 
@@ -113,7 +114,7 @@ def main():
                             "achieved_GBps": round(ach, 1), "peak": 770.0, "bound": "nvlink (measured peer copy)",
                             "frac": round(ach / 770.0, 4), "bit_exact": ok})
         del dst, rsrc
-    T, k, H = 4096, 8, 7168
+    T, k, H = (256 if args.quick else 4096), 8, 7168
     row = H * 2
     rows = T * k
     if not only or "k2" in only or "k3" in only:
@@ -152,6 +153,26 @@ def main():
             out.append({"kernel": "K3 iccl_scatter_rows", "rows": rows, "row_bytes": row, "us": round(t * 1e6, 2),
                         "achieved_GBps": round(alg / t / 1e9, 1), "peak": hbm, "bound": "hbm",
                         "frac": round(alg / t / 1e9 / hbm, 4), "bit_exact": ok})
+    if not only or "k8" in only:
+        # K8 (fused dispatch) on one rank: every routed row stays local, so
+        # the kernel is K2's expand plus K8's handshake words (no peer flags)
+        import paper_2510_00991_b200 as iccl
+        from paper_2510_00991_b200.moe import DispatchPlan, moe_dispatch_fused
+        tok = torch.randint(-32768, 32767, (T, H), dtype=torch.int16, device="cuda", generator=g)
+        order = torch.randperm(rows, device="cuda", generator=g)
+        pos = torch.empty_like(order)
+        pos[order] = torch.arange(rows, device="cuda")
+        comm = iccl.Communicator(0, 1, 0, iccl.IcclConfig.defaults())
+        plan = DispatchPlan(order, torch.div(order, k, rounding_mode="floor"), pos, [rows], [rows])
+        recv = torch.empty(rows, H, dtype=torch.int16, device="cuda")
+        t = timed(lambda: moe_dispatch_fused(comm, tok, plan, recv), args.reps, s)
+        ok = torch.equal(recv, tok[torch.div(order, k, rounding_mode="floor")])
+        comm.destroy()
+        alg = T * row + rows * row + rows * 8
+        out.append({"kernel": "K8 iccl_dispatch_push (1 rank: all rows local)", "rows": rows, "row_bytes": row,
+                    "us": round(t * 1e6, 2), "achieved_GBps": round(alg / t / 1e9, 1), "peak": hbm, "bound": "hbm",
+                    "alg_bytes": "T rows read + T*k rows written + 8 B/row index",
+                    "frac": round(alg / t / 1e9 / hbm, 4), "bit_exact": ok})
     for r in out:
         print(json.dumps(r), flush=True)
 

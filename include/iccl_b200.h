@@ -279,6 +279,17 @@ size_t iccl_selftest_rzv_bytes(void);
 int iccl_selftest_route_small(void* pair, int side);
 void iccl_selftest_route_arm(void* pair, int faults_delta, int active_path);
 int iccl_selftest_rzv_post(void* entry, int kind, uint64_t k, uint64_t bytes, uint64_t* other_bytes);
+/* The armed-transfer failover protocol on host memory:
+ * the watchdog's own pass against a host thread playing the two device
+ * attempts.  scenario 0 no fault; 1 a slow chunk (3 delta) on a live path:
+ * the CTS probe lands, no switch; 2 the primary Down from
+ * `fault_chunk`: probe lost, switch at the receiver's breakpoint, K9 copies
+ * the suffix; 3 both paths Down: ConnectionFailed; 4 an
+ * upstream stall (ready flags late by 3 delta): no probe at all.
+ * out[8] = {watchdog switches, resume chunk or -1, published done, total,
+ * both done flags written, monitor records, probe landed, async error};
+ * returns 0, or 1 if the transfer did not retire within 20 s. */
+int iccl_selftest_failover(int scenario, int nchunks, int fault_chunk, uint64_t delta_us, int64_t* out);
 
 #ifdef __cplusplus
 }

@@ -136,6 +136,7 @@ PROTOTYPES = {
     "iccl_selftest_route_small": (C.c_int, [_p, C.c_int]),
     "iccl_selftest_route_arm": (None, [_p, C.c_int, C.c_int]),
     "iccl_selftest_rzv_post": (C.c_int, [_p, C.c_int, _u64, _u64, C.POINTER(_u64)]),
+    "iccl_selftest_failover": (C.c_int, [C.c_int, C.c_int, C.c_int, _u64, C.POINTER(_i64)]),
 }
 
 

@@ -100,6 +100,7 @@ struct BackupOp {
   KernelStamp* ring;
   ArmedWords* w;
   const uint32_t* gate;    // the primary path's fault gate word when the transfer was issued behind it, or null
+  const uint32_t* bgate;   // the backup path's fault gate word (a Down backup path), or null
   const char* probe_src;   // 16 bytes moved by the probe (over the primary path's direction)
   char* probe_dst;
   unsigned int* error;     // host-mapped: set if the decision wait exceeds 60 s

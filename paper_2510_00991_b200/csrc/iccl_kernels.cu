@@ -225,6 +225,11 @@ __global__ void __launch_bounds__(kCopyThreads) iccl_backup_attempt(const __grid
         }
       }
     }
+    if (dec == kDecCopy && op.bgate) {  // the backup path itself is Down: wait for it (or the abort)
+      while (ld_sys(op.bgate) == 0 && ld_sys(&w->ctl) != kCtlAbort) {
+      }
+      if (ld_sys(&w->ctl) == kCtlAbort) dec = kDecExit;
+    }
     s_dec = dec;
   }
   __syncthreads();

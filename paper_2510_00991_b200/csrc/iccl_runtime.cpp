@@ -2111,6 +2111,7 @@ static iccl_result_t armed_launch(iccl_comm* c, Xfer&& x, int kind, cudaStream_t
   {
     std::lock_guard<std::mutex> g(c->fault_mu);
     b.gate = chn.fault[0].down ? (const uint32_t*)&c->gate_words[chn.fault[0].gate] : nullptr;
+    b.bgate = chn.fault[1].down ? (const uint32_t*)&c->gate_words[chn.fault[1].gate] : nullptr;
   }
   // the CTS probe (16 B) crosses the primary path in its direction: into the
   // peer's scratch (push) or out of it (pull)
@@ -3689,6 +3690,167 @@ int iccl_selftest_rzv_post(void* entry, int kind, uint64_t k, uint64_t bytes, ui
   if (!rzv_arrive(e, k, snap)) return 0;
   if (other_bytes) *other_bytes = snap[(kind & 1) ^ 1].bytes;
   return snap[0].gen == snap[1].gen ? 1 : -1;  // both halves belong to op k
+}
+
+// CPU self-test of the armed-transfer failover protocol (see the header):
+// the watchdog's own pass (armed_progress) drives one transfer of a
+// communicator whose control block lives in plain host memory, while a host
+// thread plays the device — the primary attempt's stream (gate waits,
+// chunk copies, prog / p_fin / go / ns / done / fin words) and K9's
+// controller (decision, CTS probe, suffix copy with one K4 stamp per chunk).
+int iccl_selftest_failover(int scenario, int nchunks, int fault_chunk, uint64_t delta_us, int64_t* out) {
+  if (nchunks < 1 || nchunks > 256 || !out) return -1;
+  iccl_comm* c = new iccl_comm();
+  c->rank = 0;
+  c->nranks = 2;
+  c->cfg.delta_us = delta_us;
+  c->cfg.probe_period_us = std::max<uint64_t>(1, delta_us / 2);
+  c->cfg.chunk_bytes = 1 << 20;
+  c->monitor_enabled = 1;
+  c->flags = (RankFlags*)calloc(2, sizeof(RankFlags));
+  c->rings = (RzvRing*)calloc(4, sizeof(RzvRing));
+  c->armed_words = (ArmedWords*)calloc(kArmedSlots, sizeof(ArmedWords));
+  c->stamps = (KernelStamp*)calloc(kStampSlots, sizeof(KernelStamp));
+  c->gate_words = (volatile uint32_t*)calloc(kGateWords, 4);
+  c->gate_closed.assign(kGateWords, 0);
+  c->armed_used.assign(kArmedSlots, 0);
+  c->ch.resize(4);
+  for (int p = 0; p < 2; p++)
+    for (int d = 0; d < 2; d++) {
+      Channel& h = c->ch[2 * p + d];
+      h.peer = p;
+      h.dir = d;
+      h.src = d == 0 ? 0 : p;
+      h.dst = d == 0 ? p : 0;
+    }
+  Channel& chn = c->ch[2];  // pushes 0 -> 1
+  ArmedWords* w = &c->armed_words[0];
+  w->resume = (uint32_t)nchunks;
+  w->ns = 1;
+  const bool dead = scenario == 2 || scenario == 3;
+  if (dead) {  // chunk-triggered Down of the primary (fired at issue, like fire_chunk_faults)
+    chn.fault[0].down = true;
+    chn.fault[0].gate = alloc_gate(c);
+    chn.fault[0].down_at = now_ns();
+  }
+  if (scenario == 3) {  // the backup path is Down as well
+    chn.fault[1].down = true;
+    chn.fault[1].gate = alloc_gate(c);
+    chn.fault[1].down_at = now_ns();
+  }
+  volatile uint32_t* pgate = dead ? &c->gate_words[chn.fault[0].gate] : nullptr;
+  volatile uint32_t* bgate = scenario == 3 ? &c->gate_words[chn.fault[1].gate] : nullptr;
+  Xfer x;
+  x.armed = true;
+  x.aw = 0;
+  x.src_rank = 0;
+  x.dst_rank = 1;
+  x.chan = 2;
+  x.s_slot = x.r_ready_slot = x.r_done_slot = 0;
+  x.s_gen = x.r_ready_gen = x.r_done_gen = 1;
+  x.nchunks = nchunks;
+  x.chunk = 1 << 20;
+  x.bytes = (size_t)nchunks << 20;
+  x.next_issue = nchunks;
+  x.rec.resize(nchunks);
+  x.bstamp.resize(nchunks);
+  for (int k = 0; k < nchunks; k++) x.bstamp[k] = k;
+  x.last_progress = x.t_obs = now_ns();
+  c->armed_used[0] = 1;
+  c->pending_xfers = 1;
+  chn.armed.push_back(std::move(x));
+  const uint64_t delta = delta_us * 1000ull;
+  std::atomic<bool> quit{false};
+  auto ld = [](volatile uint32_t* p) { return __atomic_load_n((uint32_t*)p, __ATOMIC_ACQUIRE); };
+  auto st = [](volatile uint32_t* p, uint32_t v) { __atomic_store_n((uint32_t*)p, v, __ATOMIC_SEQ_CST); };
+  auto nap = [] { std::this_thread::sleep_for(std::chrono::microseconds(20)); };
+  // the primary attempt's stream
+  std::thread primary([&] {
+    if (scenario == 4) std::this_thread::sleep_for(std::chrono::nanoseconds(3 * delta));  // upstream stall
+    st(&c->flags[0].ready[0], 1);
+    st(&c->flags[1].ready[0], 1);
+    for (int k = 0; k < nchunks && !quit; k++) {
+      if (dead && k == fault_chunk)
+        while (ld(pgate) == 0 && !quit) nap();
+      if (scenario == 1 && k == fault_chunk) std::this_thread::sleep_for(std::chrono::nanoseconds(3 * delta));
+      std::this_thread::sleep_for(std::chrono::microseconds(30));  // the chunk's copy
+      st(&w->prog, (uint32_t)(k + 1));
+    }
+    st(&w->p_fin, 1);
+    st(&w->go, 1);
+    while (ld(&w->ns) == 0 && !quit) nap();
+    st(&c->flags[1].done[0], 1);
+    st(&c->flags[0].done[0], 1);
+    st(&w->fin, 1);
+  });
+  // K9 on the backup stream
+  std::thread backup([&] {
+    while (ld(&w->go) == 0 && !quit) nap();
+    uint32_t dec = kDecNone;
+    bool probed = false;
+    while (dec == kDecNone && !quit) {
+      const uint32_t ctl = ld(&w->ctl);
+      if (ctl == kCtlSwitch) dec = kDecCopy;
+      else if (ctl == kCtlAbort) dec = kDecExit;
+      else if (ld(&w->p_fin)) dec = ld(&w->ctl) == kCtlSwitch ? kDecCopy : kDecExit;
+      else if (ctl == kCtlProbe && !probed && (!pgate || ld(pgate) != 0)) {
+        st(&w->probe_done, 1);
+        probed = true;
+      } else {
+        nap();
+      }
+    }
+    st(&w->dec, dec);
+    if (dec == kDecCopy) {
+      while (bgate && ld(bgate) == 0 && ld(&w->ctl) != kCtlAbort && !quit) nap();
+      if (!bgate || ld(bgate) != 0)
+        for (uint32_t k = ld(&w->resume); k < (uint32_t)nchunks; k++) {
+          const unsigned long long t1 = now_ns();
+          std::this_thread::sleep_for(std::chrono::microseconds(40));
+          __atomic_store_n(&c->stamps[k].t1, t1, __ATOMIC_RELEASE);
+          __atomic_store_n(&c->stamps[k].t2, (unsigned long long)now_ns(), __ATOMIC_RELEASE);
+        }
+    }
+    st(&w->b_fin, 1);
+  });
+  // the watchdog thread's pass, until the transfer retires (or fails)
+  const uint64_t t0 = now_ns();
+  int rc = 0;
+  while (!chn.armed.empty()) {
+    armed_progress(c, chn);
+    if (c->async_err.load() != ICCL_SUCCESS) break;
+    if (now_ns() - t0 > 20ull * 1000000000ull) {
+      rc = 1;  // timed out
+      break;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(5));
+  }
+  int switched = 0;
+  for (auto& e : c->sw_events) switched += e.to_path == 1 && e.trigger == 1;
+  out[0] = switched;
+  out[1] = switched ? (int64_t)ld(&w->resume) : -1;
+  out[2] = c->flags[0].pub[0].done;
+  out[3] = c->flags[0].pub[0].total;
+  out[4] = ld(&c->flags[0].done[0]) == 1 && ld(&c->flags[1].done[0]) == 1;
+  out[5] = (int64_t)c->mon.size();
+  out[6] = ld(&w->probe_done);
+  out[7] = c->async_err.load();
+  // release whatever is still parked (both paths dead), then tear down
+  quit = true;
+  st(&w->ctl, kCtlAbort);
+  st(&w->ns, 1);
+  st(&w->go, 1);
+  for (int g = 0; g < kGateWords; g++) st(&c->gate_words[g], 1);
+  primary.join();
+  backup.join();
+  free(c->flags);
+  free(c->rings);
+  free(c->armed_words);
+  free(c->stamps);
+  free((void*)c->gate_words);
+  c->flags = nullptr;
+  delete c;
+  return rc;
 }
 
 iccl_result_t iccl_monitor_read(iccl_comm_t c, iccl_mon_rec_t* recs, int max, int* n) {

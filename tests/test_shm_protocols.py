@@ -126,3 +126,51 @@ def test_route_segments_start_after_both_sides():
     lib.iccl_selftest_route_arm(pair, -1, -1)                                     # disarmed at 6
     assert lib.iccl_selftest_route_small(pair, 0) == 0
     assert lib.iccl_selftest_route_small(pair, 1) == 0
+
+
+# ---------------------------------------------------------------- failover protocol (armed transfers)
+def _failover(scenario, nchunks=12, fault_chunk=5, delta_us=2000):
+    out = (C.c_int64 * 8)()
+    rc = lib.iccl_selftest_failover(scenario, nchunks, fault_chunk, delta_us, out)
+    keys = ("switches", "resume", "done", "total", "done_flags", "records", "probe", "async_err")
+    return rc, dict(zip(keys, list(out)))
+
+
+def test_failover_protocol_no_fault():
+    rc, o = _failover(0)
+    assert rc == 0 and o["switches"] == 0 and o["probe"] == 0 and o["async_err"] == 0
+    assert o["done"] == o["total"] == 12 and o["done_flags"] == 1
+    assert o["records"] == 12  # one record per chunk
+
+
+def test_failover_protocol_slow_chunk_probe_lands_no_switch():
+    """Fig. 7(b) innocent variant: no progress for > delta on a live path; the
+    CTS probe crosses it, so the watchdog does not switch."""
+    rc, o = _failover(1)
+    assert rc == 0 and o["probe"] == 1 and o["switches"] == 0
+    assert o["done"] == 12 and o["done_flags"] == 1
+
+
+@pytest.mark.parametrize("fault_chunk", [0, 1, 5, 11])
+def test_failover_protocol_dead_primary_switches_at_breakpoint(fault_chunk):
+    """The primary Down from `fault_chunk`: the probe is lost, the watchdog
+    switches with resume = the receiver's breakpoint, the
+    backup attempt delivers chunks [resume, N), and the op completes exactly
+    once: one record per chunk, both done flags written by the watchdog."""
+    rc, o = _failover(2, fault_chunk=fault_chunk)
+    assert rc == 0 and o["switches"] == 1 and o["async_err"] == 0
+    assert o["resume"] == fault_chunk
+    assert o["done"] == o["total"] == 12 and o["done_flags"] == 1
+    assert o["records"] == 12
+
+
+def test_failover_protocol_both_paths_dead_connection_failed():
+    rc, o = _failover(3, fault_chunk=4)
+    assert o["switches"] == 1 and o["async_err"] == 7  # ICCL_ERR_CONNECTION_FAILED (SPEC.md:295)
+
+
+def test_failover_protocol_upstream_stall_never_probes():
+    """A side's stream reaches the op late (ready flags set after 3 delta):
+    an upstream stall, not a path failure — no probe, no switch."""
+    rc, o = _failover(4)
+    assert rc == 0 and o["probe"] == 0 and o["switches"] == 0 and o["done_flags"] == 1
