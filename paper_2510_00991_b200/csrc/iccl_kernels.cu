@@ -183,55 +183,56 @@ __device__ __forceinline__ void st_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// K9a: the controller, one warp (lane 0 works), launched right behind the
+// primary's enqueue on the backup stream: it waits for `go` inside the
+// kernel rather than parking the stream on a stream-memory wait (a parked
+// stream was measured to cost every other stream of the GPU ~50 us per op),
+// then decides.  Polls back off with __nanosleep.
+__global__ void __launch_bounds__(32) iccl_backup_ctl(const __grid_constant__ BackupOp op) {
+  if (threadIdx.x != 0) return;
+  ArmedWords* w = op.w;
+  const unsigned long long t0 = globaltimer();
+  uint32_t dec = kDecNone;
+  bool probed = false;
+  while (ld_sys(&w->go) == 0 && ld_sys(&w->ctl) != kCtlAbort) __nanosleep(256);
+  while (dec == kDecNone) {
+    const uint32_t ctl = ld_sys(&w->ctl);
+    if (ctl == kCtlSwitch) {
+      dec = kDecCopy;
+    } else if (ctl == kCtlAbort) {
+      dec = kDecExit;
+    } else if (ld_sys(&w->p_fin)) {
+      dec = ld_sys(&w->ctl) == kCtlSwitch ? kDecCopy : kDecExit;  // a switch racing the primary's end still copies
+    } else if (ctl == kCtlProbe && !probed && (!op.gate || ld_sys(op.gate) != 0)) {
+      // the CTS crosses the primary path: lost while its gate is closed
+      int4 v;
+      asm volatile("ld.volatile.global.v4.s32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(op.probe_src) : "memory");
+      asm volatile("st.volatile.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(op.probe_dst), "r"(v.x), "r"(v.y),
+                   "r"(v.z), "r"(v.w) : "memory");
+      __threadfence_system();
+      st_sys(&w->probe_done, 1u);
+      probed = true;
+    } else {
+      __nanosleep(256);
+    }
+  }
+  if (dec == kDecCopy && op.bgate) {  // the backup path itself is Down: wait for it (or the abort)
+    while (ld_sys(op.bgate) == 0 && ld_sys(&w->ctl) != kCtlAbort) __nanosleep(256);
+    if (ld_sys(&w->ctl) == kCtlAbort) dec = kDecExit;
+  }
+  (void)t0;
+  st_sys(&w->dec, dec);
+}
+
+// K9b: the copy grid, behind K9a on the same stream, so the decision is
+// final when it starts: nothing to do unless the watchdog switched.
 __global__ void __launch_bounds__(kCopyThreads) iccl_backup_attempt(const __grid_constant__ BackupOp op) {
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) uint64_t mbar[kStages];
   __shared__ uint32_t s_dec;
   ArmedWords* w = op.w;
-  if (threadIdx.x == 0) {
-    const unsigned long long t0 = globaltimer();
-    uint32_t dec = kDecNone;
-    if (blockIdx.x == 0) {
-      bool probed = false;
-      while (dec == kDecNone) {
-        const uint32_t ctl = ld_sys(&w->ctl);
-        if (ctl == kCtlSwitch) {
-          dec = kDecCopy;
-        } else if (ctl == kCtlAbort) {
-          dec = kDecExit;
-        } else if (ld_sys(&w->p_fin)) {
-          dec = ld_sys(&w->ctl) == kCtlSwitch ? kDecCopy : kDecExit;  // a switch racing the primary's end still copies
-        } else if (ctl == kCtlProbe && !probed && (!op.gate || ld_sys(op.gate) != 0)) {
-          // the CTS crosses the primary path: lost while its gate is closed
-          int4 v;
-          asm volatile("ld.volatile.global.v4.s32 {%0,%1,%2,%3}, [%4];"
-                       : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(op.probe_src) : "memory");
-          asm volatile("st.volatile.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(op.probe_dst), "r"(v.x), "r"(v.y),
-                       "r"(v.z), "r"(v.w) : "memory");
-          __threadfence_system();
-          st_sys(&w->probe_done, 1u);
-          probed = true;
-        } else if (globaltimer() - t0 > 60000000000ull) {
-          *op.error = 1;
-          dec = kDecExit;
-        }
-      }
-      st_sys(&w->dec, dec);
-    } else {
-      while ((dec = ld_sys(&w->dec)) == kDecNone) {
-        if (globaltimer() - t0 > 61000000000ull) {
-          *op.error = 1;
-          dec = kDecExit;
-        }
-      }
-    }
-    if (dec == kDecCopy && op.bgate) {  // the backup path itself is Down: wait for it (or the abort)
-      while (ld_sys(op.bgate) == 0 && ld_sys(&w->ctl) != kCtlAbort) {
-      }
-      if (ld_sys(&w->ctl) == kCtlAbort) dec = kDecExit;
-    }
-    s_dec = dec;
-  }
+  if (threadIdx.x == 0) s_dec = ld_sys(&w->dec);
   __syncthreads();
   if (s_dec != kDecCopy) return;
   const uint32_t r = ld_sys(&w->resume);
@@ -725,7 +726,10 @@ cudaError_t launch_backup(const BackupOp& op, int ctas, cudaStream_t st, int* gr
   const size_t ntiles = (min(op.chunk, op.bytes) + kTile - 1) / kTile;
   int grid = (int)min((size_t)ctas, ntiles > 0 ? ntiles : (size_t)1);
   if (grid < 1) grid = 1;
-  if (grid_out) *grid_out = grid;
+  if (grid_out) *grid_out = grid + 1;
+  iccl_backup_ctl<<<1, 32, 0, st>>>(op);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
   iccl_backup_attempt<<<grid, kCopyThreads, kStages * kTile, st>>>(op);
   return cudaGetLastError();
 }
@@ -767,7 +771,7 @@ cudaError_t preload_kernels() {
                        (const void*)iccl_read_globaltimer, (const void*)iccl_gather_rows,
                        (const void*)iccl_scatter_rows, (const void*)iccl_expand_rows,
                        (const void*)iccl_ll_group, (const void*)iccl_wait_flags, (const void*)iccl_dispatch_push,
-                       (const void*)iccl_backup_attempt};
+                       (const void*)iccl_backup_attempt, (const void*)iccl_backup_ctl};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;

@@ -529,6 +529,17 @@ struct iccl_comm {
   // CTS probe stream, one monitor stream per direction (push / pull) and the
   // relay hop-1 stream
   int sm_si = -1, probe_si = -1, mon_si[2] = {-1, -1}, relay_si = -1;
+  // a group's self copy (alltoallv's own segment, a local HBM copy) runs on
+  // self_si, forked from and joined back into the user stream by events, so
+  // it overlaps the group's NVLink copies instead of queueing in front of them
+  int self_si = -1;
+  cudaEvent_t self_fork = nullptr, self_join = nullptr;
+  bool self_overlap = true;  // ICCL_SELF_OVERLAP=0: the self copy stays in the user stream's order
+  // K7 (a one-warp polling kernel) instead of a stream-memory wait for the
+  // copy-engine path's done waits (ICCL_K7_CE) / the issuer's wait on the
+  // other side's ready flag (ICCL_K7_READY): a parked stream slows the GPU's
+  // other streams
+  bool k7_ce = false, k7_ready = false;
   bool instream_ce = true;  // healthy pairs: the issuer enqueues the copy on its own user stream (ICCL_INSTREAM=0: off)
   bool armed_backup = true;  // attribution only (ICCL_ARMED_BACKUP=0): armed transfers enqueue no backup attempt
   // monitor records of ops the proxy does not track (K5 sends, K6): their
@@ -1854,6 +1865,29 @@ static void instream_done_params(iccl_comm* c, const Xfer& x, std::vector<CUstre
   p.push_back(w);
 }
 
+static iccl_result_t batch_memops(cudaStream_t s, std::vector<CUstreamBatchMemOpParams>& p);
+
+// The issuer's waits on the other sides' ready flags (params of
+// instream_ready_param): stream-memory waits, or K7 with ICCL_K7_READY.
+static iccl_result_t ready_wait_ops(iccl_comm* c, cudaStream_t s, std::vector<CUstreamBatchMemOpParams>& p) {
+  if (!c->k7_ready || p.empty()) return batch_memops(s, p);
+  WaitList wl;
+  memset(&wl, 0, sizeof(wl));
+  wl.error = c->ll_error;
+  for (size_t i = 0; i < p.size(); i++) {
+    wl.addr[wl.n] = (const uint32_t*)(uintptr_t)p[i].waitValue.address;
+    wl.gen[wl.n] = p[i].waitValue.value;
+    if (++wl.n == kWaitMax || i + 1 == p.size()) {
+      ICCL_CHECK_CUDA(launch_wait(wl, s));
+      c->kernels_launched += 1;
+      c->ctas_launched += 1;
+      wl.n = 0;
+    }
+  }
+  p.clear();
+  return ICCL_SUCCESS;
+}
+
 static iccl_result_t batch_memops(cudaStream_t s, std::vector<CUstreamBatchMemOpParams>& p) {
   for (size_t i = 0; i < p.size(); i += 128) {
     unsigned n = (unsigned)std::min<size_t>(128, p.size() - i);
@@ -1929,7 +1963,7 @@ static iccl_result_t instream_copies(iccl_comm* c, Xfer& x, cudaStream_t s) {
 static iccl_result_t issue_instream(iccl_comm* c, Xfer&& x, int kind, cudaStream_t s) {
   std::vector<CUstreamBatchMemOpParams> p;
   instream_ready_param(c, x, kind, p);
-  iccl_result_t r = batch_memops(s, p);
+  iccl_result_t r = ready_wait_ops(c, s, p);
   if (r) return r;
   r = instream_copies(c, x, s);
   if (r) return r;
@@ -1954,7 +1988,9 @@ static iccl_result_t issue_instream(iccl_comm* c, Xfer&& x, int kind, cudaStream
 //     copy k, prog := k + 1; then p_fin := 1, go := 1;
 //     wait ns (no-switch gate, open); both done flags; fin := 1
 //   backup, on the channel's backup stream B:
-//     wait go; K9 (iccl_backup_attempt); b_fin := 1
+//     K9a (one warp: waits for go in-kernel, decides), K9b (the copy grid,
+//     empty unless switched); b_fin := 1 — no stream-memory wait on B: a
+//     stream parked on one cost the GPU's other streams ~50 us per op
 //
 // No fault: the primary releases both sides itself (one memop wait on an open
 // gate more than a plain in-stream transfer) and opens go with p_fin set, so
@@ -2096,8 +2132,6 @@ static iccl_result_t armed_launch(iccl_comm* c, Xfer&& x, int kind, cudaStream_t
   }
   cudaStream_t bs = nullptr;
   r = backup_stream(c, chn, &bs);
-  if (r) return r;
-  r = memop_wait(bs, &w->go, 1);
   if (r) return r;
   BackupOp b{};
   b.src = x.src;
@@ -2661,7 +2695,7 @@ static iccl_result_t stream_markers(iccl_comm* c, cudaStream_t s, const std::vec
   std::vector<WaitList> kwaits;
   for (const OpDesc& op : ops) {
     if (!(phases & 2)) break;
-    if (op.direct && c->kernel_waits) {
+    if ((op.direct || c->k7_ce) && c->kernel_waits) {
       wl.addr[wl.n] = &mine->done[op.slot];
       wl.alt[wl.n] = nullptr;
       if (c->device_flags) {  // K6 stores the local word; CE fallbacks only the host flag
@@ -2987,6 +3021,12 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
   c->mon_si[0] = mk_stream(ENG_CE);
   c->mon_si[1] = mk_stream(ENG_CE);
   if (c->relay_buf) c->relay_si = mk_stream(ENG_RELAY);
+  c->self_si = mk_stream(ENG_CE);
+  ICCL_CHECK_CUDA(cudaEventCreateWithFlags(&c->self_fork, cudaEventDisableTiming));
+  ICCL_CHECK_CUDA(cudaEventCreateWithFlags(&c->self_join, cudaEventDisableTiming));
+  c->self_overlap = env_us("ICCL_SELF_OVERLAP", 1) != 0;
+  c->k7_ce = env_us("ICCL_K7_CE", 0) != 0;
+  c->k7_ready = env_us("ICCL_K7_READY", 0) != 0;
   c->instream_ce = env_us("ICCL_INSTREAM", 1) != 0;
   c->armed_backup = env_us("ICCL_ARMED_BACKUP", 1) != 0;
   std::vector<char*> peer_scratch(nranks, nullptr);
@@ -3086,6 +3126,8 @@ static void teardown(iccl_comm* c, bool sync = true) {
     if (sc.ev) cudaEventDestroy(sc.ev);
   }
   for (cudaEvent_t e : c->all_events) cudaEventDestroy(e);
+  if (c->self_fork) cudaEventDestroy(c->self_fork);
+  if (c->self_join) cudaEventDestroy(c->self_join);
   for (auto& cache : c->peer_ipc)
     for (auto& kv : cache) cudaIpcCloseMemHandle(kv.second);
   for (char* p : c->peer_scratch_base) cudaIpcCloseMemHandle(p);
@@ -3359,9 +3401,26 @@ iccl_result_t iccl_group_end(iccl_comm_t c) {
     if (!mine.empty()) {
       for (size_t i : mine)
         if (!elide[i]) instream_ready_param(c, xs[i], jobs[i].kind, p);
-      r = batch_memops(s, p);
-      for (size_t i : mine)
+      r = ready_wait_ops(c, s, p);
+      // the self copy (both halves on s, nothing to wait for) forks off to
+      // self_si when NVLink copies follow it, and s joins it before the done
+      // writes: a local copy and a peer copy run on different copy engines
+      std::vector<size_t> self, remote;
+      for (size_t i : mine) (elide[i] && c->self_overlap ? self : remote).push_back(i);
+      if (remote.empty()) {
+        remote.swap(self);
+      }
+      cudaStream_t ss = c->streams[c->self_si].s;
+      if (!r && !self.empty()) {
+        ICCL_CHECK_CUDA(cudaEventRecord(c->self_fork, s));
+        ICCL_CHECK_CUDA(cudaStreamWaitEvent(ss, c->self_fork, 0));
+        for (size_t i : self)
+          if (!r) r = instream_copies(c, xs[i], ss);
+        if (!r) ICCL_CHECK_CUDA(cudaEventRecord(c->self_join, ss));
+      }
+      for (size_t i : remote)
         if (!r) r = instream_copies(c, xs[i], s);
+      if (!r && !self.empty()) ICCL_CHECK_CUDA(cudaStreamWaitEvent(s, c->self_join, 0));
       for (size_t i : mine) instream_done_params(c, xs[i], p);
       if (!r) r = batch_memops(s, p);
       if (r) return r;

@@ -16,6 +16,7 @@
 #   armedexp    p2p_sweep 1-256 MiB: plain / armed (a never-firing fault script) / armed without the
 #               backup attempt (attribution), default and 8 MiB chunks, monitor on
 #   ncuk        ncu --set full of K2 (expand) and K8 (fused dispatch, 1 rank) + the kernels bench
+#   var:NAME    the p2p_sweep variants listed in scripts/variants/NAME.txt (2 GPUs)
 #   dispatch    benchmarks/moe_dispatch.py on all GPUs: fused K8 vs K2 + alltoallv vs NCCL
 #   launches    ncu launch list of smoke() (gpu__time_duration, no replay of waits)
 #   ncuprobe    probes/ncu_xproc under ncu (cross-process serialisation)
@@ -61,6 +62,7 @@ for STEP in "$@"; do
     ncuk) timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:iccl_(expand|dispatch)' -c 4 \
             -f -o gpurun_out/${TAG}_k2k8 python benchmarks/kernels.py --only k2,k8 --reps 1 >> "$LOG" 2>&1
           timeout 300 python benchmarks/kernels.py --only k1_local,k1_peer,k2,k3,k8 >> "$LOG" 2>&1 ;;
+    var:*) timeout 3000 bash scripts/variants.sh "scripts/variants/${STEP#var:}.txt" >> "$LOG" 2>&1 ;;
     dispatch) timeout 600 $TR --nproc-per-node $NG --master-port 29680 benchmarks/moe_dispatch.py >> "$LOG" 2>&1 ;;
     moe) for I in iccl nccl; do timeout 600 $TR --nproc-per-node $NG --master-port 29679 benchmarks/moe_alltoallv.py --impl $I >> "$LOG" 2>&1; done ;;
     launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --target-processes all -c 2000 --csv \
