@@ -724,12 +724,12 @@ cudaError_t launch_backup(const BackupOp& op, int ctas, cudaStream_t st, int* gr
     return cudaErrorInvalidValue;
   if (cudaError_t e = configure_smem()) return e;
   const size_t ntiles = (min(op.chunk, op.bytes) + kTile - 1) / kTile;
-  int grid = (int)min((size_t)ctas, ntiles > 0 ? ntiles : (size_t)1);
+  int grid = (int)min((size_t)max(ctas, 1), ntiles > 0 ? ntiles : (size_t)1);
   if (grid < 1) grid = 1;
   if (grid_out) *grid_out = grid + 1;
   iccl_backup_ctl<<<1, 32, 0, st>>>(op);
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess || ctas == 0) return e;  // ctas 0: the controller alone (attribution runs)
   iccl_backup_attempt<<<grid, kCopyThreads, kStages * kTile, st>>>(op);
   return cudaGetLastError();
 }

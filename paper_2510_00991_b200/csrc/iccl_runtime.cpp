@@ -542,6 +542,7 @@ struct iccl_comm {
   bool k7_ce = false, k7_ready = false;
   bool instream_ce = true;  // healthy pairs: the issuer enqueues the copy on its own user stream (ICCL_INSTREAM=0: off)
   bool armed_backup = true;  // attribution only (ICCL_ARMED_BACKUP=0): armed transfers enqueue no backup attempt
+  int k9_mode = 0;           // attribution only (ICCL_K9_MODE): 1 = K9a alone, 2 = b_fin memop alone
   // monitor records of ops the proxy does not track (K5 sends, K6): their
   // %globaltimer stamps (K4), turned into records once t2 lands
   struct KRec {
@@ -2161,7 +2162,8 @@ static iccl_result_t armed_launch(iccl_comm* c, Xfer&& x, int kind, cudaStream_t
   ICCL_RETURN_IF((((uintptr_t)x.src ^ (uintptr_t)x.dst) & 15) != 0, ICCL_ERR_INVALID_ARGUMENT,
                  "armed transfer between tensors of different alignment mod 16");
   int grid = 0;
-  ICCL_CHECK_CUDA(launch_backup(b, c->cfg.sm_cap, bs, &grid));
+  if (c->k9_mode == 0) ICCL_CHECK_CUDA(launch_backup(b, c->cfg.sm_cap, bs, &grid));
+  if (c->k9_mode == 1) ICCL_CHECK_CUDA(launch_backup(b, 0, bs, &grid));  // K9a only
   c->kernels_launched += 1;
   c->ctas_launched += grid;
   r = memop_write(bs, &w->b_fin, 1);
@@ -2380,6 +2382,10 @@ static void watch_loop(iccl_comm* c) {
     }
     for (Xfer& x : batch) c->ch[x.chan].armed.push_back(std::move(x));
     batch.clear();
+    // time-triggered faults fire here too: the proxy thread may sit in a CUDA
+    // call that a user thread's synchronous call behind the faulted op blocks
+    // (host stores only; fire_time_faults is idempotent under fault_mu)
+    fire_time_faults(c);
     bool any = false, busy = false;
     for (Channel& chn : c->ch) {
       if (chn.armed.empty() && !chn.armed_failed_over) continue;
@@ -3029,6 +3035,7 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
   c->k7_ready = env_us("ICCL_K7_READY", 0) != 0;
   c->instream_ce = env_us("ICCL_INSTREAM", 1) != 0;
   c->armed_backup = env_us("ICCL_ARMED_BACKUP", 1) != 0;
+  c->k9_mode = (int)env_us("ICCL_K9_MODE", 0);
   std::vector<char*> peer_scratch(nranks, nullptr);
   for (int p = 0; p < nranks; p++) {
     if (p == rank) {
