@@ -437,6 +437,7 @@ struct Channel {
   int relay_rank = -1;  // relay GPU of the backup path: lowest rank not an endpoint (topology.py:140-151 tie-break)
   // armed transfers (owned by the watchdog thread)
   int b_si = -1;                   // the channel's backup-attempt stream, created on first use
+  int p_si = -1;                   // the channel's progress-word stream (armed primaries), created on first use
   std::deque<Xfer> armed;
   bool armed_failed_over = false;  // the watchdog moved the pair to its backup path
   uint64_t armed_last_probe = 0;
@@ -543,6 +544,7 @@ struct iccl_comm {
   bool instream_ce = true;  // healthy pairs: the issuer enqueues the copy on its own user stream (ICCL_INSTREAM=0: off)
   bool armed_backup = true;  // attribution only (ICCL_ARMED_BACKUP=0): armed transfers enqueue no backup attempt
   int k9_mode = 0;           // attribution only (ICCL_K9_MODE): 1 = K9a alone, 2 = b_fin memop alone
+  bool prog_events = true;   // armed primaries' progress words from a side stream (ICCL_PROG_EVENTS=0: in-stream memops)
   // monitor records of ops the proxy does not track (K5 sends, K6): their
   // %globaltimer stamps (K4), turned into records once t2 lands
   struct KRec {
@@ -1011,6 +1013,7 @@ static int stream_for(iccl_comm* c, Channel& chn, int path, int engine, int k) {
 }
 
 static void fault_up(iccl_comm* c, FaultState& fs) {
+  ICCL_TRACE("gate %d opens", fs.gate);
   fs.down = false;
   release_gate(c, fs.gate);
   fs.gate = -1;
@@ -1037,6 +1040,8 @@ static void fire_time_faults(iccl_comm* c) {
     if (f.f.src != c->rank && f.f.dst != c->rank) continue;
     if (t - c->faults_t0 < f.f.t_us * 1000ull) continue;
     f.fired = true;
+    ICCL_TRACE("time fault %s path %d of %d->%d fires at +%.1f us", f.f.up ? "Up" : "Down", f.f.path, f.f.src, f.f.dst,
+               (t - c->faults_t0) * 1e-3);
     for (Channel& chn : c->ch)
       if (chn.src == f.f.src && chn.dst == f.f.dst) apply_fault(c, chn.fault[f.f.path & 1], f.f.up, t);
   }
@@ -1050,6 +1055,8 @@ static void fire_chunk_faults(iccl_comm* c, Channel& chn, int op_index, int chun
     if (f.fired || f.f.trigger_kind != 1 || f.f.src != chn.src || f.f.dst != chn.dst) continue;
     if (f.f.op_index != op_index || f.f.chunk != chunk || (f.f.path & 1) != path) continue;
     f.fired = true;
+    ICCL_TRACE("chunk fault %s path %d of %d->%d fires at chunk %d (+%.1f us)", f.f.up ? "Up" : "Down", path, chn.src,
+               chn.dst, chunk, (now_ns() - c->faults_t0) * 1e-3);
     FaultState& fs = chn.fault[path];
     if (!f.f.up && !fs.down) {
       fs.down = true;
@@ -2021,6 +2028,23 @@ static iccl_result_t backup_stream(iccl_comm* c, Channel& chn, cudaStream_t* out
   return ICCL_SUCCESS;
 }
 
+// Progress words of an armed primary are written from this stream, behind
+// an untimed event recorded after each chunk: a stream-memory write between
+// two copies would drain the copy engine (+4.6 us per chunk at 8 MiB chunks,
+// profiles/r02/README.md §4), an event does not.
+static iccl_result_t prog_stream(iccl_comm* c, Channel& chn, cudaStream_t* out) {
+  if (chn.p_si < 0) {
+    StreamCtx sc;
+    ICCL_CHECK_CUDA(cudaStreamCreateWithFlags(&sc.s, cudaStreamNonBlocking));
+    ICCL_CHECK_CUDA(cudaEventCreateWithFlags(&sc.ev, cudaEventDisableTiming));
+    sc.engine = ENG_CE;
+    c->streams.push_back(sc);
+    chn.p_si = (int)c->streams.size() - 1;
+  }
+  *out = c->streams[chn.p_si].s;
+  return ICCL_SUCCESS;
+}
+
 // The device-driven failover covers a transfer that starts on the primary
 // with the SM backup; the relay backup and transfers issued on the backup
 // path run the proxy-driven chunk pipeline (rzv_launch).
@@ -2079,6 +2103,11 @@ static iccl_result_t armed_launch(iccl_comm* c, Xfer&& x, int kind, cudaStream_t
     r = wait_both_ready(c, ps, x);
   }
   if (r) return r;
+  cudaStream_t pstr = nullptr;
+  if (c->prog_events) {
+    r = prog_stream(c, chn, &pstr);
+    if (r) return r;
+  }
   for (int k = 0; k < x.nchunks; k++) {
     const size_t off = (size_t)k * x.chunk, n = std::min(x.chunk, x.bytes - off);
     {
@@ -2103,7 +2132,14 @@ static iccl_result_t armed_launch(iccl_comm* c, Xfer&& x, int kind, cudaStream_t
     }
     c->copies_issued += 1;
     c->bytes_issued += n;
-    r = memop_write(ps, &w->prog, (uint32_t)(k + 1));
+    if (c->prog_events) {
+      if (!x.rec[k].ev) x.rec[k].ev = get_event(c);
+      ICCL_CHECK_CUDA(cudaEventRecord(x.rec[k].ev, ps));
+      ICCL_CHECK_CUDA(cudaStreamWaitEvent(pstr, x.rec[k].ev, 0));
+      r = memop_write(pstr, &w->prog, (uint32_t)(k + 1));
+    } else {
+      r = memop_write(ps, &w->prog, (uint32_t)(k + 1));
+    }
     if (r) return r;
   }
   p.push_back(wparam(&w->p_fin, 1));
@@ -2303,6 +2339,7 @@ static bool armed_progress(iccl_comm* c, Channel& chn) {
     }
     x.completed = x.nchunks;
     publish(c, x);
+    put_events(c, x);  // the progress events (pool bookkeeping only, no CUDA call)
     __atomic_store_n(&c->armed_used[x.aw], (uint8_t)0, __ATOMIC_RELEASE);
     chn.armed.pop_front();
     c->pending_xfers.fetch_sub(1);
@@ -3036,6 +3073,7 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
   c->instream_ce = env_us("ICCL_INSTREAM", 1) != 0;
   c->armed_backup = env_us("ICCL_ARMED_BACKUP", 1) != 0;
   c->k9_mode = (int)env_us("ICCL_K9_MODE", 0);
+  c->prog_events = env_us("ICCL_PROG_EVENTS", 1) != 0;
   std::vector<char*> peer_scratch(nranks, nullptr);
   for (int p = 0; p < nranks; p++) {
     if (p == rank) {
