@@ -3452,7 +3452,9 @@ iccl_result_t iccl_group_end(iccl_comm_t c) {
       // writes: a local copy and a peer copy run on different copy engines
       std::vector<size_t> self, remote;
       for (size_t i : mine) (elide[i] && c->self_overlap ? self : remote).push_back(i);
-      if (remote.empty()) {
+      bool armed_here = false;  // armed transfers of this stream (mode 2) go between the fork and the join
+      for (size_t i = 0; i < jobs.size(); i++) armed_here |= mode[i] == 2 && jobs[i].stream == s;
+      if (remote.empty() && !armed_here) {
         remote.swap(self);
       }
       cudaStream_t ss = c->streams[c->self_si].s;
@@ -3465,14 +3467,17 @@ iccl_result_t iccl_group_end(iccl_comm_t c) {
       }
       for (size_t i : remote)
         if (!r) r = instream_copies(c, xs[i], s);
+      for (size_t i = 0; i < jobs.size() && !r; i++)
+        if (mode[i] == 2 && jobs[i].stream == s) r = armed_launch(c, std::move(xs[i]), jobs[i].kind, s, true);
       if (!r && !self.empty()) ICCL_CHECK_CUDA(cudaStreamWaitEvent(s, c->self_join, 0));
       for (size_t i : mine) instream_done_params(c, xs[i], p);
       if (!r) r = batch_memops(s, p);
       if (r) return r;
       for (size_t i : mine) rzv_track(c, std::move(xs[i]), false);
+    } else {
+      for (size_t i = 0; i < jobs.size() && !r; i++)
+        if (mode[i] == 2 && jobs[i].stream == s) r = armed_launch(c, std::move(xs[i]), jobs[i].kind, s, true);
     }
-    for (size_t i = 0; i < jobs.size() && !r; i++)
-      if (mode[i] == 2 && jobs[i].stream == s) r = armed_launch(c, std::move(xs[i]), jobs[i].kind, s, true);
     if (r) return r;
     if (!ce.empty()) r = stream_markers(c, s, ce, 2);  // done waits
     if (r) return r;

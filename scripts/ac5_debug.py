@@ -10,18 +10,25 @@ os.environ["ICCL_DEBUG"] = "1"
 import gpu_scenarios as sc  # noqa: E402
 from gpu_helpers import run_ranks  # noqa: E402
 
-MiB = 1 << 20
-with tempfile.TemporaryDirectory() as d:
-    try:
-        res = run_ranks(2, sc.monitor_accuracy, d, nchunks=128, chunk=16 * MiB, stall_chunk=64, up_us=20_000,
-                        config=dict(chunk_bytes=16 * MiB, monitor_enabled=True, delta_us=200_000, window=1024))
-        print("switches", [r["switches"] for r in res], [r["switch_desc"] for r in res])
-    finally:
-        for r in range(2):
-            p = os.path.join(d, f"rank{r}.log")
-            if os.path.exists(p):
-                lines = open(p).read().splitlines()
-                print(f"---- rank {r}: {len(lines)} lines")
-                keep = [ln for ln in lines if "fault" in ln or "gate" in ln or "switch" in ln or "issue" in ln
-                        or "posted" in ln or "Error" in ln]
-                print("\n".join(keep[:200]))
+
+
+def main():
+    MiB = 1 << 20
+    with tempfile.TemporaryDirectory() as d:
+        try:
+            res = run_ranks(2, sc.monitor_accuracy, d, nchunks=128, chunk=16 * MiB, stall_chunk=64, up_us=20_000,
+                            config=dict(chunk_bytes=16 * MiB, monitor_enabled=True, delta_us=200_000, window=1024))
+            print("switches", [r["switches"] for r in res], [r["switch_desc"] for r in res])
+        finally:
+            for r in range(2):
+                p = os.path.join(d, f"rank{r}.log")
+                if os.path.exists(p):
+                    lines = open(p).read().splitlines()
+                    print(f"---- rank {r}: {len(lines)} lines")
+                    keep = [ln for ln in lines if "fault" in ln or "gate" in ln or "switch" in ln or "issue" in ln
+                            or "posted" in ln or "Error" in ln]
+                    print("\n".join(keep[:200]))
+
+
+if __name__ == "__main__":
+    main()
