@@ -64,6 +64,10 @@ for STEP in "$@"; do
           timeout 300 python benchmarks/kernels.py --only k1_local,k1_peer,k2,k3,k8 >> "$LOG" 2>&1 ;;
     var:*) timeout 3000 bash scripts/variants.sh "scripts/variants/${STEP#var:}.txt" >> "$LOG" 2>&1 ;;
     dispatch) timeout 600 $TR --nproc-per-node $NG --master-port 29680 benchmarks/moe_dispatch.py >> "$LOG" 2>&1 ;;
+    failcaps) for C in 16 32 64; do echo "## sm_cap $C" >> "$LOG"
+                ICCL_SM_CAP=$C timeout 600 $TR --nproc-per-node $NG --master-port 2969$((C % 7)) benchmarks/failover.py >> "$LOG" 2>&1
+                ICCL_SM_CAP=$C timeout 600 $TR --nproc-per-node $NG --master-port 2969$((C % 7 + 1)) benchmarks/failover.py --chunk-mib 32 >> "$LOG" 2>&1
+              done ;;
     moe) for I in iccl nccl; do timeout 600 $TR --nproc-per-node $NG --master-port 29679 benchmarks/moe_alltoallv.py --impl $I >> "$LOG" 2>&1; done ;;
     launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --target-processes all -c 2000 --csv \
                 --log-file gpurun_out/${TAG}_launches.csv python -c "import __graft_entry__ as g; g.smoke()" >> "$LOG" 2>&1 ;;

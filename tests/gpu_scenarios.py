@@ -414,6 +414,13 @@ def monitor_accuracy(comm, rank, world, nchunks, chunk, stall_chunk, up_us):
     out = {}
     src = to_dev(payload(n, seed=5), dev) if rank == 0 else None
     dst = torch.empty(n, dtype=torch.uint8, device=dev) if rank == 1 else None
+    # warm-up op on the same tensors: the first use of a peer allocation
+    # opens its IPC mapping (135 ms for this 2 GiB buffer on a B200 box),
+    # which would delay the issue — and the Down — past the timed Up
+    if rank == 0:
+        comm.send(src, 1)
+    else:
+        comm.recv(dst, 0)
     torch.cuda.synchronize()
     comm.monitor.drain()
     # the Up is timed from the install: both ranks install together, right
