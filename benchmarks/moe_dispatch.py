@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Config 4's dispatch half, three ways:
+"""Config 4's dispatch and combine, three ways each:
 
   fused    K8 (iccl_dispatch_rows): each token row read once, its k routed
            copies stored straight into the owners' receive buffers over
@@ -7,6 +7,13 @@
   unfused  K2 (expand form) into a packed buffer, then the copy-engine
            alltoallv (0 SMs for the transfer)
   nccl     torch gather of the routed rows + NCCL all_to_all_single
+
+and the combine (identity experts: the received rows go straight back):
+
+  fused    K10 (iccl_combine_rows): each token rank loads its rows from the
+           expert ranks' tensors over NVLink into their (token, k) slots
+  unfused  the reverse copy-engine alltoallv into a packed buffer, then K3
+  nccl     NCCL all_to_all_single, then torch index_copy_
 
 T = 4096 tokens per rank, top-8 of 64 experts, hidden 7168 bf16, skewed
 routing (§8d).  One step = one dispatch; device time per step (CUDA events),
@@ -44,8 +51,8 @@ def main():
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
     import paper_2510_00991_b200 as iccl
-    from paper_2510_00991_b200.moe import (config4_routing, config4_tokens, expand_rows, moe_dispatch_fused,
-                                           plan_dispatch)
+    from paper_2510_00991_b200.moe import (config4_routing, config4_tokens, expand_rows, moe_combine_fused,
+                                           moe_dispatch_fused, plan_dispatch, scatter_rows)
     T, k, E, H = args.tokens, 8, 64, 7168
     row = 2 * H
     comm = iccl.init(rank, world, local, iccl.IcclConfig.defaults())
@@ -62,6 +69,19 @@ def main():
     packed = torch.empty(T * k, H, dtype=tokens.dtype, device=dev)
     nrecv = sum(plan.recv_counts)
     bufs = {a: torch.zeros(nrecv, H, dtype=tokens.dtype, device=dev) for a in ("fused", "unfused", "nccl")}
+
+    back = torch.empty(T * k, H, dtype=tokens.dtype, device=dev)
+    outs = {a: torch.zeros(T * k, H, dtype=tokens.dtype, device=dev) for a in ("fused", "unfused", "nccl")}
+
+    def combine(arm):
+        if arm == "fused":
+            moe_combine_fused(comm, bufs["fused"], plan, T, k, outs["fused"])
+        elif arm == "unfused":
+            comm.alltoallv(back, bufs["unfused"], plan.send_counts, plan.recv_counts)
+            scatter_rows(back, plan.order, outs["unfused"])
+        else:
+            dist.all_to_all_single(back, bufs["nccl"], plan.send_counts, plan.recv_counts)
+            outs["nccl"].index_copy_(0, plan.order, back)
 
     def step(arm):
         if arm == "fused":
@@ -108,6 +128,25 @@ def main():
         if arm != "nccl":
             res[arm]["kernels_per_step"] = (s1["kernels_launched"] - s0["kernels_launched"]) / args.steps
             res[arm]["ctas_per_step"] = (s1["ctas_launched"] - s0["ctas_launched"]) / args.steps
+        # the combine alone, then dispatch + combine (one MoE step without the experts)
+        for name, fn in (("combine", lambda: combine(arm)), ("dispatch_combine", lambda: (step(arm), combine(arm)))):
+            for _ in range(args.warmup):
+                fn()
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0.record(st)
+            for _ in range(args.steps):
+                fn()
+            e1.record(st)
+            torch.cuda.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            res[arm][f"ms_per_{name}"] = round(float(t.item()), 4)
+        ok = torch.equal(outs[arm].view(T, k, H).view(torch.int16),
+                         tokens.view(torch.int16).unsqueeze(1).expand(T, k, H))
+        okt = torch.tensor([1.0 if ok else 0.0], device=dev, dtype=torch.float64)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        res[arm]["roundtrip_bit_exact"] = bool(okt.item() > 0)
     if rank == 0:
         print(json.dumps(res), flush=True)
     comm.destroy()

@@ -229,6 +229,19 @@ iccl_result_t iccl_dispatch_rows(iccl_comm_t comm, const void* tokens, int64_t n
                                  const int64_t* pos, const size_t* scounts, void* rbuf, const size_t* rcounts,
                                  int64_t row_bytes, cudaStream_t s);
 
+/* ---- fused MoE combine (K10) --------------------------------------------
+ * Collective over the communicator, the reverse of iccl_dispatch_rows.
+ * Result identical to
+ *   iccl_alltoallv(expert_rows, scounts, prefix(scounts), packed, rcounts, prefix(rcounts), row_bytes)
+ *   iccl_scatter_rows(packed -> out, idx = order)      (out row order[r] = packed row r)
+ * but the receiving rank's kernel loads its rows straight from the senders'
+ * expert_rows over NVLink and stores them at their out rows, with no packed
+ * buffer.  scounts: rows this rank returns to each rank (grouped by rank in
+ * expert_rows); rcounts: rows it gets back from each (the packed layout that
+ * `order` indexes).  Pairs armed for failover take the unfused form. */
+iccl_result_t iccl_combine_rows(iccl_comm_t comm, const void* expert_rows, const size_t* scounts, void* out,
+                                const int64_t* order, const size_t* rcounts, int64_t row_bytes, cudaStream_t s);
+
 /* ---- MoE pack / unpack permutation kernels (K2 / K3), stream-ordered ----
  * dst row i <- src row idx[i] (gather, dispatch pack); dst row idx[i] <- src
  * row i (scatter, combine unpack).  idx is a device int64 array; rows are

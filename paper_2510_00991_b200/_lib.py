@@ -123,6 +123,7 @@ PROTOTYPES = {
     "iccl_scatter_rows": (_c, [_p, _p, _p, _i64, _i64, C.c_int, _p]),
     "iccl_expand_rows": (_c, [_p, _p, _p, _i64, C.c_int32, _i64, C.c_int, _p]),
     "iccl_dispatch_rows": (_c, [_p, _p, _i64, C.c_int32, _p, C.POINTER(_sz), _p, C.POINTER(_sz), _i64, _p]),
+    "iccl_combine_rows": (_c, [_p, _p, C.POINTER(_sz), _p, _p, C.POINTER(_sz), _i64, _p]),
     "iccl_copy_sm": (_c, [_p, _p, _sz, C.c_int, _p]),
     "iccl_retry_timeout_ns": (_u64, [C.c_int, C.c_int]),
     "iccl_switch_pointers": (C.c_int, [C.POINTER(XferState), C.POINTER(XferState)]),

@@ -221,6 +221,37 @@ struct DispatchOp {
   FusedDest d[kMaxFusedRanks];
 };
 cudaError_t launch_dispatch(const DispatchOp& op, int ctas, cudaStream_t st, int* grid_out = nullptr);
+// K10: fused MoE combine (the reverse alltoallv + K3 in one kernel, no
+// staging): packed row r (rows grouped by the expert rank d that holds them,
+// lo[d] <= r < hi[d]) is loaded from row r - lo[d] of seg[d] — this rank's
+// segment in rank d's expert-output tensor, IPC-mapped (NVLink loads) or
+// local — and stored at out row order[r].
+struct FusedSrc {
+  const char* seg;
+  int64_t lo, hi;
+  const uint32_t* ready;  // the source's send-op ready flag (host-mapped), null for the self segment
+  uint32_t ready_gen;
+  uint32_t done_gen;
+  uint32_t* done;         // the source's send-op done flag, or null
+  uint32_t* my_done;      // this rank's recv-op done flag, or null
+  uint32_t my_done_gen;
+  uint32_t pad;
+};
+struct CombineOp {
+  int4* out;
+  const int64_t* order;  // [n_rows]: out row of packed row r
+  int64_t n_rows;
+  int32_t n, parts;
+  int64_t row16;
+  uint32_t go_gen, pad;
+  unsigned int* ticket;
+  unsigned int* counter;
+  unsigned int* go;
+  unsigned int* error;
+  KernelStamp* stamp;
+  FusedSrc d[kMaxFusedRanks];
+};
+cudaError_t launch_combine(const CombineOp& op, int ctas, cudaStream_t st, int* grid_out = nullptr);
 cudaError_t launch_scatter_rows(const void* src, void* dst, const int64_t* idx, int64_t n_rows, int64_t row_bytes,
                                 int ctas, cudaStream_t st);
 }  // namespace iccl

@@ -15,6 +15,8 @@
 //                     move yields a WR/WC record.
 // K2  gather rows     MoE dispatch pack: dst[i] = src[idx[i]] (16 B vectors).
 // K3  scatter rows    MoE combine unpack: dst[idx[i]] = src[i].
+// K10 combine pull    fused MoE combine: the reverse alltoallv as NVLink loads
+//                     from the expert ranks' tensors + K3's scatter.
 // K9  backup attempt  the pre-enqueued backup of an armed transfer: CTS
 //                     probe on request, K1 over the suffix after a switch.
 // K8  dispatch push   fused MoE dispatch: K2's expand form storing every
@@ -383,7 +385,7 @@ __global__ void __launch_bounds__(256) iccl_gather_rows(const int4* __restrict__
 // Each token row is split into `parts` column ranges, one warp each, so T
 // tokens give T * parts warps (a whole-row warp left ~1/3 of the warp slots
 // busy at T = 4096: ncu, profiles/r01/ncu/k2_expand_k3_summary.csv).
-__global__ void __launch_bounds__(256) iccl_expand_rows(const int4* __restrict__ src, int4* __restrict__ dst,
+__global__ void __launch_bounds__(256, 5) iccl_expand_rows(const int4* __restrict__ src, int4* __restrict__ dst,
                                                        const int64_t* __restrict__ pos, int64_t n_src, int k,
                                                        int64_t row16, int parts) {
   const int lane = threadIdx.x & 31;
@@ -439,7 +441,7 @@ __device__ __forceinline__ int fused_dest_of(const int64_t* hi, int n, int64_t p
   return lo;
 }
 
-__global__ void __launch_bounds__(256) iccl_dispatch_push(const __grid_constant__ DispatchOp op) {
+__global__ void __launch_bounds__(256, 5) iccl_dispatch_push(const __grid_constant__ DispatchOp op) {
   __shared__ int64_t s_lo[kMaxFusedRanks], s_hi[kMaxFusedRanks];
   __shared__ int4* s_seg[kMaxFusedRanks];
   for (int d = threadIdx.x; d < op.n; d += blockDim.x) {
@@ -516,6 +518,95 @@ __global__ void __launch_bounds__(256) iccl_dispatch_push(const __grid_constant_
     }
   }
   __threadfence_system();  // every thread's row stores, before the CTA's arrival
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atomicAdd(op.counter, 1u) == gridDim.x - 1) {
+      atomicExch(op.counter, 0u);
+      atomicExch(op.ticket, 0u);
+      __threadfence_system();
+      if (op.stamp) {
+        const unsigned long long t = globaltimer();
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&op.stamp->t2), "l"(t) : "memory");
+      }
+      for (int d = 0; d < op.n; d++) {
+        if (op.d[d].done)
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(op.d[d].done), "r"(op.d[d].done_gen) : "memory");
+        if (op.d[d].my_done)
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(op.d[d].my_done), "r"(op.d[d].my_done_gen)
+                       : "memory");
+      }
+    }
+  }
+}
+
+// K10: fused MoE combine (iccl_internal.h CombineOp).  The mirror of K8:
+// the receiving (token) rank runs it and pulls — each warp loads one column
+// part of a packed row from the expert rank's tensor over NVLink (four
+// 16-byte loads in flight per lane) and stores it at the row's (token, k)
+// slot; same entry ticket / exit counter handshake as K8, with the roles of
+// the flags swapped (it waits for the sources' ready flags and releases their
+// done flags).
+__global__ void __launch_bounds__(256, 5) iccl_combine_pull(const __grid_constant__ CombineOp op) {
+  __shared__ int64_t s_lo[kMaxFusedRanks], s_hi[kMaxFusedRanks];
+  __shared__ const int4* s_seg[kMaxFusedRanks];
+  for (int d = threadIdx.x; d < op.n; d += blockDim.x) {
+    s_lo[d] = op.d[d].lo;
+    s_hi[d] = op.d[d].hi;
+    s_seg[d] = (const int4*)op.d[d].seg;
+  }
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = globaltimer();
+    if (atomicAdd(op.ticket, 1u) == 0) {
+      for (int d = 0; d < op.n; d++) {
+        if (!op.d[d].ready) continue;
+        uint32_t v;
+        do {
+          asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(op.d[d].ready) : "memory");
+          if ((int32_t)(v - op.d[d].ready_gen) < 0 && globaltimer() - t0 > 10000000000ull) {
+            *op.error = 1;
+            break;
+          }
+        } while ((int32_t)(v - op.d[d].ready_gen) < 0);
+      }
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(op.go), "r"(op.go_gen) : "memory");
+      if (op.stamp) {
+        const unsigned long long t = globaltimer();
+        asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(&op.stamp->t1), "l"(t) : "memory");
+      }
+    } else {
+      uint32_t v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(op.go) : "memory");
+        if (v != op.go_gen && globaltimer() - t0 > 10000000000ull) {
+          *op.error = 1;
+          break;
+        }
+      } while (v != op.go_gen);
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t row16 = op.row16;
+  const int64_t span = (row16 + op.parts - 1) / op.parts;
+  for (int64_t w = warp; w < op.n_rows * op.parts; w += nwarps) {
+    const int64_t r = w / op.parts;
+    const int64_t c0 = (w % op.parts) * span, c1 = min(row16, c0 + span);
+    const int d = fused_dest_of(s_hi, op.n, r);
+    const int4* src = s_seg[d] + (r - s_lo[d]) * row16;
+    int4* dst = op.out + op.order[r] * row16;
+    int64_t c = c0 + lane;
+    for (; c + 96 < c1; c += 128) {
+      const int4 v0 = ld_nc(src + c), v1 = ld_nc(src + c + 32), v2 = ld_nc(src + c + 64), v3 = ld_nc(src + c + 96);
+      st_cs(dst + c, v0);
+      st_cs(dst + c + 32, v1);
+      st_cs(dst + c + 64, v2);
+      st_cs(dst + c + 96, v3);
+    }
+    for (; c < c1; c += 32) st_cs(dst + c, ld_nc(src + c));
+  }
+  __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {
     if (atomicAdd(op.counter, 1u) == gridDim.x - 1) {
@@ -724,13 +815,20 @@ cudaError_t launch_backup(const BackupOp& op, int ctas, cudaStream_t st, int* gr
     return cudaErrorInvalidValue;
   if (cudaError_t e = configure_smem()) return e;
   const size_t ntiles = (min(op.chunk, op.bytes) + kTile - 1) / kTile;
-  int grid = (int)min((size_t)max(ctas, 1), ntiles > 0 ? ntiles : (size_t)1);
+  int grid = (int)min((size_t)max(ctas, 16), ntiles > 0 ? ntiles : (size_t)1);
+  if (ctas > 0) grid = (int)min((size_t)ctas, ntiles > 0 ? ntiles : (size_t)1);
   if (grid < 1) grid = 1;
   if (grid_out) *grid_out = grid + 1;
   iccl_backup_ctl<<<1, 32, 0, st>>>(op);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || ctas == 0) return e;  // ctas 0: the controller alone (attribution runs)
-  iccl_backup_attempt<<<grid, kCopyThreads, kStages * kTile, st>>>(op);
+  // attribution runs only (ctas < 0): -1 = the copy grid without its shared
+  // memory (it must not copy), -2 = a one-CTA copy grid
+  if (ctas == -1) {
+    iccl_backup_attempt<<<grid, kCopyThreads, 0, st>>>(op);
+    return cudaGetLastError();
+  }
+  iccl_backup_attempt<<<ctas == -2 ? 1 : grid, kCopyThreads, kStages * kTile, st>>>(op);
   return cudaGetLastError();
 }
 
@@ -771,7 +869,8 @@ cudaError_t preload_kernels() {
                        (const void*)iccl_read_globaltimer, (const void*)iccl_gather_rows,
                        (const void*)iccl_scatter_rows, (const void*)iccl_expand_rows,
                        (const void*)iccl_ll_group, (const void*)iccl_wait_flags, (const void*)iccl_dispatch_push,
-                       (const void*)iccl_backup_attempt, (const void*)iccl_backup_ctl};
+                       (const void*)iccl_backup_attempt, (const void*)iccl_backup_ctl,
+                       (const void*)iccl_combine_pull};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;
@@ -815,11 +914,27 @@ cudaError_t launch_dispatch(const DispatchOp& op, int ctas, cudaStream_t st, int
   }
   const int64_t warps = op.n_tokens * op.parts;
   int64_t grid = (warps + 7) / 8;
-  const int64_t cap = ctas > 0 ? ctas : 4 * (int64_t)sms;  // 4 x 256-thread CTAs per SM resident
+  const int64_t cap = ctas > 0 ? ctas : 5 * (int64_t)sms;  // one wave: 5 x 256-thread CTAs per SM (48 registers)
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
   if (grid_out) *grid_out = (int)grid;
   iccl_dispatch_push<<<(int)grid, 256, 0, st>>>(op);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine(const CombineOp& op, int ctas, cudaStream_t st, int* grid_out) {
+  if (grid_out) *grid_out = 0;
+  // launched even with no rows: its last CTA writes the done flags
+  if (op.n > kMaxFusedRanks || op.row16 <= 0 || ((uintptr_t)op.out & 15)) return cudaErrorInvalidValue;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t grid = (op.n_rows * op.parts + 7) / 8;
+  const int64_t cap = ctas > 0 ? ctas : 5 * (int64_t)sms;
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  if (grid_out) *grid_out = (int)grid;
+  iccl_combine_pull<<<(int)grid, 256, 0, st>>>(op);
   return cudaGetLastError();
 }
 
@@ -829,6 +944,12 @@ cudaError_t launch_expand_rows(const void* src, void* dst, const int64_t* pos, i
   if ((row_bytes & 15) || ((uintptr_t)src & 15) || ((uintptr_t)dst & 15)) return cudaErrorInvalidValue;
   const int64_t row16 = row_bytes / 16;
   const int parts = (int)max((int64_t)1, min((int64_t)8, row16 / 128));  // >= 4 int4 per lane per part
+  if (ctas <= 0) {  // one wave: 5 x 256-thread CTAs per SM (48 registers)
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    ctas = 5 * sms;
+  }
   iccl_expand_rows<<<rows_grid(n_src * parts, ctas), 256, 0, st>>>((const int4*)src, (int4*)dst, pos, n_src, k,
                                                                    row16, parts);
   return cudaGetLastError();

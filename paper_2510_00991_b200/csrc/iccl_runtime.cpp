@@ -316,6 +316,7 @@ struct OpDesc {
   bool issued_instream = false;  // this side issued the copy on its own user stream (no markers)
   bool markers_elided = false;   // self pair, both halves on one stream in one group: no markers at all
   bool fused = false;            // a send of a fused dispatch (K8 stores the rows; iccl_dispatch_rows)
+  bool pull = false;             // a recv of a fused combine (K10 loads the rows; iccl_combine_rows)
   DirectOp dop{};        // K6 parameters when issued_direct
   int kstamp = -1;       // monitor on: K5 send / K6 stamp slot (K4), turned into a record by the proxy
 };
@@ -511,6 +512,12 @@ struct iccl_comm {
   bool dispatch_fused = false;
   cudaStream_t dispatch_stream = nullptr;
   DispatchOp dispatch_op{};
+  // fused MoE combine (iccl_combine_rows): its recvs rendezvous at group_end
+  // (each waits for the sender's half and pulls), then K10 runs on the stream
+  bool in_combine = false;
+  bool combine_fused = false;
+  cudaStream_t combine_stream = nullptr;
+  CombineOp combine_op{};
   char* dispatch_stage = nullptr;  // staging of the unfused fallback (an armed pair), grown on demand
   size_t dispatch_stage_bytes = 0;
   int direct_ctas = 32;       // K6 grid (>= 16 CTAs keep NVLink busy, kernels bench)
@@ -543,7 +550,8 @@ struct iccl_comm {
   bool k7_ce = false, k7_ready = false;
   bool instream_ce = true;  // healthy pairs: the issuer enqueues the copy on its own user stream (ICCL_INSTREAM=0: off)
   bool armed_backup = true;  // attribution only (ICCL_ARMED_BACKUP=0): armed transfers enqueue no backup attempt
-  int k9_mode = 0;           // attribution only (ICCL_K9_MODE): 1 = K9a alone, 2 = b_fin memop alone
+  int k9_mode = 0;           // attribution only (ICCL_K9_MODE): 1 = K9a alone, 2 = b_fin memop alone,
+                             // 3 = K9b launched without its shared memory, 4 = a one-CTA K9b
   bool prog_events = true;   // armed primaries' progress words from a side stream (ICCL_PROG_EVENTS=0: in-stream memops)
   // monitor records of ops the proxy does not track (K5 sends, K6): their
   // %globaltimer stamps (K4), turned into records once t2 lands
@@ -2200,6 +2208,8 @@ static iccl_result_t armed_launch(iccl_comm* c, Xfer&& x, int kind, cudaStream_t
   int grid = 0;
   if (c->k9_mode == 0) ICCL_CHECK_CUDA(launch_backup(b, c->cfg.sm_cap, bs, &grid));
   if (c->k9_mode == 1) ICCL_CHECK_CUDA(launch_backup(b, 0, bs, &grid));  // K9a only
+  if (c->k9_mode == 3) ICCL_CHECK_CUDA(launch_backup(b, -1, bs, &grid));  // K9b without shared memory
+  if (c->k9_mode == 4) ICCL_CHECK_CUDA(launch_backup(b, -2, bs, &grid));  // one-CTA K9b
   c->kernels_launched += 1;
   c->ctas_launched += grid;
   r = memop_write(bs, &w->b_fin, 1);
@@ -2683,11 +2693,87 @@ static iccl_result_t launch_fused_dispatch(iccl_comm* c, cudaStream_t s, const s
   c->ctas_launched += grid;
   c->dispatch_fused = false;  // launched
   for (const OpDesc& o : sends) {
+    if (!o.fused) continue;
     c->copies_issued += 1;
     c->bytes_issued += o.bytes;
     OpDesc m = o;
     m.kstamp = rec.kstamp;
     push_krec(c, m, 0);
+  }
+  return ICCL_SUCCESS;
+}
+
+// A recv of a fused combine: it waits for the sender's half (RTS: the
+// expert rank's tensor segment) unconditionally, so it always arrives second
+// and claims the transfer — K10 pulls the rows; the sender never issues.
+static iccl_result_t pull_rendezvous(iccl_comm* c, OpDesc& op) {
+  const int peer = op.peer;
+  const uint64_t k = c->pair_recvs[peer]++;
+  RzvEntry& e = rzv_entry(c, 1, peer, k);
+  const uint64_t g = k / kRzvDepth;
+  const uint64_t t0 = now_ns();
+  while (!rzv_free(e, k) || e.arrivals.load(std::memory_order_acquire) < 2 * g + 1) {
+    if (c->async_err.load() != ICCL_SUCCESS) return (iccl_result_t)c->async_err.load();
+    if (c->hdr->abort.load()) return ICCL_ERR_ABORTED;
+    if (now_ns() - t0 > 60ull * 1000000000ull) {
+      set_last_error("fused combine: rank " + std::to_string(peer) + " posted no matching send within 60 s");
+      return ICCL_ERR_TIMEOUT;
+    }
+    sched_yield();
+  }
+  RzvSide& mine = e.side[1];
+  mine.bytes = op.bytes;
+  mine.slot = op.slot;
+  mine.gen = op.gen;
+  mine.direct_ptr = (uint64_t)(uintptr_t)op.src;
+  mine.stream = (uint64_t)(uintptr_t)c->combine_stream;
+  mine.buffer_id = 0;
+  mine.base_offset = 0;
+  RzvSide side[2];
+  ICCL_RETURN_IF(!rzv_arrive(e, k, side), ICCL_ERR_SYSTEM, "fused combine recv arrived first");
+  const RzvSide& snd = side[0];
+  if (snd.bytes != op.bytes) {
+    __atomic_store_n(&flags_of(c, c->rank)->done[op.slot], op.gen, __ATOMIC_SEQ_CST);
+    __atomic_store_n(&flags_of(c, peer)->done[snd.slot], snd.gen, __ATOMIC_SEQ_CST);
+    std::string msg = "combine of " + std::to_string(snd.bytes) + " B from rank " + std::to_string(peer) +
+                      " matched a receive of " + std::to_string(op.bytes) + " B on rank " + std::to_string(c->rank);
+    set_async(c, ICCL_ERR_SIZE_MISMATCH, msg);
+    set_last_error(msg);
+    return ICCL_ERR_SIZE_MISMATCH;
+  }
+  char* mapped = nullptr;
+  iccl_result_t r = open_peer_buffer(c, c->ch[2 * peer + 1], snd, &mapped);
+  if (r) return r;
+  FusedSrc& d = c->combine_op.d[peer];
+  d.seg = mapped;
+  d.ready = &flags_of(c, peer)->ready[snd.slot];
+  d.ready_gen = snd.gen;
+  d.done = &flags_of(c, peer)->done[snd.slot];
+  d.done_gen = snd.gen;
+  d.my_done = &flags_of(c, c->rank)->done[op.slot];
+  d.my_done_gen = op.gen;
+  c->pulls_issued += 1;
+  ICCL_TRACE("fused combine pull %d->%d #%llu, %zu B", peer, c->rank, (unsigned long long)k, op.bytes);
+  return ICCL_SUCCESS;
+}
+
+// K10 for the pending combine on stream s (its pulling recvs: `recvs`).
+static iccl_result_t launch_fused_combine(iccl_comm* c, cudaStream_t s, const std::vector<OpDesc>& recvs) {
+  CombineOp& op = c->combine_op;
+  OpDesc rec{};
+  op.stamp = alloc_kstamp(c, rec);
+  int grid = 0;
+  ICCL_CHECK_CUDA(launch_combine(op, c->dispatch_ctas, s, &grid));
+  c->kernels_launched += 1;
+  c->ctas_launched += grid;
+  c->combine_fused = false;  // launched
+  for (const OpDesc& o : recvs) {
+    if (!o.pull) continue;
+    c->copies_issued += 1;
+    c->bytes_issued += o.bytes;
+    OpDesc m = o;
+    m.kstamp = rec.kstamp;
+    push_krec(c, m, 1);
   }
   return ICCL_SUCCESS;
 }
@@ -2858,7 +2944,7 @@ static iccl_result_t enqueue_op(iccl_comm* c, int kind, const void* buf, size_t 
   // (route_small: both sides route the pair's q-th small op alike).
   // (a dispatch's segments never take LL: a fused sender has no source
   // tensor to stream, and both sides must classify alike)
-  const bool small = !c->in_dispatch && peer != c->rank && c->cfg.transport != ICCL_TRANSPORT_CE &&
+  const bool small = !c->in_dispatch && !c->in_combine && peer != c->rank && c->cfg.transport != ICCL_TRANSPORT_CE &&
                      bytes <= c->cfg.sm_small_bytes && bytes <= kLLMaxBytes && c->ll_region != nullptr;
   op.ll = small && !route_small(pair_of(c, kind == 0 ? c->rank : peer, kind == 0 ? peer : c->rank), kind);
   op.direct = !small && peer != c->rank && c->cfg.transport == ICCL_TRANSPORT_AUTO &&
@@ -2867,12 +2953,17 @@ static iccl_result_t enqueue_op(iccl_comm* c, int kind, const void* buf, size_t 
     if (kind == 1) op.direct = true;  // done wait in K7 (whoever fills the segment)
     op.fused = kind == 0 && c->dispatch_fused;
   }
+  if (c->in_combine && peer != c->rank) {
+    if (kind == 0) op.direct = true;  // done wait in K7 (whoever drains the segment)
+    op.pull = kind == 1 && c->combine_fused;
+  }
   if (op.ll) {
     op.ll_seq = kind == 0 ? ++c->ll_sent[peer] : ++c->ll_recvd[peer];
-  } else if (kind == 1 || c->group_depth == 0) {
+  } else if ((kind == 1 && !op.pull) || c->group_depth == 0) {
     r = rzv_post(c, op, kind == 0 ? kSendWaitUs : 0, c->group_depth > 0, s);
     if (r) return r;
-  }  // a send inside a group posts at group_end, after every recv of the group
+  }  // a send inside a group posts at group_end, after every recv of the group (a
+     // combine's pulling recv too, after its sender's half)
   c->ranks[c->rank].op_count.fetch_add(1, std::memory_order_relaxed);
   if (req) *req = ((uint64_t)op.slot << 32) | op.gen;
   if (c->group_depth > 0) {
@@ -3359,7 +3450,14 @@ iccl_result_t iccl_group_end(iccl_comm_t c) {
       continue;
     }
     const uint64_t t = now_ns();
-    iccl_result_t r = rzv_post(c, p.first, t < deadline ? (deadline - t) / 1000 : 0, true, p.second);
+    // a combine's sends post at once: their receivers pull (K10) and wait for them
+    const uint64_t budget = c->in_combine ? 0 : (t < deadline ? (deadline - t) / 1000 : 0);
+    iccl_result_t r = rzv_post(c, p.first, budget, true, p.second);
+    if (r) return r;
+  }
+  for (auto& p : ops) {
+    if (!p.first.pull) continue;
+    iccl_result_t r = pull_rendezvous(c, p.first);
     if (r) return r;
   }
   // every transfer this side issues for the group: in-stream on the op's own
@@ -3431,13 +3529,14 @@ iccl_result_t iccl_group_end(iccl_comm_t c) {
     std::vector<OpDesc> ce, ll, direct, fused;
     for (auto& p : ops) {
       if (p.second != s || p.first.issued_instream || p.first.markers_elided) continue;
-      (p.first.fused ? fused : p.first.ll ? ll : p.first.issued_direct ? direct : ce).push_back(p.first);
+      (p.first.fused || p.first.pull ? fused : p.first.ll ? ll : p.first.issued_direct ? direct : ce).push_back(p.first);
     }
     iccl_result_t r = ICCL_SUCCESS;
     if (!ce.empty()) r = stream_markers(c, s, ce, 1);  // ready
     if (!r && !ll.empty()) r = launch_ll_ops(c, s, ll);
     if (!r && !direct.empty()) r = launch_direct_ops(c, s, direct);
     if (!r && c->dispatch_fused && c->dispatch_stream == s) r = launch_fused_dispatch(c, s, fused);
+    if (!r && c->combine_fused && c->combine_stream == s) r = launch_fused_combine(c, s, fused);
     if (r) return r;
     std::vector<CUstreamBatchMemOpParams> p;
     std::vector<size_t> mine;
@@ -3558,7 +3657,7 @@ iccl_result_t iccl_dispatch_rows(iccl_comm_t c, const void* tokens, int64_t n_to
       ICCL_CHECK_CUDA(cudaMalloc((void**)&c->dispatch_stage, need));
       c->dispatch_stage_bytes = need;
     }
-    if (stot) ICCL_CHECK_CUDA(launch_expand_rows(tokens, c->dispatch_stage, pos, n_tokens, k, row_bytes, 148 * 8, s));
+    if (stot) ICCL_CHECK_CUDA(launch_expand_rows(tokens, c->dispatch_stage, pos, n_tokens, k, row_bytes, 0, s));
     c->in_dispatch = true;
     r = iccl_alltoallv(c, c->dispatch_stage, scounts, sd.data(), rbuf, rcounts, rd.data(), (size_t)row_bytes, s);
     c->in_dispatch = false;
@@ -3608,6 +3707,100 @@ iccl_result_t iccl_dispatch_rows(iccl_comm_t c, const void* tokens, int64_t n_to
   if (!r && c->dispatch_fused) r = launch_fused_dispatch(c, s, {});
   c->dispatch_fused = false;
   c->in_dispatch = false;
+  return r;
+}
+
+// Fused MoE combine (K10): see include/iccl_b200.h.  Equivalent to
+// iccl_alltoallv of the expert rows back to their token ranks into a packed
+// buffer followed by iccl_scatter_rows(packed -> out, order), in one kernel
+// on the receiving side and without the packed buffer.  If a pair this rank
+// receives from is armed for failover, the call takes exactly that unfused
+// form (staging + alltoallv + K3); senders cannot tell the two forms apart.
+iccl_result_t iccl_combine_rows(iccl_comm_t c, const void* expert_rows, const size_t* scounts, void* out,
+                                const int64_t* order, const size_t* rcounts, int64_t row_bytes, cudaStream_t s) {
+  ICCL_RETURN_IF(!c || !scounts || !rcounts || row_bytes <= 0 || (row_bytes & 15), ICCL_ERR_INVALID_ARGUMENT,
+                 "combine: bad arguments (row_bytes a multiple of 16)");
+  ICCL_RETURN_IF(c->group_depth > 0, ICCL_ERR_INVALID_ARGUMENT, "combine inside a group");
+  ICCL_RETURN_IF(c->nranks > kMaxFusedRanks, ICCL_ERR_INVALID_ARGUMENT, "combine: more than 64 ranks");
+  ICCL_RETURN_IF(((uintptr_t)expert_rows & 15) || ((uintptr_t)out & 15), ICCL_ERR_INVALID_ARGUMENT,
+                 "combine: the expert rows and the output must be 16-byte aligned");
+  int ae = c->async_err.load();
+  if (ae != ICCL_SUCCESS) {
+    set_last_error(c->async_msg);
+    return (iccl_result_t)ae;
+  }
+  const int n = c->nranks, me = c->rank;
+  std::vector<size_t> sd(n), rd(n);
+  size_t stot = 0, rtot = 0;
+  for (int d = 0; d < n; d++) {
+    sd[d] = stot;
+    rd[d] = rtot;
+    stot += scounts[d];
+    rtot += rcounts[d];
+  }
+  ICCL_RETURN_IF(scounts[me] != rcounts[me], ICCL_ERR_SIZE_MISMATCH, "combine: self send and receive counts differ");
+  ICCL_RETURN_IF(stot > 0 && !expert_rows, ICCL_ERR_INVALID_ARGUMENT, "combine: null expert rows");
+  ICCL_RETURN_IF(rtot > 0 && (!out || !order), ICCL_ERR_INVALID_ARGUMENT, "combine: null output / order");
+  bool fused = true;
+  for (int d = 0; d < n && fused; d++)
+    if (d != me && rcounts[d] && xfer_armed(c, 1, d)) fused = false;
+  iccl_result_t r = ICCL_SUCCESS;
+  if (!fused) {
+    const size_t need = rtot * (size_t)row_bytes;
+    if (need > c->dispatch_stage_bytes) {
+      if (c->dispatch_stage) {
+        ICCL_CHECK_CUDA(cudaStreamSynchronize(s));
+        ICCL_CHECK_CUDA(cudaFree(c->dispatch_stage));
+        c->dispatch_stage = nullptr;
+      }
+      ICCL_CHECK_CUDA(cudaMalloc((void**)&c->dispatch_stage, need));
+      c->dispatch_stage_bytes = need;
+    }
+    c->in_combine = true;
+    r = iccl_alltoallv(c, expert_rows, scounts, sd.data(), c->dispatch_stage, rcounts, rd.data(), (size_t)row_bytes, s);
+    c->in_combine = false;
+    if (!r && rtot) ICCL_CHECK_CUDA(launch_scatter_rows(c->dispatch_stage, out, order, (int64_t)rtot, row_bytes, 148 * 8, s));
+    return r;
+  }
+  OpDesc cop{};
+  r = next_slot(c, &cop.slot, &cop.gen, &cop.op_seq);
+  if (r) return r;
+  CombineOp& op = c->combine_op;
+  memset(&op, 0, sizeof(op));
+  op.out = (int4*)out;
+  op.order = order;
+  op.n_rows = (int64_t)rtot;
+  op.n = n;
+  op.row16 = row_bytes / 16;
+  op.parts = (int)std::max<int64_t>(1, std::min<int64_t>(8, op.row16 / 128));
+  op.ticket = c->ll_counters + (c->ll_ctr_next++ % kLLCounters);
+  op.counter = c->ll_counters + (c->ll_ctr_next++ % kLLCounters);
+  op.go = c->ll_counters + kLLCounters + (cop.slot % kLLCounters);
+  op.go_gen = cop.gen;
+  op.error = c->ll_error;
+  for (int d = 0; d < n; d++) {
+    op.d[d].lo = (int64_t)rd[d];
+    op.d[d].hi = (int64_t)(rd[d] + rcounts[d]);
+  }
+  op.d[me].seg = (const char*)expert_rows + sd[me] * (size_t)row_bytes;
+  op.d[me].my_done = &flags_of(c, me)->done[cop.slot];
+  op.d[me].my_done_gen = cop.gen;
+  c->combine_stream = s;
+  c->combine_fused = true;
+  c->in_combine = true;
+  r = iccl_group_start(c);
+  for (int kk = 1; kk < n && r == ICCL_SUCCESS; kk++) {
+    const int to = (me + kk) % n, from = (me - kk + n) % n;
+    if (rcounts[from]) r = iccl_recv(c, out, rcounts[from] * (size_t)row_bytes, from, s, nullptr);
+    if (!r && scounts[to])
+      r = iccl_send(c, (const char*)expert_rows + sd[to] * (size_t)row_bytes, scounts[to] * (size_t)row_bytes, to, s,
+                    nullptr);
+  }
+  iccl_result_t r2 = iccl_group_end(c);
+  if (!r) r = r2;
+  if (!r && c->combine_fused) r = launch_fused_combine(c, s, {});  // no remote recv on s: the self segment
+  c->combine_fused = false;
+  c->in_combine = false;
   return r;
 }
 
@@ -3751,7 +3944,7 @@ iccl_result_t iccl_expand_rows(const void* src, void* dst, const int64_t* pos, i
                                int64_t row_bytes, int ctas, cudaStream_t s) {
   if ((n_src > 0 && k > 0 && (!src || !dst || !pos)) || n_src < 0 || k < 0 || row_bytes <= 0)
     return ICCL_ERR_INVALID_ARGUMENT;
-  ICCL_CHECK_CUDA(launch_expand_rows(src, dst, pos, n_src, k, row_bytes, ctas > 0 ? ctas : 148 * 8, s));
+  ICCL_CHECK_CUDA(launch_expand_rows(src, dst, pos, n_src, k, row_bytes, ctas, s));
   return ICCL_SUCCESS;
 }
 

@@ -160,3 +160,27 @@ def moe_combine(comm, expert_out: torch.Tensor, plan: DispatchPlan, T: int, k: i
         out = torch.empty((T * k,) + tuple(expert_out.shape[1:]), dtype=expert_out.dtype, device=expert_out.device)
     scatter_rows(back, plan.order, out, stream=stream)
     return out.view(T, k, *expert_out.shape[1:])
+
+
+def moe_combine_fused(comm, expert_out: torch.Tensor, plan: DispatchPlan, T: int, k: int,
+                      out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """The same result as :func:`moe_combine` in one kernel on the receiving
+    side, K10 (``iccl_combine_rows``): every row this rank routed out comes
+    back straight from the expert rank's tensor (NVLink loads) into its
+    (token, k) slot of ``out`` [T, k, ...] — no packed staging buffer.  Pairs
+    armed for failover take the unfused form inside the library."""
+    if not expert_out.is_cuda or not expert_out.is_contiguous():
+        raise InvalidArgument("expert_out must be a contiguous CUDA tensor")
+    shape = tuple(expert_out.shape[1:])
+    if out is None:
+        out = torch.empty((T * k,) + shape, dtype=expert_out.dtype, device=expert_out.device)
+    row = out[0].numel() * out.element_size() if out.shape[0] else 16
+    n = len(plan.send_counts)
+    Arr = C.c_size_t * n
+    sc = Arr(*[int(x) for x in plan.recv_counts])   # rows this rank returns to each rank
+    rc = Arr(*[int(x) for x in plan.send_counts])   # rows it gets back (the packed layout `order` indexes)
+    src = expert_out.data_ptr() if expert_out.numel() else out.data_ptr()
+    raise_for(lib.iccl_combine_rows(comm._h, C.c_void_p(src), sc, C.c_void_p(out.data_ptr()),
+                                    C.c_void_p(plan.order.data_ptr()), rc, int(row), _sh(stream)),
+              "iccl_combine_rows")
+    return out.view(T, k, *shape)

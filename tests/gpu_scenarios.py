@@ -422,6 +422,8 @@ def monitor_accuracy(comm, rank, world, nchunks, chunk, stall_chunk, up_us):
     else:
         comm.recv(dst, 0)
     torch.cuda.synchronize()
+    import time
+    time.sleep(0.5)  # the peer's proxy premaps the other tensor in the background
     comm.monitor.drain()
     # the Up is timed from the install: both ranks install together, right
     # before the op, so the Down (at the chunk's issue) always precedes it
@@ -449,7 +451,8 @@ def monitor_accuracy(comm, rank, world, nchunks, chunk, stall_chunk, up_us):
     return out
 
 
-def moe_config4(comm, rank, world, T, k=8, E=64, H=7168, fault=None, keep_bytes=True, fused=False, reps=1):
+def moe_config4(comm, rank, world, T, k=8, E=64, H=7168, fault=None, keep_bytes=True, fused=False, reps=1,
+                fused_combine=False):
     """BASELINE config 4 at `world` ranks: K2 pack (expand), dispatch
     alltoallv, combine alltoallv, K3 unpack, with the §8(d) routing and
     payload.  Checks on the device, at any size: every rank's received rows
@@ -462,8 +465,8 @@ def moe_config4(comm, rank, world, T, k=8, E=64, H=7168, fault=None, keep_bytes=
     `packed` is then built afterwards, for the oracle comparison only.  reps:
     the dispatch runs that many times (buffers reused, the last one checked)."""
     from paper_2510_00991_b200 import FaultScript
-    from paper_2510_00991_b200.moe import (config4_routing, config4_tokens, expand_rows, moe_dispatch_fused,
-                                           plan_dispatch, scatter_rows)
+    from paper_2510_00991_b200.moe import (config4_routing, config4_tokens, expand_rows, moe_combine_fused,
+                                           moe_dispatch_fused, plan_dispatch, scatter_rows)
     dev = dev_of(rank)
     experts = config4_routing(rank, T, k, E, dev)
 
@@ -494,8 +497,13 @@ def moe_config4(comm, rank, world, T, k=8, E=64, H=7168, fault=None, keep_bytes=
             comm.alltoallv(recv, packed, plan.recv_counts, plan.send_counts)
     if fused:
         expand_rows(tokens, plan.pos, k, packed)
-    comm.alltoallv(back, recv, plan.send_counts, plan.recv_counts)
-    scatter_rows(back, plan.order, out)
+    if fused_combine:
+        for _ in range(reps):
+            out.fill_(0)
+            moe_combine_fused(comm, recv, plan, T, k, out)
+    else:
+        comm.alltoallv(back, recv, plan.send_counts, plan.recv_counts)
+        scatter_rows(back, plan.order, out)
     torch.cuda.synchronize()
     # device-side expected rows: what every source i routed to this rank
     per_rank = E // world

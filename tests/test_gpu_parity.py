@@ -451,3 +451,35 @@ def test_fused_dispatch_armed_pair_falls_back(torch_cuda, tmp_path):
     _moe_oracle_check(res, world, T)
     sw = [(r, int(p), int(t)) for r in (1, 2) for p, t in zip(res[r]["switch_peers"], res[r]["switch_to"])]
     assert any(t == 1 for _, _, t in sw), sw
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_fused_combine_vs_oracle(torch_cuda, tmp_path, world):
+    """K10 (fused combine: the reverse alltoallv as NVLink loads + K3's
+    scatter in one kernel, no staging) returns every routed row to its
+    (token, k) slot: the round trip after a fused dispatch equals the tokens,
+    three back-to-back combines reuse the buffers, and the dispatched bytes
+    equal the oracle's."""
+    import gpu_scenarios as sc
+    T = 128
+    res = run_ranks(world, sc.moe_config4, tmp_path, T=T, fused=True, fused_combine=True, reps=3, timeout=300)
+    for r in range(world):
+        assert bool(res[r]["recv_ok"][0]) and bool(res[r]["roundtrip_ok"][0]), r
+    if world > 1:
+        _moe_oracle_check(res, world, T)
+
+
+def test_fused_combine_8_ranks_full_size_and_armed_fallback(torch_cuda, tmp_path):
+    """Config 4 at full size on 8 ranks with K8 + K10, and a 4-rank run with
+    pair 2 -> 1 armed (rank 1 combines through staging + the alltoallv + K3,
+    where the failover applies): every round trip restores the tokens."""
+    import gpu_scenarios as sc
+    res = run_ranks(8, sc.moe_config4, tmp_path, T=4096, keep_bytes=False, fused=True, fused_combine=True,
+                    timeout=300)
+    for r in range(8):
+        assert bool(res[r]["recv_ok"][0]) and bool(res[r]["roundtrip_ok"][0]), r
+    (tmp_path / "armed").mkdir()
+    res = run_ranks(4, sc.moe_config4, tmp_path / "armed", T=128, fused=True, fused_combine=True,
+                    fault=(2, 1, 1 << 20), timeout=300, config=dict(chunk_bytes=256 * 1024))
+    for r in range(4):
+        assert bool(res[r]["recv_ok"][0]) and bool(res[r]["roundtrip_ok"][0]), r
