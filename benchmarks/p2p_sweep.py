@@ -51,6 +51,9 @@ def main():
     ap.add_argument("--armed", action="store_true",
                     help="install a fault script on pair 0->1 that never fires: its ops take the failover-capable path")
     ap.add_argument("--records", action="store_true", help="window monitor on")
+    ap.add_argument("--backup-path", action="store_true",
+                    help="switch_qp both directions to the backup path first (the SM-kernel K1 path): its bandwidth "
+                         "as a fraction of the primary's is the paper's backup retention")
     args = ap.parse_args()
     if args.impl == "nccl-ce":
         os.environ["NCCL_P2P_USE_CUDA_MEMCPY"] = "1"
@@ -74,6 +77,8 @@ def main():
         comm = iccl.init(rank, world, local, cfg)
         if args.armed:
             comm.set_faults(iccl.FaultScript().down(0, 1, chunk=1 << 30, op_index=1 << 30))
+        if args.backup_path:
+            comm.switch_qp(peer, "ToBackup")
 
     def send(t):
         comm.send(t, peer) if comm else dist.send(t, peer)
@@ -131,7 +136,8 @@ def main():
         for _ in range(3):
             pp_loop(s, r)()
         rec = {"impl": args.impl, "bytes": n, "bidir": bool(args.bidir), "armed": bool(args.armed),
-               "monitor": bool(args.records), "chunk_bytes": args.chunk_bytes}
+               "monitor": bool(args.records), "chunk_bytes": args.chunk_bytes, "path": "backup" if args.backup_path
+               else "primary"}
         if comm:
             comm.monitor.drain()
         for mode, pre in (("gpu", True), ("api", False)):

@@ -104,6 +104,8 @@ struct BackupOp {
   const char* probe_src;   // 16 bytes moved by the probe (over the primary path's direction)
   char* probe_dst;
   unsigned int* error;     // host-mapped: set if the decision wait exceeds 60 s
+  unsigned int* dec_dev;   // K9a -> K9b decision word in GPU memory: (seq << 2) | decision
+  uint32_t seq;            // this transfer's generation of dec_dev (30 bits)
 };
 cudaError_t launch_backup(const BackupOp& op, int ctas, cudaStream_t st, int* grid_out = nullptr);
 // K6: direct zero-copy of a mid-size message by the side that arrived second

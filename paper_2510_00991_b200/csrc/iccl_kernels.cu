@@ -224,6 +224,9 @@ __global__ void __launch_bounds__(32) iccl_backup_ctl(const __grid_constant__ Ba
     if (ld_sys(&w->ctl) == kCtlAbort) dec = kDecExit;
   }
   (void)t0;
+  // the copy grid reads the decision from this GPU's memory (a host-mapped
+  // read by each of its CTAs cost ~12 us per armed op, profiles/r02 §4)
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(op.dec_dev), "r"((op.seq << 2) | dec) : "memory");
   st_sys(&w->dec, dec);
 }
 
@@ -234,7 +237,13 @@ __global__ void __launch_bounds__(kCopyThreads) iccl_backup_attempt(const __grid
   __shared__ __align__(8) uint64_t mbar[kStages];
   __shared__ uint32_t s_dec;
   ArmedWords* w = op.w;
-  if (threadIdx.x == 0) s_dec = ld_sys(&w->dec);
+  if (threadIdx.x == 0) {
+    uint32_t v;
+    do {  // K9a precedes on the stream: the word is final, the loop only guards the generation
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(op.dec_dev) : "memory");
+    } while ((v >> 2) != (op.seq & 0x3fffffffu));
+    s_dec = v & 3u;
+  }
   __syncthreads();
   if (s_dec != kDecCopy) return;
   const uint32_t r = ld_sys(&w->resume);
@@ -385,7 +394,7 @@ __global__ void __launch_bounds__(256) iccl_gather_rows(const int4* __restrict__
 // Each token row is split into `parts` column ranges, one warp each, so T
 // tokens give T * parts warps (a whole-row warp left ~1/3 of the warp slots
 // busy at T = 4096: ncu, profiles/r01/ncu/k2_expand_k3_summary.csv).
-__global__ void __launch_bounds__(256, 5) iccl_expand_rows(const int4* __restrict__ src, int4* __restrict__ dst,
+__global__ void __launch_bounds__(256) iccl_expand_rows(const int4* __restrict__ src, int4* __restrict__ dst,
                                                        const int64_t* __restrict__ pos, int64_t n_src, int k,
                                                        int64_t row16, int parts) {
   const int lane = threadIdx.x & 31;
@@ -944,11 +953,11 @@ cudaError_t launch_expand_rows(const void* src, void* dst, const int64_t* pos, i
   if ((row_bytes & 15) || ((uintptr_t)src & 15) || ((uintptr_t)dst & 15)) return cudaErrorInvalidValue;
   const int64_t row16 = row_bytes / 16;
   const int parts = (int)max((int64_t)1, min((int64_t)8, row16 / 128));  // >= 4 int4 per lane per part
-  if (ctas <= 0) {  // one wave: 5 x 256-thread CTAs per SM (48 registers)
+  if (ctas <= 0) {  // 8 x 256-thread CTAs per SM (62 registers: 4 resident, two waves) measured best
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    ctas = 5 * sms;
+    ctas = 8 * sms;
   }
   iccl_expand_rows<<<rows_grid(n_src * parts, ctas), 256, 0, st>>>((const int4*)src, (int4*)dst, pos, n_src, k,
                                                                    row16, parts);

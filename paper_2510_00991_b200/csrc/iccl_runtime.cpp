@@ -576,6 +576,7 @@ struct iccl_comm {
   ArmedWords* armed_words = nullptr;
   std::vector<uint8_t> armed_used;  // API thread sets, watchdog clears (atomic byte ops)
   uint32_t armed_next = 0;
+  uint32_t armed_seq = 1;  // generations of the K9 decision words
   std::mutex mon_mu;
   std::deque<iccl_mon_rec_t> mon;
   std::deque<iccl_switch_event_t> sw_events;
@@ -2197,6 +2198,9 @@ static iccl_result_t armed_launch(iccl_comm* c, Xfer&& x, int kind, cudaStream_t
   b.probe_src = chn.dir == 0 ? c->scratch : chn.peer_scratch;
   b.probe_dst = chn.dir == 0 ? chn.peer_scratch : c->scratch + 2048 + 16 * chn.peer;
   b.error = c->ll_error;
+  // K9a -> K9b decision word: one per armed slot in GPU memory (after the K6 go words)
+  b.dec_dev = c->ll_counters + 2 * kLLCounters + slot;
+  b.seq = (c->armed_seq++) & 0x3fffffffu;
   b.stamp_base = (uint32_t)(c->next_stamp.fetch_add(x.nchunks) % kStampSlots);
   x.bstamp.assign(x.nchunks, -1);
   for (int k = 0; k < x.nchunks; k++) {
@@ -3085,8 +3089,10 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
     c->event_ready = env_us("ICCL_EVENT_READY", 0) != 0;
     c->k6_vec_bytes = (size_t)env_us("ICCL_K6_VEC_KIB", 0) * 1024;
     c->dispatch_ctas = (int)env_us("ICCL_DISPATCH_CTAS", 0);
-    // kLLCounters arrival counters + kLLCounters K6 go words
-    ICCL_CHECK_CUDA(cudaMalloc((void**)&c->ll_counters, 2 * kLLCounters * sizeof(unsigned int)));
+    // kLLCounters arrival counters + kLLCounters K6 go words + kArmedSlots K9 decision words
+    const size_t nctr = 2 * kLLCounters + kArmedSlots;
+    ICCL_CHECK_CUDA(cudaMalloc((void**)&c->ll_counters, nctr * sizeof(unsigned int)));
+    ICCL_CHECK_CUDA(cudaMemset(c->ll_counters, 0xff, nctr * sizeof(unsigned int)));
     ICCL_CHECK_CUDA(cudaMemset(c->ll_counters, 0, 2 * kLLCounters * sizeof(unsigned int)));
     c->ll_sent.assign(nranks, 0);
     c->ll_recvd.assign(nranks, 0);
