@@ -243,6 +243,7 @@ struct CombineOp {
   int4* out;
   const int64_t* order;  // [n_rows]: out row of packed row r
   int64_t n_rows;
+  int64_t stride;        // visiting order of the rows: r = (i * stride) mod n_rows, gcd(stride, n_rows) = 1
   int32_t n, parts;
   int64_t row16;
   uint32_t go_gen, pad;

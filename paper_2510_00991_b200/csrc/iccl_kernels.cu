@@ -600,7 +600,10 @@ __global__ void __launch_bounds__(256, 5) iccl_combine_pull(const __grid_constan
   const int64_t row16 = op.row16;
   const int64_t span = (row16 + op.parts - 1) / op.parts;
   for (int64_t w = warp; w < op.n_rows * op.parts; w += nwarps) {
-    const int64_t r = w / op.parts;
+    // rows visited in a stride permutation (stride coprime to n_rows): the
+    // warps in flight at any moment pull from every source segment at once,
+    // so the local copy of the self segment overlaps the NVLink loads
+    const int64_t r = (int64_t)(((unsigned long long)(w / op.parts) * op.stride) % (unsigned long long)op.n_rows);
     const int64_t c0 = (w % op.parts) * span, c1 = min(row16, c0 + span);
     const int d = fused_dest_of(s_hi, op.n, r);
     const int4* src = s_seg[d] + (r - s_lo[d]) * row16;

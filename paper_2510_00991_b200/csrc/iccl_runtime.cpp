@@ -3776,6 +3776,12 @@ iccl_result_t iccl_combine_rows(iccl_comm_t c, const void* expert_rows, const si
   op.out = (int4*)out;
   op.order = order;
   op.n_rows = (int64_t)rtot;
+  {  // a stride near n_rows / golden ratio, coprime to n_rows (a bijection of the rows)
+    auto gcd = [](uint64_t a, uint64_t b) { while (b) { uint64_t t = a % b; a = b; b = t; } return a; };
+    uint64_t st = rtot > 2 ? (uint64_t)(rtot * 0.6180339887) | 1 : 1;
+    while (rtot > 1 && gcd(st, rtot) != 1) st += 2;
+    op.stride = (int64_t)st;
+  }
   op.n = n;
   op.row16 = row_bytes / 16;
   op.parts = (int)std::max<int64_t>(1, std::min<int64_t>(8, op.row16 / 128));
