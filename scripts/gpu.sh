@@ -11,6 +11,7 @@
 #   sweep       benchmarks/p2p_sweep.py (2 ranks)
 #   sweeps      p2p_sweep: iccl-auto, nccl, nccl-zero (zero-CTA), nccl-ce; unidirectional and --bidir
 #   gemm        gemm_interference on all GPUs: none, iccl-ce 256 MiB, iccl-auto / nccl at 4 and 16 MiB
+#   gemmk7      gemm_interference iccl-ce 256 MiB with memop waits vs K7 waits (parked streams)
 #   failover    benchmarks/failover.py on all GPUs (sm backup; relay when >= 3 GPUs)
 #   moe         benchmarks/moe_alltoallv.py on all GPUs, iccl and nccl
 #   armedexp    p2p_sweep 1-256 MiB: plain / armed (a never-firing fault script) / armed without the
@@ -64,6 +65,9 @@ for STEP in "$@"; do
           timeout 300 python benchmarks/kernels.py --only k1_local,k1_peer,k2,k3,k8 >> "$LOG" 2>&1 ;;
     var:*) timeout 3000 bash scripts/variants.sh "scripts/variants/${STEP#var:}.txt" >> "$LOG" 2>&1 ;;
     dispatch) timeout 600 $TR --nproc-per-node $NG --master-port 29680 benchmarks/moe_dispatch.py >> "$LOG" 2>&1 ;;
+    gemmk7) for V in "X=0" "ICCL_K7_CE=1" "ICCL_K7_CE=1 ICCL_K7_READY=1" "X=0"; do echo "## $V" >> "$LOG"
+              env $V timeout 600 $TR --nproc-per-node $NG --master-port 29720 benchmarks/gemm_interference.py --impl iccl-ce >> "$LOG" 2>&1
+            done ;;
     failcaps) for C in 16 32 64; do echo "## sm_cap $C" >> "$LOG"
                 ICCL_SM_CAP=$C timeout 600 $TR --nproc-per-node $NG --master-port 2969$((C % 7)) benchmarks/failover.py >> "$LOG" 2>&1
                 ICCL_SM_CAP=$C timeout 600 $TR --nproc-per-node $NG --master-port 2969$((C % 7 + 1)) benchmarks/failover.py --chunk-mib 32 >> "$LOG" 2>&1

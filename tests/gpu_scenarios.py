@@ -451,6 +451,53 @@ def monitor_accuracy(comm, rank, world, nchunks, chunk, stall_chunk, up_us):
     return out
 
 
+def monitor_competing(comm, rank, world, nchunks, chunk, comp_bytes, delay_us):
+    """AC5's smoothing claim ("competing flow halving
+    bandwidth mid-stream ... var(W=1) >= var(W=8) >= var(W=32)") on the
+    product: rank 0 pushes `nchunks` chunks to rank 1, monitor on; `delay_us`
+    after the start rank 2 pushes `comp_bytes` to rank 1 as well, so the two
+    flows share rank 1's ingress for a while.  Rank 1 posts both receives
+    first (on two streams), so the senders push and rank 0 holds the
+    monitored flow's records."""
+    import time
+    dev = dev_of(rank)
+    n = nchunks * chunk
+    src = to_dev(payload(n, seed=6), dev) if rank == 0 else None
+    src2 = to_dev(payload(comp_bytes, seed=7), dev) if rank == 2 else None
+    dst = torch.empty(n, dtype=torch.uint8, device=dev) if rank == 1 else None
+    dst2 = torch.empty(comp_bytes, dtype=torch.uint8, device=dev) if rank == 1 else None
+    sa, sb = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+
+    def round_(tag, delay):
+        if rank == 1:
+            wa = comm.irecv(dst, 0, stream=sa)
+            wb = comm.irecv(dst2, 2, stream=sb)
+            _store_barrier(comm, tag)
+            wa.synchronize()
+            wb.synchronize()
+        else:
+            _store_barrier(comm, tag)
+            if rank == 2:
+                time.sleep(delay * 1e-6)
+            comm.send(src if rank == 0 else src2, 1)
+        torch.cuda.synchronize()
+
+    round_("mc0", 0)          # warm-up: IPC mappings opened
+    time.sleep(0.5)
+    comm.monitor.drain()
+    round_("mc1", delay_us)
+    time.sleep(0.05)
+    out = {}
+    recs = sorted([r for r in comm.monitor.drain() if r.peer == 1], key=lambda r: r.t2)
+    out["t1"] = np.array([r.t1 for r in recs], np.int64)
+    out["t2"] = np.array([r.t2 for r in recs], np.int64)
+    out["bytes"] = np.array([r.size for r in recs], np.int64)
+    if rank == 1:
+        out["ok"] = np.array([bool(torch.equal(dst, to_dev(payload(n, seed=6), dev))) and
+                              bool(torch.equal(dst2, to_dev(payload(comp_bytes, seed=7), dev)))])
+    return out
+
+
 def moe_config4(comm, rank, world, T, k=8, E=64, H=7168, fault=None, keep_bytes=True, fused=False, reps=1,
                 fused_combine=False):
     """BASELINE config 4 at `world` ranks: K2 pack (expand), dispatch
