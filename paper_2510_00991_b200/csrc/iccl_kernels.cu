@@ -640,6 +640,199 @@ __global__ void __launch_bounds__(256, 5) iccl_combine_pull(const __grid_constan
   }
 }
 
+// K2, TMA form: one warp per CTA.  Lane 0 streams each (token, tile) item
+// into a ring of kExpStages shared-memory stages (cp.async.bulk
+// global->shared, mbarrier complete_tx); lanes 0..k-1 then each issue one
+// bulk store of the stage to their packed row (cp.async.bulk shared->global,
+// one bulk group per lane per item).  No register copies at all: the copy
+// engines of the SM (TMA) move the bytes; the pos entries of the next item
+// are loaded one item ahead.  Rows are split into tiles of <= tile bytes
+// (16-byte multiples).
+constexpr int kExpStages = 4;
+__global__ void __launch_bounds__(32) iccl_expand_tma(const char* __restrict__ src, char* __restrict__ dst,
+                                                      const int64_t* __restrict__ pos, int64_t n_src, int k,
+                                                      int64_t row_bytes, int64_t tile, int64_t ntile) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(8) uint64_t mbar[kExpStages];
+  const int lane = threadIdx.x;
+  const int64_t items = n_src * ntile;
+  const int64_t first = blockIdx.x;
+  const int64_t mine = first < items ? (items - first + gridDim.x - 1) / gridDim.x : 0;
+  if (lane == 0) {
+    for (int i = 0; i < kExpStages; i++) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  auto issue_load = [&](int64_t j) {
+    const int64_t it = first + j * gridDim.x, t = it / ntile, off = (it % ntile) * tile;
+    const uint32_t bytes = (uint32_t)min(tile, row_bytes - off);
+    const int st = (int)(j % kExpStages);
+    const uint32_t mb = smem_u32(&mbar[st]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(smem + (size_t)st * tile)),
+        "l"(src + t * row_bytes + off), "r"(bytes), "r"(mb)
+        : "memory");
+  };
+  if (lane == 0)
+    for (int64_t j = 0; j < mine && j < kExpStages; j++) issue_load(j);
+  int64_t p_next = (mine > 0 && lane < k) ? pos[(first / ntile) * k + lane] : 0;
+  for (int64_t j = 0; j < mine; j++) {
+    const int64_t it = first + j * gridDim.x, t = it / ntile, off = (it % ntile) * tile;
+    const uint32_t bytes = (uint32_t)min(tile, row_bytes - off);
+    const int64_t p = p_next;
+    if (j + 1 < mine && lane < k) p_next = pos[((first + (j + 1) * gridDim.x) / ntile) * k + lane];
+    const int st = (int)(j % kExpStages);
+    const uint32_t mb = smem_u32(&mbar[st]);
+    const uint32_t parity = (uint32_t)((j / kExpStages) & 1);
+    uint32_t ready = 0;
+    while (!ready)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(ready)
+          : "r"(mb), "r"(parity)
+          : "memory");
+    if (lane < k) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + p * row_bytes + off),
+                   "r"(smem_u32(smem + (size_t)st * tile)), "r"(bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    if (j + kExpStages < mine) {
+      // the stage is reloaded once every lane's store has read it out of smem
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) issue_load(j + kExpStages);
+    }
+    (void)t;
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// K8, TMA form: K2's TMA ring (iccl_expand_tma) with K8's destinations and
+// handshake: lane 0 of the first CTA to arrive polls every destination's
+// ready flag and releases the others; lanes 0..k-1 resolve their packed
+// row's owner (binary search over the per-rank ranges) and bulk-store the
+// stage straight into that rank's receive buffer (NVLink for a peer); the
+// last CTA releases the done flags after its bulk stores completed.
+__global__ void __launch_bounds__(32) iccl_dispatch_tma(const __grid_constant__ DispatchOp op, int64_t tile,
+                                                        int64_t ntile) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(8) uint64_t mbar[kExpStages];
+  __shared__ int64_t s_lo[kMaxFusedRanks], s_hi[kMaxFusedRanks];
+  __shared__ char* s_seg[kMaxFusedRanks];
+  const int lane = threadIdx.x;
+  for (int d = lane; d < op.n; d += 32) {
+    s_lo[d] = op.d[d].lo;
+    s_hi[d] = op.d[d].hi;
+    s_seg[d] = op.d[d].seg;
+  }
+  if (lane == 0) {
+    const unsigned long long t0 = globaltimer();
+    if (atomicAdd(op.ticket, 1u) == 0) {
+      for (int d = 0; d < op.n; d++) {
+        if (!op.d[d].ready) continue;
+        uint32_t v;
+        do {
+          asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(op.d[d].ready) : "memory");
+          if ((int32_t)(v - op.d[d].ready_gen) < 0 && globaltimer() - t0 > 10000000000ull) {
+            *op.error = 1;
+            break;
+          }
+        } while ((int32_t)(v - op.d[d].ready_gen) < 0);
+      }
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(op.go), "r"(op.go_gen) : "memory");
+      if (op.stamp) {
+        const unsigned long long t = globaltimer();
+        asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(&op.stamp->t1), "l"(t) : "memory");
+      }
+    } else {
+      uint32_t v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(op.go) : "memory");
+        if (v != op.go_gen && globaltimer() - t0 > 10000000000ull) {
+          *op.error = 1;
+          break;
+        }
+      } while (v != op.go_gen);
+    }
+    for (int i = 0; i < kExpStages; i++) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const char* src = (const char*)op.tokens;
+  const int64_t row_bytes = op.row16 * 16;
+  const int64_t items = op.n_tokens * ntile;
+  const int64_t first = blockIdx.x;
+  const int64_t mine = first < items ? (items - first + gridDim.x - 1) / gridDim.x : 0;
+  auto issue_load = [&](int64_t j) {
+    const int64_t it = first + j * gridDim.x, t = it / ntile, off = (it % ntile) * tile;
+    const uint32_t bytes = (uint32_t)min(tile, row_bytes - off);
+    const int st = (int)(j % kExpStages);
+    const uint32_t mb = smem_u32(&mbar[st]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(smem + (size_t)st * tile)),
+        "l"(src + t * row_bytes + off), "r"(bytes), "r"(mb)
+        : "memory");
+  };
+  if (lane == 0)
+    for (int64_t j = 0; j < mine && j < kExpStages; j++) issue_load(j);
+  int64_t p_next = (mine > 0 && lane < op.k) ? op.pos[(first / ntile) * op.k + lane] : 0;
+  for (int64_t j = 0; j < mine; j++) {
+    const int64_t it = first + j * gridDim.x, off = (it % ntile) * tile;
+    const uint32_t bytes = (uint32_t)min(tile, row_bytes - off);
+    const int64_t p = p_next;
+    if (j + 1 < mine && lane < op.k) p_next = op.pos[((first + (j + 1) * gridDim.x) / ntile) * op.k + lane];
+    const int st = (int)(j % kExpStages);
+    const uint32_t mb = smem_u32(&mbar[st]);
+    const uint32_t parity = (uint32_t)((j / kExpStages) & 1);
+    uint32_t ready = 0;
+    while (!ready)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(ready)
+          : "r"(mb), "r"(parity)
+          : "memory");
+    if (lane < op.k) {
+      const int d = fused_dest_of(s_hi, op.n, p);
+      char* dp = s_seg[d] + (p - s_lo[d]) * row_bytes + off;
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dp),
+                   "r"(smem_u32(smem + (size_t)st * tile)), "r"(bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    if (j + kExpStages < mine) {
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) issue_load(j + kExpStages);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // this lane's stores performed
+  __threadfence_system();
+  __syncwarp();
+  if (lane == 0) {
+    if (atomicAdd(op.counter, 1u) == gridDim.x - 1) {
+      atomicExch(op.counter, 0u);
+      atomicExch(op.ticket, 0u);
+      __threadfence_system();
+      if (op.stamp) {
+        const unsigned long long t = globaltimer();
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&op.stamp->t2), "l"(t) : "memory");
+      }
+      for (int d = 0; d < op.n; d++) {
+        if (op.d[d].done)
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(op.d[d].done), "r"(op.d[d].done_gen) : "memory");
+        if (op.d[d].my_done)
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(op.d[d].my_done), "r"(op.d[d].my_done_gen)
+                       : "memory");
+      }
+    }
+  }
+}
+
 // K3: inverse permutation (combine unpack), dst row idx[r] <- src row r.
 __global__ void __launch_bounds__(256) iccl_scatter_rows(const int4* __restrict__ src, int4* __restrict__ dst,
                                                         const int64_t* __restrict__ idx, int64_t n_rows,
@@ -882,7 +1075,8 @@ cudaError_t preload_kernels() {
                        (const void*)iccl_scatter_rows, (const void*)iccl_expand_rows,
                        (const void*)iccl_ll_group, (const void*)iccl_wait_flags, (const void*)iccl_dispatch_push,
                        (const void*)iccl_backup_attempt, (const void*)iccl_backup_ctl,
-                       (const void*)iccl_combine_pull};
+                       (const void*)iccl_combine_pull, (const void*)iccl_expand_tma,
+                       (const void*)iccl_dispatch_tma};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;
@@ -924,6 +1118,26 @@ cudaError_t launch_dispatch(const DispatchOp& op, int ctas, cudaStream_t st, int
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
+  static const bool tma = getenv("ICCL_K8_TMA") ? atoi(getenv("ICCL_K8_TMA")) != 0 : true;
+  if (tma) {
+    const int64_t row_bytes = op.row16 * 16;
+    const int64_t ntile = (row_bytes + 32768 - 1) / 32768;
+    const int64_t tile = ((row_bytes + ntile - 1) / ntile + 15) / 16 * 16;
+    const int smem = (int)(kExpStages * tile);
+    static bool configured = false;
+    if (!configured) {
+      cudaError_t e = cudaFuncSetAttribute(iccl_dispatch_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 32768);
+      if (e != cudaSuccess) return e;
+      configured = true;
+    }
+    const int per_sm = (int)max((int64_t)1, min((int64_t)8, (int64_t)(200 * 1024) / (smem + 2048)));
+    int64_t grid = ctas > 0 ? ctas : (int64_t)per_sm * sms;
+    if (grid > op.n_tokens * ntile) grid = op.n_tokens * ntile;
+    if (grid < 1) grid = 1;
+    if (grid_out) *grid_out = (int)grid;
+    iccl_dispatch_tma<<<(int)grid, 32, smem, st>>>(op, tile, ntile);
+    return cudaGetLastError();
+  }
   const int64_t warps = op.n_tokens * op.parts;
   int64_t grid = (warps + 7) / 8;
   const int64_t cap = ctas > 0 ? ctas : 5 * (int64_t)sms;  // one wave: 5 x 256-thread CTAs per SM (48 registers)
@@ -954,6 +1168,28 @@ cudaError_t launch_expand_rows(const void* src, void* dst, const int64_t* pos, i
                                int64_t row_bytes, int ctas, cudaStream_t st) {
   if (n_src == 0 || k == 0) return cudaSuccess;
   if ((row_bytes & 15) || ((uintptr_t)src & 15) || ((uintptr_t)dst & 15)) return cudaErrorInvalidValue;
+  static const bool tma = getenv("ICCL_K2_TMA") ? atoi(getenv("ICCL_K2_TMA")) != 0 : true;
+  if (tma && k <= 32) {
+    // TMA form: tiles of <= 32 KB, kExpStages stages per one-warp CTA
+    const int64_t ntile = (row_bytes + 32768 - 1) / 32768;
+    const int64_t tile = ((row_bytes + ntile - 1) / ntile + 15) / 16 * 16;
+    const int smem = (int)(kExpStages * tile);
+    static int configured = 0;
+    if (configured < smem) {
+      cudaError_t e = cudaFuncSetAttribute(iccl_expand_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 32768);
+      if (e != cudaSuccess) return e;
+      configured = 4 * 32768;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int per_sm = (int)max((int64_t)1, min((int64_t)8, (int64_t)(220 * 1024) / (smem + 1024)));
+    int64_t grid = ctas > 0 ? ctas : (int64_t)per_sm * sms;
+    if (grid > n_src * ntile) grid = n_src * ntile;
+    iccl_expand_tma<<<(int)grid, 32, smem, st>>>((const char*)src, (char*)dst, pos, n_src, k, row_bytes, tile,
+                                                 ntile);
+    return cudaGetLastError();
+  }
   const int64_t row16 = row_bytes / 16;
   const int parts = (int)max((int64_t)1, min((int64_t)8, row16 / 128));  // >= 4 int4 per lane per part
   if (ctas <= 0) {  // 8 x 256-thread CTAs per SM (62 registers: 4 resident, two waves) measured best
