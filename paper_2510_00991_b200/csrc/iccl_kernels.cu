@@ -833,6 +833,127 @@ __global__ void __launch_bounds__(32) iccl_dispatch_tma(const __grid_constant__ 
   }
 }
 
+// K10, TMA form: lane 0 of each one-warp CTA bulk-loads (row, tile) items
+// straight from the source rank's tensor (NVLink for a peer) into a ring of
+// shared-memory stages and bulk-stores each to its out row; rows are visited
+// in K10's coprime-stride order.  Same handshake as K10.
+__global__ void __launch_bounds__(32) iccl_combine_tma(const __grid_constant__ CombineOp op, int64_t tile,
+                                                       int64_t ntile) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(8) uint64_t mbar[kExpStages];
+  __shared__ int64_t s_lo[kMaxFusedRanks], s_hi[kMaxFusedRanks];
+  __shared__ const char* s_seg[kMaxFusedRanks];
+  const int lane = threadIdx.x;
+  for (int d = lane; d < op.n; d += 32) {
+    s_lo[d] = op.d[d].lo;
+    s_hi[d] = op.d[d].hi;
+    s_seg[d] = op.d[d].seg;
+  }
+  if (lane == 0) {
+    const unsigned long long t0 = globaltimer();
+    if (atomicAdd(op.ticket, 1u) == 0) {
+      for (int d = 0; d < op.n; d++) {
+        if (!op.d[d].ready) continue;
+        uint32_t v;
+        do {
+          asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(op.d[d].ready) : "memory");
+          if ((int32_t)(v - op.d[d].ready_gen) < 0 && globaltimer() - t0 > 10000000000ull) {
+            *op.error = 1;
+            break;
+          }
+        } while ((int32_t)(v - op.d[d].ready_gen) < 0);
+      }
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(op.go), "r"(op.go_gen) : "memory");
+      if (op.stamp) {
+        const unsigned long long t = globaltimer();
+        asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(&op.stamp->t1), "l"(t) : "memory");
+      }
+    } else {
+      uint32_t v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(op.go) : "memory");
+        if (v != op.go_gen && globaltimer() - t0 > 10000000000ull) {
+          *op.error = 1;
+          break;
+        }
+      } while (v != op.go_gen);
+    }
+    for (int i = 0; i < kExpStages; i++) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  if (lane == 0) {
+    const int64_t row_bytes = op.row16 * 16;
+    const int64_t items = op.n_rows * ntile;
+    const int64_t first = blockIdx.x;
+    const int64_t mine = first < items ? (items - first + gridDim.x - 1) / gridDim.x : 0;
+    auto item = [&](int64_t j, int64_t* r, int64_t* off) {
+      const int64_t it = first + j * gridDim.x;
+      *r = (int64_t)(((unsigned long long)(it / ntile) * op.stride) % (unsigned long long)op.n_rows);
+      *off = (it % ntile) * tile;
+    };
+    int64_t orow_ring[kExpStages];  // out rows of the items in flight (loaded with the tile: latency hidden)
+    auto issue_load = [&](int64_t j) {
+      int64_t r, off;
+      item(j, &r, &off);
+      orow_ring[j % kExpStages] = op.order[r];
+      const int d = fused_dest_of(s_hi, op.n, r);
+      const uint32_t bytes = (uint32_t)min(tile, row_bytes - off);
+      const int st = (int)(j % kExpStages);
+      const uint32_t mb = smem_u32(&mbar[st]);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(smem + (size_t)st * tile)),
+          "l"(s_seg[d] + (r - s_lo[d]) * row_bytes + off), "r"(bytes), "r"(mb)
+          : "memory");
+    };
+    for (int64_t j = 0; j < mine && j < kExpStages; j++) issue_load(j);
+    for (int64_t j = 0; j < mine; j++) {
+      int64_t r, off;
+      item(j, &r, &off);
+      const int64_t orow = orow_ring[j % kExpStages];
+      const uint32_t bytes = (uint32_t)min(tile, row_bytes - off);
+      const int st = (int)(j % kExpStages);
+      const uint32_t mb = smem_u32(&mbar[st]);
+      const uint32_t parity = (uint32_t)((j / kExpStages) & 1);
+      uint32_t ready = 0;
+      while (!ready)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(ready)
+            : "r"(mb), "r"(parity)
+            : "memory");
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"((char*)op.out + orow * row_bytes + off),
+                   "r"(smem_u32(smem + (size_t)st * tile)), "r"(bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      if (j + kExpStages < mine) {
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        issue_load(j + kExpStages);
+      }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __threadfence_system();
+    if (atomicAdd(op.counter, 1u) == gridDim.x - 1) {
+      atomicExch(op.counter, 0u);
+      atomicExch(op.ticket, 0u);
+      __threadfence_system();
+      if (op.stamp) {
+        const unsigned long long t = globaltimer();
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&op.stamp->t2), "l"(t) : "memory");
+      }
+      for (int d = 0; d < op.n; d++) {
+        if (op.d[d].done)
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(op.d[d].done), "r"(op.d[d].done_gen) : "memory");
+        if (op.d[d].my_done)
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(op.d[d].my_done), "r"(op.d[d].my_done_gen)
+                       : "memory");
+      }
+    }
+  }
+}
+
 // K3: inverse permutation (combine unpack), dst row idx[r] <- src row r.
 __global__ void __launch_bounds__(256) iccl_scatter_rows(const int4* __restrict__ src, int4* __restrict__ dst,
                                                         const int64_t* __restrict__ idx, int64_t n_rows,
@@ -1076,7 +1197,7 @@ cudaError_t preload_kernels() {
                        (const void*)iccl_ll_group, (const void*)iccl_wait_flags, (const void*)iccl_dispatch_push,
                        (const void*)iccl_backup_attempt, (const void*)iccl_backup_ctl,
                        (const void*)iccl_combine_pull, (const void*)iccl_expand_tma,
-                       (const void*)iccl_dispatch_tma};
+                       (const void*)iccl_dispatch_tma, (const void*)iccl_combine_tma};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;
@@ -1155,6 +1276,26 @@ cudaError_t launch_combine(const CombineOp& op, int ctas, cudaStream_t st, int* 
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static const bool tma = getenv("ICCL_K10_TMA") ? atoi(getenv("ICCL_K10_TMA")) != 0 : true;
+  if (tma) {
+    const int64_t row_bytes = op.row16 * 16;
+    const int64_t ntile = (row_bytes + 32768 - 1) / 32768;
+    const int64_t tile = ((row_bytes + ntile - 1) / ntile + 15) / 16 * 16;
+    const int smem = (int)(kExpStages * tile);
+    static bool configured = false;
+    if (!configured) {
+      cudaError_t e = cudaFuncSetAttribute(iccl_combine_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 32768);
+      if (e != cudaSuccess) return e;
+      configured = true;
+    }
+    const int per_sm = (int)max((int64_t)1, min((int64_t)8, (int64_t)(200 * 1024) / (smem + 2048)));
+    int64_t grid = ctas > 0 ? ctas : (int64_t)per_sm * sms;
+    if (grid > op.n_rows * ntile) grid = op.n_rows * ntile;
+    if (grid < 1) grid = 1;
+    if (grid_out) *grid_out = (int)grid;
+    iccl_combine_tma<<<(int)grid, 32, smem, st>>>(op, tile, ntile);
+    return cudaGetLastError();
+  }
   int64_t grid = (op.n_rows * op.parts + 7) / 8;
   const int64_t cap = ctas > 0 ? ctas : 5 * (int64_t)sms;
   if (grid > cap) grid = cap;
