@@ -1239,7 +1239,7 @@ cudaError_t launch_dispatch(const DispatchOp& op, int ctas, cudaStream_t st, int
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
-  static const bool tma = getenv("ICCL_K8_TMA") ? atoi(getenv("ICCL_K8_TMA")) != 0 : true;
+  static const bool tma = getenv("ICCL_K8_TMA") ? atoi(getenv("ICCL_K8_TMA")) != 0 : false;  // measured no faster (profiles/r02 §5)
   if (tma) {
     const int64_t row_bytes = op.row16 * 16;
     const int64_t ntile = (row_bytes + 32768 - 1) / 32768;
@@ -1309,7 +1309,7 @@ cudaError_t launch_expand_rows(const void* src, void* dst, const int64_t* pos, i
                                int64_t row_bytes, int ctas, cudaStream_t st) {
   if (n_src == 0 || k == 0) return cudaSuccess;
   if ((row_bytes & 15) || ((uintptr_t)src & 15) || ((uintptr_t)dst & 15)) return cudaErrorInvalidValue;
-  static const bool tma = getenv("ICCL_K2_TMA") ? atoi(getenv("ICCL_K2_TMA")) != 0 : true;
+  static const bool tma = getenv("ICCL_K2_TMA") ? atoi(getenv("ICCL_K2_TMA")) != 0 : false;  // measured slower (profiles/r02 §5)
   if (tma && k <= 32) {
     // TMA form: tiles of <= 32 KB, kExpStages stages per one-warp CTA
     const int64_t ntile = (row_bytes + 32768 - 1) / 32768;
