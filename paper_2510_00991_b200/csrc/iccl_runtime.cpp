@@ -2299,6 +2299,8 @@ static bool armed_progress(iccl_comm* c, Channel& chn) {
         x.completed++;
       }
       if (m > 0) {
+        ICCL_TRACE("armed pair %d->%d: primary chunks %d..%d landed (+%.1f us since the last observation)", chn.src,
+                   chn.dst, x.completed - m, x.completed - 1, (tnow - x.t_obs) * 1e-3);
         x.t_obs = tnow;
         x.last_progress = tnow;
         busy = true;
@@ -2366,9 +2368,11 @@ static bool armed_progress(iccl_comm* c, Channel& chn) {
     const bool elig = cyc_geq(flags_of(c, x.src_rank)->ready[x.s_slot], x.s_gen) &&
                       cyc_geq(flags_of(c, x.dst_rank)->ready[x.r_ready_slot], x.r_ready_gen);
     if (!elig) {
+      if (x.eligible) ICCL_TRACE("armed pair %d->%d: ready flags not both set", chn.src, chn.dst);
       x.last_progress = tnow;  // innocent stall upstream: a side's stream has not reached the op
       x.t_obs = tnow;
     } else if (!x.eligible) {
+      ICCL_TRACE("armed pair %d->%d: both ready flags set", chn.src, chn.dst);
       x.eligible = true;
       x.last_progress = tnow;
       x.t_obs = tnow;

@@ -19,6 +19,12 @@ def main():
             res = run_ranks(2, sc.monitor_accuracy, d, nchunks=128, chunk=16 * MiB, stall_chunk=64, up_us=20_000,
                             config=dict(chunk_bytes=16 * MiB, monitor_enabled=True, delta_us=200_000, window=1024))
             print("switches", [r["switches"] for r in res], [r["switch_desc"] for r in res])
+            for r in res:
+                if len(r["t2"]):
+                    import numpy as np
+                    d = r["t2"] - r["t1"]
+                    print("records", len(d), "dur min/med/max ns", d.min(), int(np.median(d)), d.max(),
+                          "span us", (r["t2"][-1] - r["t1"][0]) / 1e3)
         finally:
             for r in range(2):
                 p = os.path.join(d, f"rank{r}.log")
@@ -26,7 +32,7 @@ def main():
                     lines = open(p).read().splitlines()
                     print(f"---- rank {r}: {len(lines)} lines")
                     keep = [ln for ln in lines if "fault" in ln or "gate" in ln or "switch" in ln or "issue" in ln
-                            or "posted" in ln or "Error" in ln]
+                            or "posted" in ln or "Error" in ln or "armed pair" in ln]
                     print("\n".join(keep[:200]))
 
 
