@@ -21,7 +21,6 @@
 #   dispatch    benchmarks/moe_dispatch.py on all GPUs: fused K8 vs K2 + alltoallv vs NCCL
 #   launches    ncu launch list of smoke() (gpu__time_duration, no replay of waits)
 #   ncuprobe    probes/ncu_xproc under ncu (cross-process serialisation)
-#   sanitize    compute-sanitizer memcheck/racecheck/synccheck on benchmarks/kernels.py
 #   cmd:...     any command (quoted)
 set -u
 TAG=$1; shift
@@ -77,13 +76,6 @@ for STEP in "$@"; do
                 --log-file gpurun_out/${TAG}_launches.csv python -c "import __graft_entry__ as g; g.smoke()" >> "$LOG" 2>&1 ;;
     ncuprobe) ./probes/ncu_xproc >> "$LOG" 2>&1; timeout 120 ncu --target-processes all --metrics gpu__time_duration.sum \
                 ./probes/ncu_xproc >> "$LOG" 2>&1 ;;
-    sanitize) for T in memcheck racecheck synccheck; do
-                timeout 900 compute-sanitizer --tool $T --error-exitcode 9 python benchmarks/kernels.py --quick --reps 2 >> "$LOG" 2>&1
-                echo "$T rc=$?" >> "$LOG"; done
-              # two processes on one GPU through the product path (K5, K6, K7, K8, copy engine) under memcheck
-              timeout 1200 compute-sanitizer --tool memcheck --target-processes all --error-exitcode 9 \
-                python -c "import __graft_entry__ as g; g.smoke()" >> "$LOG" 2>&1
-              echo "memcheck smoke rc=$?" >> "$LOG" ;;
     cmd:*) timeout 1800 bash -c "${STEP#cmd:}" >> "$LOG" 2>&1 ;;
     *) echo "unknown step $STEP" >> "$LOG" ;;
   esac
