@@ -84,7 +84,9 @@ struct alignas(64) ArmedWords {
   uint32_t b_fin;       // the backup attempt drained
   uint32_t fin;         // the primary passed its done writes (the slot may be reused)
   uint32_t dec;         // K9's decision (ArmedDec), which its CTAs follow
-  uint32_t pad[6];
+  uint32_t pgate;       // 1 + the gate word the primary waits on (its path is Down), or 0: the probe is lost while it is closed
+  uint32_t bgate;       // 1 + the gate word of a Down backup path, or 0
+  uint32_t pad[4];
 };
 // K9: the backup attempt of an armed transfer, one launch per transfer,
 // started once `go` opens.  CTA 0 decides: the primary finished with no
@@ -99,8 +101,7 @@ struct BackupOp {
   uint32_t nchunks, ring_slots, stamp_base, pad;
   KernelStamp* ring;
   ArmedWords* w;
-  const uint32_t* gate;    // the primary path's fault gate word when the transfer was issued behind it, or null
-  const uint32_t* bgate;   // the backup path's fault gate word (a Down backup path), or null
+  const uint32_t* gates;   // the gate words (w->pgate / w->bgate index them)
   const char* probe_src;   // 16 bytes moved by the probe (over the primary path's direction)
   char* probe_dst;
   unsigned int* error;     // host-mapped: set if the decision wait exceeds 60 s

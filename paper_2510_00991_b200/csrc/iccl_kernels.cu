@@ -190,6 +190,12 @@ __device__ __forceinline__ void st_sys(uint32_t* p, uint32_t v) {
 // kernel rather than parking the stream on a stream-memory wait (a parked
 // stream was measured to cost every other stream of the GPU ~50 us per op),
 // then decides.  Polls back off with __nanosleep.
+// The primary path can carry the CTS: not Down, or its gate open again.
+__device__ __forceinline__ bool probe_path_open(const BackupOp& op) {
+  const uint32_t g = ld_sys(&op.w->pgate);
+  return g == 0 || ld_sys(op.gates + g - 1) != 0;
+}
+
 __global__ void __launch_bounds__(32) iccl_backup_ctl(const __grid_constant__ BackupOp op) {
   if (threadIdx.x != 0) return;
   ArmedWords* w = op.w;
@@ -205,7 +211,7 @@ __global__ void __launch_bounds__(32) iccl_backup_ctl(const __grid_constant__ Ba
       dec = kDecExit;
     } else if (ld_sys(&w->p_fin)) {
       dec = ld_sys(&w->ctl) == kCtlSwitch ? kDecCopy : kDecExit;  // a switch racing the primary's end still copies
-    } else if (ctl == kCtlProbe && !probed && (!op.gate || ld_sys(op.gate) != 0)) {
+    } else if (ctl == kCtlProbe && !probed && probe_path_open(op)) {
       // the CTS crosses the primary path: lost while its gate is closed
       int4 v;
       asm volatile("ld.volatile.global.v4.s32 {%0,%1,%2,%3}, [%4];"
@@ -219,8 +225,9 @@ __global__ void __launch_bounds__(32) iccl_backup_ctl(const __grid_constant__ Ba
       __nanosleep(256);
     }
   }
-  if (dec == kDecCopy && op.bgate) {  // the backup path itself is Down: wait for it (or the abort)
-    while (ld_sys(op.bgate) == 0 && ld_sys(&w->ctl) != kCtlAbort) __nanosleep(256);
+  const uint32_t bg = ld_sys(&w->bgate);
+  if (dec == kDecCopy && bg) {  // the backup path itself is Down: wait for it (or the abort)
+    while (ld_sys(op.gates + bg - 1) == 0 && ld_sys(&w->ctl) != kCtlAbort) __nanosleep(256);
     if (ld_sys(&w->ctl) == kCtlAbort) dec = kDecExit;
   }
   (void)t0;

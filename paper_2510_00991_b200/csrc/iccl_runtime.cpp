@@ -2096,128 +2096,98 @@ static iccl_result_t armed_launch(iccl_comm* c, Xfer&& x, int kind, cudaStream_t
   std::atomic_thread_fence(std::memory_order_seq_cst);
   x.armed = true;
   x.aw = slot;
-  // primary attempt
   const int eng = path_engine(c, chn, 0, x.bytes);
   cudaStream_t ps = instream ? us : c->streams[stream_for(c, chn, 0, ENG_CE, 0)].s;
-  std::vector<CUstreamBatchMemOpParams> p;
+  {
+    std::lock_guard<std::mutex> g(c->fault_mu);  // a path already Down: the probe / the backup wait on its gate
+    w->pgate = chn.fault[0].down ? (uint32_t)chn.fault[0].gate + 1 : 0;
+    w->bgate = chn.fault[1].down ? (uint32_t)chn.fault[1].gate + 1 : 0;
+  }
   iccl_result_t r;
+  // backup attempt first (its controller waits for `go` in-kernel), then the
+  // transfer goes to the watchdog, then the primary is enqueued from local
+  // state: an enqueue behind a closed gate can block once the stream's
+  // command queue is full, and the watchdog must already be watching then
+  // (it opens the gate when it switches)
+  if (c->armed_backup) {
+    ICCL_RETURN_IF((((uintptr_t)x.src ^ (uintptr_t)x.dst) & 15) != 0, ICCL_ERR_INVALID_ARGUMENT,
+                   "armed transfer between tensors of different alignment mod 16");
+    cudaStream_t bs = nullptr;
+    r = backup_stream(c, chn, &bs);
+    if (r) return r;
+    BackupOp b{};
+    b.src = x.src;
+    b.dst = x.dst;
+    b.bytes = x.bytes;
+    b.chunk = x.chunk;
+    b.nchunks = (uint32_t)x.nchunks;
+    b.ring = c->stamps;
+    b.ring_slots = kStampSlots;
+    b.w = w;
+    b.gates = (const uint32_t*)c->gate_words;
+    // the CTS probe (16 B) crosses the primary path in its direction: into the
+    // peer's scratch (push) or out of it (pull)
+    b.probe_src = chn.dir == 0 ? c->scratch : chn.peer_scratch;
+    b.probe_dst = chn.dir == 0 ? chn.peer_scratch : c->scratch + 2048 + 16 * chn.peer;
+    b.error = c->ll_error;
+    // K9a -> K9b decision word: one per armed slot in GPU memory (after the K6 go words)
+    b.dec_dev = c->ll_counters + 2 * kLLCounters + slot;
+    b.seq = (c->armed_seq++) & 0x3fffffffu;
+    b.stamp_base = (uint32_t)(c->next_stamp.fetch_add(x.nchunks) % kStampSlots);
+    x.bstamp.assign(x.nchunks, -1);
+    for (int k = 0; k < x.nchunks; k++) {
+      x.bstamp[k] = (int)((b.stamp_base + k) % kStampSlots);
+      memset((void*)&c->stamps[x.bstamp[k]], 0, sizeof(KernelStamp));
+    }
+    int grid = 0;
+    if (c->k9_mode == 0) ICCL_CHECK_CUDA(launch_backup(b, c->cfg.sm_cap, bs, &grid));
+    if (c->k9_mode == 1) ICCL_CHECK_CUDA(launch_backup(b, 0, bs, &grid));  // K9a only
+    if (c->k9_mode == 3) ICCL_CHECK_CUDA(launch_backup(b, -1, bs, &grid));  // K9b without shared memory
+    if (c->k9_mode == 4) ICCL_CHECK_CUDA(launch_backup(b, -2, bs, &grid));  // one-CTA K9b
+    c->kernels_launched += 1;
+    c->ctas_launched += grid;
+    r = memop_write(bs, &w->b_fin, 1);
+    if (r) return r;
+  } else {  // attribution runs only: no failover possible
+    x.bstamp.assign(x.nchunks, -1);
+    __atomic_store_n(&w->b_fin, 1u, __ATOMIC_SEQ_CST);
+  }
+  // everything the primary's enqueue needs, copied out of x before handing it over
+  cudaStream_t pstr = nullptr;
+  if (c->prog_events) {
+    r = prog_stream(c, chn, &pstr);
+    if (r) return r;
+    for (int k = 0; k < x.nchunks; k++)
+      if (!x.rec[k].ev) x.rec[k].ev = get_event(c);  // returned to the pool when the watchdog retires x
+  }
+  std::vector<cudaEvent_t> evs;
+  for (const ChunkRec& rc : x.rec) evs.push_back(rc.ev);
+  std::vector<CUstreamBatchMemOpParams> p, fin;
   if (instream) {
     // this side's ready flag too (the watchdog tells an upstream stall of
     // either side by the two flags), then the wait on the other side's
     p.push_back(kind == 0 ? wparam(&flags_of(c, x.src_rank)->ready[x.s_slot], x.s_gen)
                           : wparam(&flags_of(c, x.dst_rank)->ready[x.r_ready_slot], x.r_ready_gen));
     instream_ready_param(c, x, kind, p);
-    r = batch_memops(ps, p);
-  } else {
-    r = wait_both_ready(c, ps, x);
   }
-  if (r) return r;
-  cudaStream_t pstr = nullptr;
-  if (c->prog_events) {
-    r = prog_stream(c, chn, &pstr);
-    if (r) return r;
-  }
-  for (int k = 0; k < x.nchunks; k++) {
-    const size_t off = (size_t)k * x.chunk, n = std::min(x.chunk, x.bytes - off);
-    {
-      std::lock_guard<std::mutex> g(c->fault_mu);
-      if (x.fault_ops_index >= 0) fire_chunk_faults(c, chn, x.fault_ops_index, k, 0);
-      if (chn.fault[0].down) {
-        r = memop_wait(ps, &c->gate_words[chn.fault[0].gate], 1);
-        if (r) return r;
-        x.gated = true;
-      }
-    }
-    x.rec[k].t1 = now_ns();
-    x.rec[k].path = 0;
-    if (eng == ENG_SM) {
-      int grid = 0;
-      ICCL_CHECK_CUDA(launch_copy(x.src + off, x.dst + off, n, c->cfg.sm_cap, nullptr, ps, &grid));
-      c->kernels_launched += 1;
-      c->ctas_launched += grid;
-    } else {
-      ICCL_CHECK_CU(driver()->cuMemcpyDtoDAsync((CUdeviceptr)(x.dst + off), (CUdeviceptr)(x.src + off), n,
-                                                (CUstream)ps));
-    }
-    c->copies_issued += 1;
-    c->bytes_issued += n;
-    if (c->prog_events) {
-      if (!x.rec[k].ev) x.rec[k].ev = get_event(c);
-      ICCL_CHECK_CUDA(cudaEventRecord(x.rec[k].ev, ps));
-      ICCL_CHECK_CUDA(cudaStreamWaitEvent(pstr, x.rec[k].ev, 0));
-      r = memop_write(pstr, &w->prog, (uint32_t)(k + 1));
-    } else {
-      r = memop_write(ps, &w->prog, (uint32_t)(k + 1));
-    }
-    if (r) return r;
-  }
-  p.push_back(wparam(&w->p_fin, 1));
-  p.push_back(wparam(&w->go, 1));
-  r = batch_memops(ps, p);
-  if (r) return r;
-  r = memop_wait(ps, &w->ns, 1);
-  if (r) return r;
-  instream_done_params(c, x, p);
-  p.push_back(wparam(&w->fin, 1));
-  r = batch_memops(ps, p);
-  if (r) return r;
+  instream_done_params(c, x, fin);
+  fin.push_back(wparam(&w->fin, 1));
+  const int nchunks = x.nchunks, fault_ops_index = x.fault_ops_index;
+  const size_t chunk = x.chunk, bytes = x.bytes;
+  const char* src = x.src;
+  char* dst = x.dst;
+  Xfer ready_x;  // wait_both_ready reads the flag slots only
+  ready_x.src_rank = x.src_rank;
+  ready_x.dst_rank = x.dst_rank;
+  ready_x.s_slot = x.s_slot;
+  ready_x.s_gen = x.s_gen;
+  ready_x.r_ready_slot = x.r_ready_slot;
+  ready_x.r_ready_gen = x.r_ready_gen;
+  ready_x.own_ready = x.own_ready;
+  ready_x.own_side = x.own_side;
   x.next_issue = x.nchunks;
   x.instream = instream;
   x.ustream = instream ? us : nullptr;
-  // backup attempt
-  if (!c->armed_backup) {  // attribution runs only: no failover possible
-    x.bstamp.assign(x.nchunks, -1);
-    __atomic_store_n(&w->b_fin, 1u, __ATOMIC_SEQ_CST);
-    x.done_enqueued = true;
-    x.t_obs = now_ns();
-    publish(c, x);
-    c->pending_xfers.fetch_add(1);
-    std::lock_guard<std::mutex> g(c->amu);
-    c->ahandoff.push_back(std::move(x));
-    return ICCL_SUCCESS;
-  }
-  cudaStream_t bs = nullptr;
-  r = backup_stream(c, chn, &bs);
-  if (r) return r;
-  BackupOp b{};
-  b.src = x.src;
-  b.dst = x.dst;
-  b.bytes = x.bytes;
-  b.chunk = x.chunk;
-  b.nchunks = (uint32_t)x.nchunks;
-  b.ring = c->stamps;
-  b.ring_slots = kStampSlots;
-  b.w = w;
-  {
-    std::lock_guard<std::mutex> g(c->fault_mu);
-    b.gate = chn.fault[0].down ? (const uint32_t*)&c->gate_words[chn.fault[0].gate] : nullptr;
-    b.bgate = chn.fault[1].down ? (const uint32_t*)&c->gate_words[chn.fault[1].gate] : nullptr;
-  }
-  // the CTS probe (16 B) crosses the primary path in its direction: into the
-  // peer's scratch (push) or out of it (pull)
-  b.probe_src = chn.dir == 0 ? c->scratch : chn.peer_scratch;
-  b.probe_dst = chn.dir == 0 ? chn.peer_scratch : c->scratch + 2048 + 16 * chn.peer;
-  b.error = c->ll_error;
-  // K9a -> K9b decision word: one per armed slot in GPU memory (after the K6 go words)
-  b.dec_dev = c->ll_counters + 2 * kLLCounters + slot;
-  b.seq = (c->armed_seq++) & 0x3fffffffu;
-  b.stamp_base = (uint32_t)(c->next_stamp.fetch_add(x.nchunks) % kStampSlots);
-  x.bstamp.assign(x.nchunks, -1);
-  for (int k = 0; k < x.nchunks; k++) {
-    x.bstamp[k] = (int)((b.stamp_base + k) % kStampSlots);
-    memset((void*)&c->stamps[x.bstamp[k]], 0, sizeof(KernelStamp));
-  }
-  ICCL_RETURN_IF((((uintptr_t)x.src ^ (uintptr_t)x.dst) & 15) != 0, ICCL_ERR_INVALID_ARGUMENT,
-                 "armed transfer between tensors of different alignment mod 16");
-  int grid = 0;
-  if (c->k9_mode == 0) ICCL_CHECK_CUDA(launch_backup(b, c->cfg.sm_cap, bs, &grid));
-  if (c->k9_mode == 1) ICCL_CHECK_CUDA(launch_backup(b, 0, bs, &grid));  // K9a only
-  if (c->k9_mode == 3) ICCL_CHECK_CUDA(launch_backup(b, -1, bs, &grid));  // K9b without shared memory
-  if (c->k9_mode == 4) ICCL_CHECK_CUDA(launch_backup(b, -2, bs, &grid));  // one-CTA K9b
-  c->kernels_launched += 1;
-  c->ctas_launched += grid;
-  r = memop_write(bs, &w->b_fin, 1);
-  if (r) return r;
   x.done_enqueued = true;
   x.t_obs = now_ns();
   publish(c, x);
@@ -2226,7 +2196,54 @@ static iccl_result_t armed_launch(iccl_comm* c, Xfer&& x, int kind, cudaStream_t
     std::lock_guard<std::mutex> g(c->amu);
     c->ahandoff.push_back(std::move(x));
   }
-  return ICCL_SUCCESS;
+  // primary attempt
+  r = instream ? batch_memops(ps, p) : wait_both_ready(c, ps, ready_x);
+  if (r) return r;
+  // every chunk of this transfer behind a Down path waits on the gate of the
+  // Down it first met — a switch opens exactly that one (and re-arms the path
+  // with a fresh gate for later transfers), even while this loop still runs
+  int my_gate = -1;
+  for (int k = 0; k < nchunks; k++) {
+    const size_t off = (size_t)k * chunk, n = std::min(chunk, bytes - off);
+    {
+      std::lock_guard<std::mutex> g(c->fault_mu);
+      if (fault_ops_index >= 0) fire_chunk_faults(c, chn, fault_ops_index, k, 0);
+      if (chn.fault[0].down && my_gate < 0) {
+        my_gate = chn.fault[0].gate;
+        __atomic_store_n(&w->pgate, (uint32_t)my_gate + 1, __ATOMIC_SEQ_CST);  // before the first wait on it
+      }
+      if (my_gate >= 0) {
+        r = memop_wait(ps, &c->gate_words[my_gate], 1);
+        if (r) return r;
+      }
+    }
+    if (eng == ENG_SM) {
+      int grid = 0;
+      ICCL_CHECK_CUDA(launch_copy(src + off, dst + off, n, c->cfg.sm_cap, nullptr, ps, &grid));
+      c->kernels_launched += 1;
+      c->ctas_launched += grid;
+    } else {
+      ICCL_CHECK_CU(driver()->cuMemcpyDtoDAsync((CUdeviceptr)(dst + off), (CUdeviceptr)(src + off), n, (CUstream)ps));
+    }
+    c->copies_issued += 1;
+    c->bytes_issued += n;
+    if (c->prog_events) {
+      ICCL_CHECK_CUDA(cudaEventRecord(evs[k], ps));
+      ICCL_CHECK_CUDA(cudaStreamWaitEvent(pstr, evs[k], 0));
+      r = memop_write(pstr, &w->prog, (uint32_t)(k + 1));
+    } else {
+      r = memop_write(ps, &w->prog, (uint32_t)(k + 1));
+    }
+    if (r) return r;
+  }
+  p.clear();
+  p.push_back(wparam(&w->p_fin, 1));
+  p.push_back(wparam(&w->go, 1));
+  r = batch_memops(ps, p);
+  if (r) return r;
+  r = memop_wait(ps, &w->ns, 1);
+  if (r) return r;
+  return batch_memops(ps, fin);
 }
 
 // ---------------------------------------------------------------- watchdog thread
@@ -4058,6 +4075,8 @@ int iccl_selftest_failover(int scenario, int nchunks, int fault_chunk, uint64_t 
   }
   volatile uint32_t* pgate = dead ? &c->gate_words[chn.fault[0].gate] : nullptr;
   volatile uint32_t* bgate = scenario == 3 ? &c->gate_words[chn.fault[1].gate] : nullptr;
+  w->pgate = dead ? (uint32_t)chn.fault[0].gate + 1 : 0;  // as armed_launch publishes them for K9a
+  w->bgate = scenario == 3 ? (uint32_t)chn.fault[1].gate + 1 : 0;
   Xfer x;
   x.armed = true;
   x.aw = 0;
@@ -4111,7 +4130,8 @@ int iccl_selftest_failover(int scenario, int nchunks, int fault_chunk, uint64_t 
       if (ctl == kCtlSwitch) dec = kDecCopy;
       else if (ctl == kCtlAbort) dec = kDecExit;
       else if (ld(&w->p_fin)) dec = ld(&w->ctl) == kCtlSwitch ? kDecCopy : kDecExit;
-      else if (ctl == kCtlProbe && !probed && (!pgate || ld(pgate) != 0)) {
+      else if (ctl == kCtlProbe && !probed &&
+               (ld(&w->pgate) == 0 || ld(&c->gate_words[ld(&w->pgate) - 1]) != 0)) {
         st(&w->probe_done, 1);
         probed = true;
       } else {
