@@ -590,6 +590,8 @@ struct iccl_comm {
   std::mutex open_mu;   // serialises cudaIpcOpenMemHandle (map_peer_allocation)
   std::vector<Fault> faults;
   uint64_t faults_t0 = 0;
+  std::atomic<int> time_faults_pending{0};  // unfired time-triggered entries naming this rank
+  std::atomic<uint64_t> tf_last{0};          // last fire_time_faults pass (rate limit)
   std::atomic<int> path_req[2 * kMaxRanks];  // API-requested switches per channel: -1 none, else target path
   std::atomic<uint64_t> pending_xfers{0};
   std::atomic<uint64_t> kernels_launched{0}, ctas_launched{0}, copies_issued{0}, bytes_issued{0};
@@ -1042,6 +1044,14 @@ static void apply_fault(iccl_comm* c, FaultState& fs, bool up, uint64_t t) {
 }
 
 static void fire_time_faults(iccl_comm* c) {
+  // the watchdog and the proxy call this on every pass while they spin: with
+  // nothing pending they must not touch fault_mu at all, or the API thread —
+  // which takes it once per chunk it issues — starves (an armed 128-chunk
+  // issue took 44 ms, profiles/r02/raw/p_ac5_debug_n2.log)
+  if (c->time_faults_pending.load(std::memory_order_acquire) == 0) return;
+  const uint64_t now = now_ns();  // and at most every 10 us between the two threads
+  uint64_t last = c->tf_last.load(std::memory_order_relaxed);
+  if (now - last < 10000 || !c->tf_last.compare_exchange_strong(last, now)) return;
   std::lock_guard<std::mutex> g(c->fault_mu);
   uint64_t t = now_ns();
   for (auto& f : c->faults) {
@@ -1049,6 +1059,7 @@ static void fire_time_faults(iccl_comm* c) {
     if (f.f.src != c->rank && f.f.dst != c->rank) continue;
     if (t - c->faults_t0 < f.f.t_us * 1000ull) continue;
     f.fired = true;
+    c->time_faults_pending.fetch_sub(1);
     ICCL_TRACE("time fault %s path %d of %d->%d fires at +%.1f us", f.f.up ? "Up" : "Down", f.f.path, f.f.src, f.f.dst,
                (t - c->faults_t0) * 1e-3);
     for (Channel& chn : c->ch)
@@ -2456,7 +2467,7 @@ static void watch_loop(iccl_comm* c) {
     batch.clear();
     // time-triggered faults fire here too: the proxy thread may sit in a CUDA
     // call that a user thread's synchronous call behind the faulted op blocks
-    // (host stores only; fire_time_faults is idempotent under fault_mu)
+    // (host stores only; fire_time_faults is idempotent under fault_mu);
     fire_time_faults(c);
     bool any = false, busy = false;
     for (Channel& chn : c->ch) {
@@ -3935,12 +3946,15 @@ iccl_result_t iccl_fault_set(iccl_comm_t c, const iccl_fault_t* f, int n) {
       touched.emplace_back(old.f.src, old.f.dst);
     }
     c->faults.clear();
+    int timed = 0;
     for (int i = 0; i < n; i++) {
       c->faults.push_back(Fault{f[i], false});
+      timed += f[i].trigger_kind == 0 && (f[i].src == c->rank || f[i].dst == c->rank);
       pair_of(c, f[i].src, f[i].dst).faults_armed.fetch_add(1);
       touched.emplace_back(f[i].src, f[i].dst);
     }
     c->faults_t0 = now_ns();
+    c->time_faults_pending.store(timed, std::memory_order_release);
     for (auto& chn : c->ch) chn.fault_seq_base = chn.dir == 0 ? c->pair_sends[chn.peer] : c->pair_recvs[chn.peer];
   }
   for (auto& t : touched) route_update(pair_of(c, t.first, t.second));
