@@ -346,10 +346,12 @@ def run_product(args):
     comm.destroy()  # before the CPU baseline: the communicator's threads would share its cores
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        per_step, cores, per = cpu_reference(args.bytes, 5, 1)
+        # the reference arm's own sample: the same steps / warm-up (a step is ~10 ms of CPU work)
+        per_step, cores, per = cpu_reference(args.bytes, args.steps, args.warmup)
         cpu = {"value": round(args.bytes / per_step / 1e9, 3), "unit": "GB/s", "cores": cores, "kind": "port",
-               "sample": f"5 steps of the same {args.bytes >> 20} MiB hop split into {cores} parallel send/recv "
-                         f"transfers of {per / MiB:.2f} MiB through the oracle transport (4 MiB chunks)"}
+               "sample": f"{args.steps} steps (after {args.warmup} warm-up) of the same {args.bytes >> 20} MiB hop "
+                         f"split into {cores} parallel send/recv transfers of {per / MiB:.2f} MiB through the oracle "
+                         f"transport (SPEC.md:228-263, 4 MiB chunks)"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
