@@ -548,6 +548,7 @@ struct iccl_comm {
   // other side's ready flag (ICCL_K7_READY): a parked stream slows the GPU's
   // other streams
   bool k7_ce = false, k7_ready = false;
+  int a2a_pieces = 1;  // ICCL_A2A_PIECES: pieces per remote alltoallv segment (see iccl_alltoallv)
   bool instream_ce = true;  // healthy pairs: the issuer enqueues the copy on its own user stream (ICCL_INSTREAM=0: off)
   bool armed_backup = true;  // attribution only (ICCL_ARMED_BACKUP=0): armed transfers enqueue no backup attempt
   int k9_mode = 0;           // attribution only (ICCL_K9_MODE): 1 = K9a alone, 2 = b_fin memop alone,
@@ -3199,6 +3200,7 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
   c->self_overlap = env_us("ICCL_SELF_OVERLAP", 1) != 0;
   c->k7_ce = env_us("ICCL_K7_CE", 0) != 0;
   c->k7_ready = env_us("ICCL_K7_READY", 0) != 0;
+  c->a2a_pieces = (int)std::min<uint64_t>(16, std::max<uint64_t>(1, env_us("ICCL_A2A_PIECES", 1)));
   c->instream_ce = env_us("ICCL_INSTREAM", 1) != 0;
   c->armed_backup = env_us("ICCL_ARMED_BACKUP", 1) != 0;
   c->k9_mode = (int)env_us("ICCL_K9_MODE", 0);
@@ -3633,13 +3635,27 @@ iccl_result_t iccl_alltoallv(iccl_comm_t c, const void* sbuf, const size_t* scou
   if (r) return r;
   const int n = c->nranks;
   // rotated schedule: step k pairs rank i with i+k (send) and i-k (recv) so
-  // the NVSwitch sees no incast; k = 0 is the self copy
-  for (int k = 0; k < n && r == ICCL_SUCCESS; k++) {
-    int to = (c->rank + k) % n, from = (c->rank - k + n) % n;
-    if (rcounts[from]) r = iccl_recv(c, (char*)rbuf + rdispls[from] * elem_bytes, rcounts[from] * elem_bytes, from, s,
-                                     nullptr);
-    if (!r && scounts[to])
-      r = iccl_send(c, (const char*)sbuf + sdispls[to] * elem_bytes, scounts[to] * elem_bytes, to, s, nullptr);
+  // the NVSwitch sees no incast; k = 0 is the self copy.
+  // ICCL_A2A_PIECES = P > 1 splits every remote segment into P pieces (both
+  // sides split a pair's count the same way) and rotates piece-major, so a
+  // rank that finishes a step early cannot run ahead by a whole segment.
+  const int pieces = c->a2a_pieces;
+  for (int pc = 0; pc < pieces && r == ICCL_SUCCESS; pc++) {
+    for (int k = pc == 0 ? 0 : 1; k < n && r == ICCL_SUCCESS; k++) {
+      int to = (c->rank + k) % n, from = (c->rank - k + n) % n;
+      const int np = k == 0 ? 1 : pieces;
+      if (k == 0 && pc > 0) continue;
+      auto piece = [&](size_t cnt, size_t* lo, size_t* len) {  // piece pc of cnt elements
+        *lo = cnt * (size_t)pc / np;
+        *len = cnt * (size_t)(pc + 1) / np - *lo;
+      };
+      size_t lo, len;
+      piece(rcounts[from], &lo, &len);
+      if (len) r = iccl_recv(c, (char*)rbuf + (rdispls[from] + lo) * elem_bytes, len * elem_bytes, from, s, nullptr);
+      piece(scounts[to], &lo, &len);
+      if (!r && len)
+        r = iccl_send(c, (const char*)sbuf + (sdispls[to] + lo) * elem_bytes, len * elem_bytes, to, s, nullptr);
+    }
   }
   iccl_result_t r2 = iccl_group_end(c);
   return r ? r : r2;
