@@ -678,3 +678,74 @@ def fuzz_failover(comm, rank, world, trials, seed, delta_us):
     res["chunks"] = np.array(chunks_all, np.int64)
     res["chunks_off"] = np.array(chunks_off, np.int64)
     return res
+
+
+def pp_1f1b(comm, rank, world, M, T=64, H=256):
+    """Megatron's non-interleaved 1F1B schedule (benchmarks/pp_1f1b.py: fused
+    send_forward_recv_backward / send_backward_recv_forward as one batched
+    isend/irecv on a communication stream, GEMMs on the compute stream) on
+    small activations.  Every sent tensor's bytes are published through the
+    store under (src, dst, direction, microbatch); every received tensor is
+    compared with them.  Returns the number of matching / total receives."""
+    import paper_2510_00991_b200 as iccl
+    dev = dev_of(rank)
+    st = comm._test_store
+    S = world
+    first, last = rank == 0, rank == S - 1
+    g = torch.Generator(device=dev).manual_seed(10 + rank)
+    W = torch.randn(H, H, dtype=torch.bfloat16, device=dev, generator=g) * 0.05
+    x0 = torch.randn(T, H, dtype=torch.bfloat16, device=dev, generator=g)
+    comp = torch.cuda.current_stream()
+    cstream = torch.cuda.Stream(device=dev)
+    sent = {"f": 0, "b": 0}
+    got = {"f": 0, "b": 0}
+    checks = []
+
+    def exchange(sends, recvs):
+        cstream.wait_stream(comp)
+        outs = [torch.empty(T, H, dtype=torch.bfloat16, device=dev) for _ in recvs]
+        with torch.cuda.stream(cstream):
+            ops = [iccl.P2POp("isend", t, p) for t, p, _ in sends] + \
+                  [iccl.P2POp("irecv", o, p) for o, (p, _) in zip(outs, recvs)]
+            comm.batch_isend_irecv(ops, stream=cstream)
+        cstream.synchronize()
+        for t, p, d in sends:
+            st.set(f"pp/{rank}/{p}/{d}/{sent[d]}", t.view(torch.int16).cpu().numpy().tobytes())
+            sent[d] += 1
+        for o, (p, d) in zip(outs, recvs):
+            want = st.get(f"pp/{p}/{rank}/{d}/{got[d]}")
+            checks.append(o.view(torch.int16).cpu().numpy().tobytes() == want)
+            got[d] += 1
+        comp.wait_stream(cstream)
+        return outs
+
+    def forward(x):
+        return (x0 if x is None else x) @ W
+
+    def backward(dy):
+        return dy @ W.t()
+
+    warm = min(S - rank - 1, M)
+    for _ in range(warm):
+        x = None if first else exchange([], [(rank - 1, "f")])[0]
+        exchange([(forward(x), rank + 1, "f")], [])
+    steady = M - warm
+    x = None if (first or steady == 0) else exchange([], [(rank - 1, "f")])[0]
+    for i in range(steady):
+        y = forward(x)
+        dy = y if last else exchange([(y, rank + 1, "f")], [(rank + 1, "b")])[0]
+        dx = backward(dy)
+        if i == steady - 1:
+            if not first:
+                exchange([(dx, rank - 1, "b")], [])
+        elif first:
+            x = None
+        else:
+            x = exchange([(dx, rank - 1, "b")], [(rank - 1, "f")])[0]
+    for _ in range(warm):
+        dy = exchange([], [(rank + 1, "b")])[0]
+        dx = backward(dy)
+        if not first:
+            exchange([(dx, rank - 1, "b")], [])
+    torch.cuda.synchronize()
+    return {"ok": np.array([sum(checks)]), "n": np.array([len(checks)])}

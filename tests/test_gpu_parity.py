@@ -483,3 +483,18 @@ def test_fused_combine_8_ranks_full_size_and_armed_fallback(torch_cuda, tmp_path
                     fault=(2, 1, 1 << 20), timeout=300, config=dict(chunk_bytes=256 * 1024))
     for r in range(4):
         assert bool(res[r]["recv_ok"][0]) and bool(res[r]["roundtrip_ok"][0]), r
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_pp_1f1b_schedule_bytes(torch_cuda, tmp_path, world):
+    """SURVEY §8f row f2 on the product: Megatron's 1F1B schedule (batched
+    send_forward_recv_backward / send_backward_recv_forward on a
+    communication stream, GEMMs on the compute stream) over `world` stages,
+    8 microbatches: no deadlock, and every received activation / gradient is
+    byte-identical to what its stage sent."""
+    import gpu_scenarios as sc
+    res = run_ranks(world, sc.pp_1f1b, tmp_path, M=8, timeout=300)
+    for r in range(world):
+        n = int(res[r]["n"][0])
+        exp = 0 if world == 1 else (8 if r in (0, world - 1) else 16)
+        assert n == exp and int(res[r]["ok"][0]) == n, (r, n, int(res[r]["ok"][0]))
