@@ -181,12 +181,14 @@ def test_AC5_competing_flow_smoothing(torch_cuda, tmp_path):
     # the three series indexed by completion (record i closes one sample of each)
     s1, s8, s32 = (np.concatenate([np.full(w - 1, np.nan), _series(t1, t2, b, w)]) for w in (1, 8, 32))
     base = np.median(s1[:48])
-    assert np.nanmin(s8) < 0.85 * base, "the competing flow must slow the monitored one"
-    # the transition: where the W=8 series first drops clearly below the
-    # steady rate; the variances are compared over the same completions
-    # around it (+-32, the widest window's span)
-    k = int(np.argmax(s8 < 0.85 * base))
-    assert k >= 64, "the competing flow must start after the steady phase"
+    # the transition: the first completion from which the W=8 series stays
+    # clearly below the steady rate for 16 samples (a lone dip — ranks sharing
+    # one GPU get time-sliced — is not the competing flow); the variances are
+    # compared over the same completions around it (+-32, the widest window)
+    slow = s8 < 0.85 * base
+    ks = [i for i in range(48, n - 16) if slow[i:i + 16].all()]
+    assert ks, "the competing flow must slow the monitored one"
+    k = ks[0]
     lo, hi = k - 32, min(n, k + 32)
     v1, v8, v32 = np.var(s1[lo:hi]), np.var(s8[lo:hi]), np.var(s32[lo:hi])
     assert v1 >= v8 >= v32, (k, v1, v8, v32)
