@@ -467,7 +467,7 @@ def monitor_competing(comm, rank, world, nchunks, chunk, comp_bytes, delay_us):
     dst = torch.empty(n, dtype=torch.uint8, device=dev) if rank == 1 else None
     dst2 = torch.empty(comp_bytes, dtype=torch.uint8, device=dev) if rank == 1 else None
     sa, sb = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
-    hammer = [torch.empty(1 << 30, dtype=torch.uint8, device=dev) for _ in range(2)] if rank == 2 else None
+    hammer = [torch.empty(1 << 30, dtype=torch.uint8, device=dev) for _ in range(2)] if rank == 0 else None
 
     def round_(tag, delay):
         if rank == 1:
@@ -480,14 +480,17 @@ def monitor_competing(comm, rank, world, nchunks, chunk, comp_bytes, delay_us):
             _store_barrier(comm, tag)
             if rank == 2:
                 time.sleep(delay * 1e-6)
-                if delay and torch.cuda.device_count() == 1:
-                    # all ranks on one GPU: the "peer" copies are local copies,
-                    # which two copy engines run side by side without slowing
-                    # each other, so the competitor is an HBM-bound stream of
-                    # device copies that takes most of the HBM bandwidth
+            comm.send(src if rank == 0 else src2, 1)
+            if rank == 0 and delay and torch.cuda.device_count() == 1:
+                # all ranks on one GPU: the "peer" copies are local copies,
+                # which two copy engines run side by side without slowing each
+                # other (and other processes' kernels are time-sliced), so the
+                # competitor is an HBM-bound stream of device copies in this
+                # process, on a second stream, `delay` after the send
+                time.sleep(delay * 1e-6)
+                with torch.cuda.stream(sb):
                     for _ in range(12):
                         hammer[0].copy_(hammer[1])
-            comm.send(src if rank == 0 else src2, 1)
         torch.cuda.synchronize()
 
     round_("mc0", 0)          # warm-up: IPC mappings opened
