@@ -129,7 +129,7 @@ def test_route_segments_start_after_both_sides():
 
 
 # ---------------------------------------------------------------- failover protocol (armed transfers)
-def _failover(scenario, nchunks=12, fault_chunk=5, delta_us=2000):
+def _failover(scenario, nchunks=12, fault_chunk=5, delta_us=20_000):
     out = (C.c_int64 * 8)()
     rc = lib.iccl_selftest_failover(scenario, nchunks, fault_chunk, delta_us, out)
     keys = ("switches", "resume", "done", "total", "done_flags", "records", "probe", "async_err")
