@@ -12,6 +12,19 @@ from gpu_helpers import run_ranks  # noqa: E402
 
 
 
+def competing():
+    import numpy as np
+    MiB = 1 << 20
+    os.environ["ICCL_DEBUG"] = "0"
+    with tempfile.TemporaryDirectory() as d:
+        res = run_ranks(3, sc.monitor_competing, d, nchunks=384, chunk=16 * MiB, comp_bytes=2048 * MiB,
+                        delay_us=2000, config=dict(chunk_bytes=16 * MiB, monitor_enabled=True, window=1024))
+        t1, t2 = res[0]["t1"], res[0]["t2"]
+        dur = (t2 - t1) / 1e3
+        print("competing: records", len(dur), "span us", (t2[-1] - t1[0]) / 1e3)
+        print("durations us (every 8th):", np.round(dur[::8], 1).tolist())
+
+
 def main():
     MiB = 1 << 20
     with tempfile.TemporaryDirectory() as d:
@@ -38,3 +51,4 @@ def main():
 
 if __name__ == "__main__":
     main()
+    competing()
