@@ -3172,6 +3172,9 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
   c->ch.resize(2 * nranks);
   uint32_t* prog = c->pinned;  // first 32 KB of pinned: progress words
   int next_prog = 0;
+  // the proxy indexes c->streams while the API thread may still add a
+  // channel's backup / progress stream: reserve so it never reallocates
+  c->streams.reserve(64 + 40 * (size_t)nranks);
   auto mk_stream = [&](int engine) -> int {
     StreamCtx sc;
     cudaStreamCreateWithPriority(&sc.s, cudaStreamNonBlocking, prio_hi);
@@ -3974,6 +3977,17 @@ iccl_result_t iccl_fault_set(iccl_comm_t c, const iccl_fault_t* f, int n) {
     for (auto& chn : c->ch) chn.fault_seq_base = chn.dir == 0 ? c->pair_sends[chn.peer] : c->pair_recvs[chn.peer];
   }
   for (auto& t : touched) route_update(pair_of(c, t.first, t.second));
+  // the streams an armed transfer of these pairs uses, created now: creating
+  // a stream while the device is busy took up to 72 ms (profiles/r02/raw/
+  // x_ac5_debug_n2.log), which would land inside the first armed issue
+  for (int i = 0; i < n; i++)
+    for (Channel& chn : c->ch)
+      if (chn.src == f[i].src && chn.dst == f[i].dst) {
+        cudaStream_t s = nullptr;
+        iccl_result_t r = backup_stream(c, chn, &s);
+        if (!r) r = prog_stream(c, chn, &s);
+        if (r) return r;
+      }
   return ICCL_SUCCESS;
 }
 

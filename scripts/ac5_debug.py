@@ -35,8 +35,8 @@ def main():
             for r in res:
                 if len(r["t2"]):
                     import numpy as np
-                    d = r["t2"] - r["t1"]
-                    print("records", len(d), "dur min/med/max ns", d.min(), int(np.median(d)), d.max(),
+                    du = r["t2"] - r["t1"]
+                    print("records", len(du), "dur min/med/max ns", du.min(), int(np.median(du)), du.max(),
                           "span us", (r["t2"][-1] - r["t1"][0]) / 1e3)
         finally:
             for r in range(2):
