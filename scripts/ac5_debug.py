@@ -17,7 +17,7 @@ def competing():
     MiB = 1 << 20
     os.environ["ICCL_DEBUG"] = "0"
     with tempfile.TemporaryDirectory() as d:
-        res = run_ranks(3, sc.monitor_competing, d, nchunks=384, chunk=16 * MiB, comp_bytes=2048 * MiB,
+        res = run_ranks(2, sc.monitor_competing, d, nchunks=384, chunk=16 * MiB, comp_bytes=2048 * MiB,
                         delay_us=2000, config=dict(chunk_bytes=16 * MiB, monitor_enabled=True, window=1024))
         t1, t2 = res[0]["t1"], res[0]["t2"]
         dur = (t2 - t1) / 1e3
@@ -29,8 +29,8 @@ def main():
     MiB = 1 << 20
     with tempfile.TemporaryDirectory() as d:
         try:
-            res = run_ranks(2, sc.monitor_accuracy, d, nchunks=128, chunk=16 * MiB, stall_chunk=64, up_us=20_000,
-                            config=dict(chunk_bytes=16 * MiB, monitor_enabled=True, delta_us=200_000, window=1024))
+            res = run_ranks(2, sc.monitor_accuracy, d, nchunks=128, chunk=16 * MiB, stall_chunk=64, up_us=200_000,
+                            config=dict(chunk_bytes=16 * MiB, monitor_enabled=True, delta_us=5_000_000, window=1024))
             print("switches", [r["switches"] for r in res], [r["switch_desc"] for r in res])
             for r in res:
                 if len(r["t2"]):

@@ -454,43 +454,40 @@ def monitor_accuracy(comm, rank, world, nchunks, chunk, stall_chunk, up_us):
 def monitor_competing(comm, rank, world, nchunks, chunk, comp_bytes, delay_us):
     """AC5's smoothing claim ("competing flow halving
     bandwidth mid-stream ... var(W=1) >= var(W=8) >= var(W=32)") on the
-    product: rank 0 pushes `nchunks` chunks to rank 1, monitor on; `delay_us`
-    after the start rank 2 pushes `comp_bytes` to rank 1 as well, so the two
-    flows share rank 1's ingress for a while.  Rank 1 posts both receives
-    first (on two streams), so the senders push and rank 0 holds the
-    monitored flow's records."""
+    product: rank 0 pushes `nchunks` chunks to rank 1 on its current stream,
+    monitor on; `delay_us` later it pushes `comp_bytes` more to rank 1 on a
+    second stream (the copy engine runs a GPU's peer copies one at a time)
+    and starts an HBM-bound stream of device copies on a third (with both
+    ranks on one GPU the copies are local, and two engines run them side by
+    side: there the HBM traffic is the competitor).  Rank 1 posts both receives first, so rank 0 pushes and
+    holds the monitored flow's records (its second flow's records go to a
+    different op and are filtered out by size)."""
     import time
     dev = dev_of(rank)
     n = nchunks * chunk
     src = to_dev(payload(n, seed=6), dev) if rank == 0 else None
-    src2 = to_dev(payload(comp_bytes, seed=7), dev) if rank == 2 else None
+    src2 = to_dev(payload(comp_bytes, seed=7), dev) if rank == 0 else None
     dst = torch.empty(n, dtype=torch.uint8, device=dev) if rank == 1 else None
     dst2 = torch.empty(comp_bytes, dtype=torch.uint8, device=dev) if rank == 1 else None
-    sa, sb = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    sa, sb, sc = (torch.cuda.Stream(device=dev) for _ in range(3))
     hammer = [torch.empty(1 << 30, dtype=torch.uint8, device=dev) for _ in range(2)] if rank == 0 else None
 
     def round_(tag, delay):
         if rank == 1:
             wa = comm.irecv(dst, 0, stream=sa)
-            wb = comm.irecv(dst2, 2, stream=sb)
+            wb = comm.irecv(dst2, 0, stream=sb)
             _store_barrier(comm, tag)
             wa.synchronize()
             wb.synchronize()
         else:
             _store_barrier(comm, tag)
-            if rank == 2:
-                time.sleep(delay * 1e-6)
-            comm.send(src if rank == 0 else src2, 1)
-            if rank == 0 and delay and torch.cuda.device_count() == 1:
-                # all ranks on one GPU: the "peer" copies are local copies,
-                # which two copy engines run side by side without slowing each
-                # other (and other processes' kernels are time-sliced), so the
-                # competitor is an HBM-bound stream of device copies in this
-                # process, on a second stream, `delay` after the send
-                time.sleep(delay * 1e-6)
-                with torch.cuda.stream(sb):
+            comm.send(src, 1)
+            time.sleep(delay * 1e-6)
+            if delay:
+                with torch.cuda.stream(sc):
                     for _ in range(12):
                         hammer[0].copy_(hammer[1])
+            comm.send(src2, 1, stream=sb)
         torch.cuda.synchronize()
 
     round_("mc0", 0)          # warm-up: IPC mappings opened
@@ -499,7 +496,10 @@ def monitor_competing(comm, rank, world, nchunks, chunk, comp_bytes, delay_us):
     round_("mc1", delay_us)
     time.sleep(0.05)
     out = {}
-    recs = sorted([r for r in comm.monitor.drain() if r.peer == 1], key=lambda r: r.t2)
+    recs = sorted([r for r in comm.monitor.drain() if r.peer == 1 and r.size == chunk and r.chunk < nchunks],
+                  key=lambda r: r.t2)
+    first_op = min((r.op_seq for r in recs), default=0)
+    recs = [r for r in recs if r.op_seq == first_op]  # the monitored flow (the competitor is a later op)
     out["t1"] = np.array([r.t1 for r in recs], np.int64)
     out["t2"] = np.array([r.t2 for r in recs], np.int64)
     out["bytes"] = np.array([r.size for r in recs], np.int64)
