@@ -454,28 +454,32 @@ def monitor_accuracy(comm, rank, world, nchunks, chunk, stall_chunk, up_us):
 def monitor_competing(comm, rank, world, nchunks, chunk, comp_bytes, delay_us):
     """AC5's smoothing claim ("competing flow halving
     bandwidth mid-stream ... var(W=1) >= var(W=8) >= var(W=32)") on the
-    product: rank 0 pushes `nchunks` chunks to rank 1 on its current stream,
-    monitor on; `delay_us` later it pushes `comp_bytes` more to rank 1 on a
-    second stream (the copy engine runs a GPU's peer copies one at a time)
-    and starts an HBM-bound stream of device copies on a third (with both
-    ranks on one GPU the copies are local, and two engines run them side by
-    side: there the HBM traffic is the competitor).  Rank 1 posts both receives first, so rank 0 pushes and
-    holds the monitored flow's records (its second flow's records go to a
-    different op and are filtered out by size)."""
+    product: rank 0 pushes `nchunks` chunks to rank 1 (copy engine, monitor
+    on); `delay_us` later a second communicator with the SM transport pushes
+    `comp_bytes` over the same link with K1 — SM stores and copy-engine
+    writes share the link, while a GPU's copy engine would only queue a
+    second copy behind the first.  With both ranks on one GPU (local copies)
+    the competitor adds an HBM-bound stream of device copies.  Rank 1 posts
+    its receives first, so rank 0 pushes and holds the monitored records."""
     import time
+    import torch.distributed as dist
+    from paper_2510_00991_b200 import Communicator, IcclConfig
     dev = dev_of(rank)
     n = nchunks * chunk
+    one_gpu = torch.cuda.device_count() == 1
+    comm2 = Communicator(rank, world, dev.index, IcclConfig.defaults(transport="sm", sm_cap=32, chunk_bytes=n),
+                         store=dist.PrefixStore("competitor", comm._test_store))
     src = to_dev(payload(n, seed=6), dev) if rank == 0 else None
     src2 = to_dev(payload(comp_bytes, seed=7), dev) if rank == 0 else None
     dst = torch.empty(n, dtype=torch.uint8, device=dev) if rank == 1 else None
     dst2 = torch.empty(comp_bytes, dtype=torch.uint8, device=dev) if rank == 1 else None
     sa, sb, sc = (torch.cuda.Stream(device=dev) for _ in range(3))
-    hammer = [torch.empty(1 << 30, dtype=torch.uint8, device=dev) for _ in range(2)] if rank == 0 else None
+    hammer = [torch.empty(1 << 30, dtype=torch.uint8, device=dev) for _ in range(2)] if rank == 0 and one_gpu else None
 
     def round_(tag, delay):
         if rank == 1:
             wa = comm.irecv(dst, 0, stream=sa)
-            wb = comm.irecv(dst2, 0, stream=sb)
+            wb = comm2.irecv(dst2, 0, stream=sb)
             _store_barrier(comm, tag)
             wa.synchronize()
             wb.synchronize()
@@ -483,11 +487,11 @@ def monitor_competing(comm, rank, world, nchunks, chunk, comp_bytes, delay_us):
             _store_barrier(comm, tag)
             comm.send(src, 1)
             time.sleep(delay * 1e-6)
-            if delay:
+            if delay and one_gpu:
                 with torch.cuda.stream(sc):
                     for _ in range(12):
                         hammer[0].copy_(hammer[1])
-            comm.send(src2, 1, stream=sb)
+            comm2.send(src2, 1, stream=sb)
         torch.cuda.synchronize()
 
     round_("mc0", 0)          # warm-up: IPC mappings opened
@@ -496,16 +500,15 @@ def monitor_competing(comm, rank, world, nchunks, chunk, comp_bytes, delay_us):
     round_("mc1", delay_us)
     time.sleep(0.05)
     out = {}
-    recs = sorted([r for r in comm.monitor.drain() if r.peer == 1 and r.size == chunk and r.chunk < nchunks],
-                  key=lambda r: r.t2)
-    first_op = min((r.op_seq for r in recs), default=0)
-    recs = [r for r in recs if r.op_seq == first_op]  # the monitored flow (the competitor is a later op)
+    recs = sorted([r for r in comm.monitor.drain() if r.peer == 1], key=lambda r: r.t2)
     out["t1"] = np.array([r.t1 for r in recs], np.int64)
     out["t2"] = np.array([r.t2 for r in recs], np.int64)
     out["bytes"] = np.array([r.size for r in recs], np.int64)
     if rank == 1:
         out["ok"] = np.array([bool(torch.equal(dst, to_dev(payload(n, seed=6), dev))) and
                               bool(torch.equal(dst2, to_dev(payload(comp_bytes, seed=7), dev)))])
+    torch.cuda.synchronize()
+    comm2.destroy()
     return out
 
 

@@ -170,9 +170,8 @@ def test_AC5_monitor_accuracy_and_smoothing(torch_cuda, tmp_path):
 
 def test_AC5_competing_flow_smoothing(torch_cuda, tmp_path):
     """AC5's smoothing claim on hardware: a second flow
-    from the same sender to the same receiver starts mid-transfer on another
-    stream and takes turns with it on the copy engine (ranks sharing one GPU:
-    an HBM-bound stream of device copies instead);
+    (SM stores through a second communicator) starts mid-transfer on the
+    same link (ranks sharing one GPU: plus an HBM-bound stream of copies);
     the monitored flow's records slow down, and over the transition
     var(W=1) >= var(W=8) >= var(W=32) (on one GPU, of the series'
     sample-to-sample differences)."""
