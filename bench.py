@@ -368,8 +368,8 @@ def run_product(args):
             "gpu_launches_note": "kernels of libiccl_b200.so in the timed region, counted by iccl_comm_stats; a "
                                  "256 MiB hop takes the copy-engine path, which by design launches none "
                                  "(north_star: 0 SMs on the default path) - its device work is the copies and "
-                                 "stream memops counted here; <=256 KiB hops run K5, <=16 MiB K6, the backup K1, "
-                                 "and --workload alltoallv K2/K3",
+                                 "stream memops counted here; <=256 KiB hops run K5, <=16 MiB K6, the backup K1 / K9, "
+                                 "and --workload alltoallv K2/K3 (fused forms: K8 / K10)",
             "sms_used_by_copies": 0, "clocks": clk.summary(),
         }
         print(json.dumps(line))
