@@ -549,6 +549,7 @@ struct iccl_comm {
   // other streams
   bool k7_ce = false, k7_ready = false;
   int a2a_pieces = 1;  // ICCL_A2A_PIECES: pieces per remote alltoallv segment (see iccl_alltoallv)
+  int a2a_order = 0;   // ICCL_A2A_ORDER: 0 rotated, 1 largest segment first
   bool instream_ce = true;  // healthy pairs: the issuer enqueues the copy on its own user stream (ICCL_INSTREAM=0: off)
   bool armed_backup = true;  // attribution only (ICCL_ARMED_BACKUP=0): armed transfers enqueue no backup attempt
   int k9_mode = 0;           // attribution only (ICCL_K9_MODE): 1 = K9a alone, 2 = b_fin memop alone,
@@ -3204,6 +3205,7 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
   c->k7_ce = env_us("ICCL_K7_CE", 0) != 0;
   c->k7_ready = env_us("ICCL_K7_READY", 0) != 0;
   c->a2a_pieces = (int)std::min<uint64_t>(16, std::max<uint64_t>(1, env_us("ICCL_A2A_PIECES", 1)));
+  c->a2a_order = (int)env_us("ICCL_A2A_ORDER", 0);
   c->instream_ce = env_us("ICCL_INSTREAM", 1) != 0;
   c->armed_backup = env_us("ICCL_ARMED_BACKUP", 1) != 0;
   c->k9_mode = (int)env_us("ICCL_K9_MODE", 0);
@@ -3643,9 +3645,15 @@ iccl_result_t iccl_alltoallv(iccl_comm_t c, const void* sbuf, const size_t* scou
   // sides split a pair's count the same way) and rotates piece-major, so a
   // rank that finishes a step early cannot run ahead by a whole segment.
   const int pieces = c->a2a_pieces;
+  // ICCL_A2A_ORDER=1: the remote sends in decreasing size (largest segment
+  // first) instead of the rotation; receives keep the rotated order
+  std::vector<int> send_to(n);
+  for (int k = 0; k < n; k++) send_to[k] = (c->rank + k) % n;
+  if (c->a2a_order == 1)
+    std::stable_sort(send_to.begin() + 1, send_to.end(), [&](int a, int b) { return scounts[a] > scounts[b]; });
   for (int pc = 0; pc < pieces && r == ICCL_SUCCESS; pc++) {
     for (int k = pc == 0 ? 0 : 1; k < n && r == ICCL_SUCCESS; k++) {
-      int to = (c->rank + k) % n, from = (c->rank - k + n) % n;
+      int to = send_to[k], from = (c->rank - k + n) % n;
       const int np = k == 0 ? 1 : pieces;
       if (k == 0 && pc > 0) continue;
       auto piece = [&](size_t cnt, size_t* lo, size_t* len) {  // piece pc of cnt elements

@@ -74,6 +74,9 @@ for STEP in "$@"; do
     a2apieces) for P in 1 2 4 1; do echo "## ICCL_A2A_PIECES=$P" >> "$LOG"
                 ICCL_A2A_PIECES=$P timeout 600 $TR --nproc-per-node $NG --master-port 29740 benchmarks/moe_alltoallv.py --impl iccl >> "$LOG" 2>&1
               done ;;
+    a2aorder) for O in 0 1 0 1; do echo "## ICCL_A2A_ORDER=$O" >> "$LOG"
+                ICCL_A2A_ORDER=$O timeout 600 $TR --nproc-per-node $NG --master-port 29741 benchmarks/moe_alltoallv.py --impl iccl >> "$LOG" 2>&1
+              done ;;
     moe) for I in iccl nccl; do timeout 600 $TR --nproc-per-node $NG --master-port 29679 benchmarks/moe_alltoallv.py --impl $I >> "$LOG" 2>&1; done ;;
     launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --target-processes all -c 2000 --csv \
                 --log-file gpurun_out/${TAG}_launches.csv python -c "import __graft_entry__ as g; g.smoke()" >> "$LOG" 2>&1 ;;
