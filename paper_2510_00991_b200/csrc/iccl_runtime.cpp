@@ -550,6 +550,8 @@ struct iccl_comm {
   bool k7_ce = false, k7_ready = false;
   int a2a_pieces = 1;  // ICCL_A2A_PIECES: pieces per remote alltoallv segment (see iccl_alltoallv)
   int a2a_order = 0;   // ICCL_A2A_ORDER: 0 rotated, 1 largest segment first
+  size_t ll_lines_per_blk = kLLLinesPerBlk;  // K5 CTAs per op: lines per CTA (ICCL_LL_LINES_PER_BLK) ...
+  int ll_max_blk = kLLMaxBlk;                // ... up to this many (ICCL_LL_MAX_BLK)
   bool instream_ce = true;  // healthy pairs: the issuer enqueues the copy on its own user stream (ICCL_INSTREAM=0: off)
   bool armed_backup = true;  // attribution only (ICCL_ARMED_BACKUP=0): armed transfers enqueue no backup attempt
   int k9_mode = 0;           // attribution only (ICCL_K9_MODE): 1 = K9a alone, 2 = b_fin memop alone,
@@ -2909,8 +2911,8 @@ static iccl_result_t launch_ll_ops(iccl_comm* c, cudaStream_t s, std::vector<OpD
     for (; i < ops.size() && b.n < kLLMaxOps; i++) {
       OpDesc& op = ops[i];
       const size_t lines = (op.bytes + 3) / 4;
-      const uint32_t nblk = (uint32_t)std::min<size_t>(kLLMaxBlk, std::max<size_t>(1, (lines + kLLLinesPerBlk - 1) /
-                                                                                          kLLLinesPerBlk));
+      const uint32_t nblk = (uint32_t)std::min<size_t>(c->ll_max_blk, std::max<size_t>(1, (lines + c->ll_lines_per_blk - 1) /
+                                                                                            c->ll_lines_per_blk));
       if (b.n > 0 && blocks + nblk > (uint32_t)kLLMaxBlocksPerLaunch) break;
       LLDesc& d = b.d[b.n++];
       d.kind = op.kind;
@@ -3206,6 +3208,8 @@ iccl_result_t iccl_comm_init_rank(iccl_comm_t* out, int nranks, iccl_unique_id_t
   c->k7_ready = env_us("ICCL_K7_READY", 0) != 0;
   c->a2a_pieces = (int)std::min<uint64_t>(16, std::max<uint64_t>(1, env_us("ICCL_A2A_PIECES", 1)));
   c->a2a_order = (int)env_us("ICCL_A2A_ORDER", 0);
+  c->ll_lines_per_blk = (size_t)std::max<uint64_t>(256, env_us("ICCL_LL_LINES_PER_BLK", kLLLinesPerBlk));
+  c->ll_max_blk = (int)std::min<uint64_t>(64, std::max<uint64_t>(1, env_us("ICCL_LL_MAX_BLK", kLLMaxBlk)));
   c->instream_ce = env_us("ICCL_INSTREAM", 1) != 0;
   c->armed_backup = env_us("ICCL_ARMED_BACKUP", 1) != 0;
   c->k9_mode = (int)env_us("ICCL_K9_MODE", 0);
