@@ -984,6 +984,25 @@ __device__ __forceinline__ bool ll_timed_out(unsigned long long t0) {
   return globaltimer() - t0 > 10000000000ull;
 }
 
+constexpr int kLLUnroll = 8;
+
+// The 4-byte word i of an LL message (byte-wise at a misaligned / short end).
+__device__ __forceinline__ uint32_t ll_load_word(const char* buf, size_t bytes, size_t i) {
+  const size_t off = i * 4;
+  if (off + 4 <= bytes && ((uintptr_t)(buf + off) & 3) == 0) return *(const uint32_t*)(buf + off);
+  uint32_t w = 0;
+  for (int k = 0; k < 4 && off + k < bytes; k++) w |= (uint32_t)(unsigned char)buf[off + k] << (8 * k);
+  return w;
+}
+__device__ __forceinline__ void ll_store_word(char* buf, size_t bytes, size_t i, uint32_t w) {
+  const size_t off = i * 4;
+  if (off + 4 <= bytes && ((uintptr_t)(buf + off) & 3) == 0) {
+    *(uint32_t*)(buf + off) = w;
+    return;
+  }
+  for (int k = 0; k < 4 && off + k < bytes; k++) buf[off + k] = (char)(w >> (8 * k));
+}
+
 __global__ void __launch_bounds__(256) iccl_ll_group(LLBatch b) {
   __shared__ int s_op;
   if (threadIdx.x == 0) {
@@ -1019,15 +1038,21 @@ __global__ void __launch_bounds__(256) iccl_ll_group(LLBatch b) {
       const unsigned long long t = globaltimer();
       asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(&d.stamp->t1), "l"(t) : "memory");
     }
-    for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-      uint32_t w = 0;
-      const size_t off = i * 4;
-      if (off + 4 <= d.bytes && ((uintptr_t)(d.buf + off) & 3) == 0) {
-        w = *(const uint32_t*)(d.buf + off);
-      } else {
-        for (int k = 0; k < 4 && off + k < d.bytes; k++) w |= (uint32_t)(unsigned char)d.buf[off + k] << (8 * k);
+    // kLLUnroll source words loaded before their line stores: the loads of
+    // one thread are in flight together instead of one latency per line
+    for (size_t i0 = lo + threadIdx.x; i0 < hi; i0 += kLLUnroll * blockDim.x) {
+      uint32_t w[kLLUnroll];
+#pragma unroll
+      for (int j = 0; j < kLLUnroll; j++) {
+        const size_t i = i0 + (size_t)j * blockDim.x;
+        w[j] = i < hi ? ll_load_word(d.buf, d.bytes, i) : 0u;
       }
-      asm volatile("st.volatile.global.v2.u32 [%0], {%1, %2};" ::"l"(slot + i), "r"(w), "r"(d.seq) : "memory");
+#pragma unroll
+      for (int j = 0; j < kLLUnroll; j++) {
+        const size_t i = i0 + (size_t)j * blockDim.x;
+        if (i < hi)
+          asm volatile("st.volatile.global.v2.u32 [%0], {%1, %2};" ::"l"(slot + i), "r"(w[j]), "r"(d.seq) : "memory");
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1043,20 +1068,29 @@ __global__ void __launch_bounds__(256) iccl_ll_group(LLBatch b) {
         asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(d.done_flag), "r"(d.done_gen) : "memory");
     }
   } else {
-    for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-      uint32_t w, f;
-      do {
-        asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(w), "=r"(f) : "l"(slot + i) : "memory");
-        if (f != d.seq && ll_timed_out(t0)) {
-          *b.error = 1;
-          break;
+    // kLLUnroll lines polled at once (their first loads in flight together);
+    // a line not there yet is re-polled on its own
+    for (size_t i0 = lo + threadIdx.x; i0 < hi; i0 += kLLUnroll * blockDim.x) {
+      uint32_t w[kLLUnroll], f[kLLUnroll];
+#pragma unroll
+      for (int j = 0; j < kLLUnroll; j++) {
+        const size_t i = i0 + (size_t)j * blockDim.x;
+        f[j] = d.seq;
+        if (i < hi)
+          asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(w[j]), "=r"(f[j]) : "l"(slot + i) : "memory");
+      }
+#pragma unroll
+      for (int j = 0; j < kLLUnroll; j++) {
+        const size_t i = i0 + (size_t)j * blockDim.x;
+        if (i >= hi) continue;
+        while (f[j] != d.seq) {
+          if (ll_timed_out(t0)) {
+            *b.error = 1;
+            break;
+          }
+          asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(w[j]), "=r"(f[j]) : "l"(slot + i) : "memory");
         }
-      } while (f != d.seq);
-      const size_t off = i * 4;
-      if (off + 4 <= d.bytes && ((uintptr_t)(d.buf + off) & 3) == 0) {
-        *(uint32_t*)(d.buf + off) = w;
-      } else {
-        for (int k = 0; k < 4 && off + k < d.bytes; k++) d.buf[off + k] = (char)(w >> (8 * k));
+        ll_store_word(d.buf, d.bytes, i, w[j]);
       }
     }
     __syncthreads();
