@@ -155,8 +155,8 @@ constexpr int kLLSlots = 4;                 // slots per ordered pair (flow-cont
 constexpr size_t kLLMaxBytes = 256 * 1024;  // largest LL message
 constexpr size_t kLLLines = kLLMaxBytes / 4;
 constexpr int kLLMaxOps = 64;               // LL ops per launch
-constexpr int kLLMaxBlk = 16;               // CTAs per op
-constexpr size_t kLLLinesPerBlk = 2048;     // 8 lines per thread at 256 threads
+constexpr int kLLMaxBlk = 64;               // CTAs per op (16 -> 64: 256 KiB 18.3 -> 27.3 GB/s, profiles/r02)
+constexpr size_t kLLLinesPerBlk = 1024;     // 4 lines per thread at 256 threads
 constexpr int kLLMaxBlocksPerLaunch = 1024;
 constexpr int kLLCounters = 4096;           // per-op arrival counters (ring)
 struct LLDesc {
