@@ -152,7 +152,7 @@ cudaError_t preload_kernels();
 // (per-op arrival counter, reset by that CTA) writes its done flag and, on
 // the receive side, returns the slot's credit.
 constexpr int kLLSlots = 4;                 // slots per ordered pair (flow-control window)
-constexpr size_t kLLMaxBytes = 256 * 1024;  // largest LL message
+constexpr size_t kLLMaxBytes = 1024 * 1024;  // largest LL message (the slot ring holds it; sm_small_bytes routes)
 constexpr size_t kLLLines = kLLMaxBytes / 4;
 constexpr int kLLMaxOps = 64;               // LL ops per launch
 constexpr int kLLMaxBlk = 64;               // CTAs per op (16 -> 64: 256 KiB 18.3 -> 27.3 GB/s, profiles/r02)
