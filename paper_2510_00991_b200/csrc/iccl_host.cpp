@@ -105,7 +105,7 @@ iccl_result_t iccl_config_init(iccl_config_t* c) {
   c->retry_count = 7;            // ICCL_IB_RETRY_CNT 7 (Table 5)
   c->delta_us = 2000;            // NVLink-scale watchdog
   c->probe_period_us = 500;      // monitor_failed_link period
-  c->sm_small_bytes = 256 * 1024;  // AUTO: <= 256 KiB between GPUs takes the LL kernel path (K5): 8-16 us vs ~21 us on the copy-engine chain
+  c->sm_small_bytes = 1024 * 1024;  // AUTO: <= 1 MiB between GPUs takes the LL kernel path (K5): 8.7-15.5 us (K6 at 1 MiB: 18.9 us)
   c->proxy_cpu = -1;
   c->relay_slot_mib = 32;        // relay backup: 2 x 32 MiB staging per source on the relay GPU
   c->direct_max_kib = 16 * 1024; // AUTO: 256 KiB < n <= 16 MiB take the direct SM path (K6): 18-40 us vs 22-48 us on the copy-engine chain

@@ -130,7 +130,7 @@ def test_path_selection_defaults_and_overrides():
     <= 16 MiB < copy engines; relay staging 32 MiB; each an ICCL_* knob."""
     import paper_2510_00991_b200 as p
     d = p.IcclConfig.defaults()
-    assert (d.sm_small_bytes, d.direct_max_kib, d.relay_slot_mib, d.backup_kind) == (256 * 1024, 16 * 1024, 32, "sm")
+    assert (d.sm_small_bytes, d.direct_max_kib, d.relay_slot_mib, d.backup_kind) == (1024 * 1024, 16 * 1024, 32, "sm")
     code = ("import paper_2510_00991_b200 as p; c=p.IcclConfig.defaults(); "
             "print(c.sm_small_bytes, c.direct_max_kib, c.relay_slot_mib, c.backup_kind)")
     env = dict(os.environ, ICCL_SM_SMALL_BYTES="4096", ICCL_DIRECT_MAX_KIB="0", ICCL_RELAY_SLOT_MIB="8",
