@@ -67,6 +67,9 @@ for STEP in "$@"; do
     gemmk7) for V in "X=0" "ICCL_K7_CE=1" "ICCL_K7_CE=1 ICCL_K7_READY=1" "X=0"; do echo "## $V" >> "$LOG"
               env $V timeout 600 $TR --nproc-per-node $NG --master-port 29720 benchmarks/gemm_interference.py --impl iccl-ce >> "$LOG" 2>&1
             done ;;
+    gemm1) for I in iccl-auto nccl; do for M in 0.25 1; do echo "## $I $M" >> "$LOG"
+             timeout 600 $TR --nproc-per-node $NG --master-port 29750 benchmarks/gemm_interference.py --impl $I --msg-mib $M >> "$LOG" 2>&1
+           done; done ;;
     failcaps) for C in 16 32 64; do echo "## sm_cap $C" >> "$LOG"
                 ICCL_SM_CAP=$C timeout 600 $TR --nproc-per-node $NG --master-port 2969$((C % 7)) benchmarks/failover.py >> "$LOG" 2>&1
                 ICCL_SM_CAP=$C timeout 600 $TR --nproc-per-node $NG --master-port 2969$((C % 7 + 1)) benchmarks/failover.py --chunk-mib 32 >> "$LOG" 2>&1
